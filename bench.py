@@ -1,0 +1,402 @@
+"""Benchmark of the time-step hot path (BASELINE.json metric: M element-steps/s).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3] [--impl native|reference]
+
+A "step" is one full fractional time step (3 x K2+K3, K4, PCG with a fixed
+50 iterations, K6, K7) over the whole mesh; the unit of work is one element
+through one step.  N = 1 runs BASELINE configs[1] (C2: jittered Kuhn TET04
+box, 88^3 cells = 4,088,832 elements).  N > 1 (torchrun, one rank per GPU,
+NCCL) runs weak scaling: an (88 N) x 88 x 88 box split by the SFC partitioner
+into N subdomains of ~4.09M elements with NCCL interface sums.
+
+Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
+on the launching stream, with a 512 MB L2 flush (untimed) between steps;
+barrier + synchronize on both sides; max over ranks.  The per-kernel
+breakdown and roofline come from one instrumented (eager) step afterwards.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CG_ITERS = 50
+DT = 1e-3
+L2_FLUSH_BYTES = 512 << 20
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--cg-iters", type=int, default=CG_ITERS)
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-windows", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def build_workload(name: str, n_ranks: int):
+    from paper_2005_05899_b200 import meshgen
+    if name == "c2":
+        n = 88
+        mesh = meshgen.box_tets(n * n_ranks, n, n, lengths=(float(n_ranks), 1.0, 1.0), jitter=0.2, seed=20200131)
+        u, p = meshgen.c2_initial(mesh.coords)
+        bc = dict(p_fixed=meshgen.boundary_nodes(mesh))
+        params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
+        desc = {"workload": "C2: jittered Kuhn TET04 box (BASELINE configs[1])", "cells": [n * n_ranks, n, n],
+                "elements": mesh.n_elements, "nodes": mesh.n_nodes, "kinds": {"tet4": mesh.n_elements}}
+    else:
+        scale = n_ranks ** (1.0 / 3.0)
+        mesh = meshgen.c3_mesh(scale)
+        u = np.zeros((mesh.n_nodes, 3))
+        u[:, 0] = 1.0
+        p = np.zeros(mesh.n_nodes)
+        bc = meshgen.channel_bcs(mesh)
+        params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
+        desc = {"workload": "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2])",
+                "elements": mesh.n_elements, "nodes": mesh.n_nodes,
+                "kinds": {r: int(c.shape[0]) for r, c in mesh.conn.items()}}
+    return mesh, u, p, bc, params, desc
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int):
+    """Compulsory bytes (and flops for K2) per launch, layout-independent
+    (SURVEY §8(d)): int32 indices, fp64 values."""
+    from paper_2005_05899_b200.meshgen import NODE_COUNT, RULE_KIND
+    conn_bytes = sum(4 * NODE_COUNT[RULE_KIND[r]] * e for r, e in counts.items())
+    N = n_nodes
+    if kernel == "K5_cg_spmv":      # vals+cols, z & p_old (gathered once), p_new & q writes
+        return 12 * nnz + 32 * N, 2 * nnz + 3 * N
+    if kernel == "K5_cg_update":    # x p r q dinv in, x r z out
+        return 64 * N, 10 * N
+    if kernel == "K2_momentum":     # conn, coords, u in; rhs out
+        return conn_bytes + 48 * N + 24 * N, sum(FLOPS_K2.get(r, 0) * e for r, e in counts.items())
+    if kernel == "K3_rk_stage":     # u0 uprev rhs gp in (24 B each), minv, uout + rhs zero out
+        return 4 * 24 * N + 8 * N + 48 * N, 12 * N
+    if kernel == "K4_divergence":
+        return conn_bytes + 48 * N + 8 * N, 0
+    if kernel == "K6_gradient":
+        return conn_bytes + 24 * N + 8 * N + 24 * N, 0
+    if kernel == "K7_correct":
+        return 24 * 3 * N + 8 * N + 16 * N + 24 * 3 * N, 6 * N
+    return 0, 0
+
+
+# flops per element of K2 as written in the kernel (DESIGN.md §4.1 counts)
+FLOPS_K2 = {"tet4": 640, "tet1": 520}
+
+
+def load_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6650.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def load_traffic():
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text())
+        except Exception:
+            return {}
+    return {}
+
+
+def cpu_baseline_sample(steps: int = 2):
+    """Oracle port (numpy, 1 thread) on a bounded sample of the C2 workload."""
+    from threadpoolctl import threadpool_limits
+    from oracle import fem
+    from paper_2005_05899_b200 import meshgen
+    with threadpool_limits(1):
+        m = meshgen.box_tets(24, 24, 24, jitter=0.2, seed=20200131)
+        u, p = meshgen.c2_initial(m.coords)
+        o = fem.FlowOracle(m, 1.0, 1e-3, 0.07, p_fixed=meshgen.boundary_nodes(m))
+        st = o.init_state(u, p)
+        st = o.step(st, DT, cg_iters=CG_ITERS)  # warm-up
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            st = o.step(st, DT, cg_iters=CG_ITERS)
+        dt = time.perf_counter() - t0
+    return {"value": m.n_elements * steps / dt / 1e6, "unit": "M element-steps/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/fem.py FlowOracle, jittered Kuhn TET04 24^3 cells ({m.n_elements} elements), "
+                      f"{steps} full steps (CG {CG_ITERS} it), numpy single thread"}
+
+
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2005_05899_b200 import _lib
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+
+    ws, rank, local = dist_env()
+    if args.gpus != ws and ws > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ws}")
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    mesh, u, p, bc, params, desc = build_workload(args.workload, ws)
+    halo = own = None
+    n_elem_total = mesh.n_elements
+    if ws > 1:
+        from paper_2005_05899_b200.decompose import decompose
+        from paper_2005_05899_b200.halo import HaloExchanger
+        from paper_2005_05899_b200.partition import sfc_partition
+        parts, _cuts, subw = sfc_partition(mesh, ws, level=8)
+        sub, plan = decompose(mesh, parts, ws, rank)
+        l2g = plan.l2g
+        bc = {k: np.asarray(v)[l2g] for k, v in bc.items()}
+        u, p = u[l2g], p[l2g]
+        halo = HaloExchanger(plan, "cuda")
+        own = halo.own
+        local_mesh = sub
+    else:
+        local_mesh = mesh
+    solver = FlowSolver(local_mesh, FlowParams(**params), **bc, windows=not args.no_windows, reorder="sfc",
+                        halo=halo, own=own)
+    solver.set_state(u, p)
+    graph = (not args.no_graph) and ws == 1
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
+
+    for _ in range(args.warmup):
+        solver.step(DT, args.cg_iters, graph=graph)
+    torch.cuda.synchronize()
+
+    # launches of this library per step (eager count; graph replays the same)
+    c0 = _lib.launch_count()
+    solver._step_body(DT, args.cg_iters, 0.0) if not graph else solver.capture(DT, args.cg_iters)
+    torch.cuda.synchronize()
+    launches_per_step = (_lib.launch_count() - c0) // (2 if graph else 1)
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        solver.step(DT, args.cg_iters, graph=graph)
+        b.record()
+        b.synchronize()
+        total_ms += a.elapsed_time(b)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    value = n_elem_total * args.steps / (total_ms / 1e3) / 1e6
+
+    # end-to-end through the public API with host buffers
+    u_h = torch.empty((solver.n, 3), dtype=torch.float64, pin_memory=True)
+    p_h = torch.empty(solver.n, dtype=torch.float64, pin_memory=True)
+    u_h.copy_(solver.u)
+    p_h.copy_(solver.p)
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    e2e_ms = 0.0
+    for _ in range(args.steps):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        solver.step_host(u_h, p_h, DT, args.cg_iters, graph=graph)
+        b.record()
+        b.synchronize()
+        e2e_ms += a.elapsed_time(b)
+    te = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
+    if ws > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_ms = float(te.item())
+    bytes_io = (u_h.numel() + p_h.numel()) * 8
+
+    # instrumented eager step: per-kernel durations
+    solver.timeline = []
+    flush.fill_(1.0)
+    solver._step_body(DT, args.cg_iters, 0.0)
+    torch.cuda.synchronize()
+    per = {}
+    for name, a, b in solver.timeline:
+        per.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
+    solver.timeline = None
+    counts = solver.dm.element_counts()
+    nnz = solver.L.nnz
+    kern = {}
+    for name, ts in per.items():
+        B, F = algorithmic_cost(name, counts, solver.n, nnz)
+        avg = float(np.mean(ts))
+        kern[name] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
+                      "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,
+                      "gflops": F / avg / 1e9 if F and avg > 0 else None}
+    dom = max(kern, key=lambda k: kern[k]["total_ms"])
+    peak, peak_kind = load_peaks()
+    traffic = load_traffic().get(dom)
+    roof = {"kernel": dom, "bound": "hbm", "achieved": round(kern[dom]["gbs"], 1), "peak": peak, "unit": "GB/s",
+            "frac": round(kern[dom]["gbs"] / peak, 4), "peak_source": peak_kind,
+            "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
+
+    result = {
+        "metric": "M element-steps/s per time step (assembly + CG)", "value": round(value, 3),
+        "unit": "M element-steps/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": dict(desc, step="3x(K2+K3) + K4 + PCG(%d it, Jacobi) + K6 + K7" % args.cg_iters,
+                       cg_iters=args.cg_iters, dt=DT, physics=params, cuda_graph=graph,
+                       scatter="windowed" if not args.no_windows else "atomics",
+                       l2="flushed (512 MB write) between timed steps", parallelism=f"dd{ws}"),
+        "e2e": {"value": round(n_elem_total * args.steps / (e2e_ms / 1e3) / 1e6, 3), "unit": "M element-steps/s",
+                "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
+                "api": "FlowSolver.step_host (pinned host u,p -> step -> host)"},
+        "roofline": roof,
+        "kernels": {k: {kk: (round(vv, 3) if isinstance(vv, float) else vv) for kk, vv in v.items()}
+                    for k, v in kern.items()},
+        "gpu_launches": int(launches_per_step * args.steps),
+        "clocks": clk,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            result["cpu_baseline"] = cpu_baseline_sample()
+        except Exception as exc:  # pragma: no cover
+            result["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(result), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def _ref_worker(args):
+    steps, warmup, seed = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    from threadpoolctl import threadpool_limits
+    sys.path.insert(0, str(ROOT))
+    from oracle import fem
+    from paper_2005_05899_b200 import meshgen
+    with threadpool_limits(1):
+        m = meshgen.box_tets(20, 20, 20, jitter=0.2, seed=20200131 + seed)
+        u, p = meshgen.c2_initial(m.coords)
+        o = fem.FlowOracle(m, 1.0, 1e-3, 0.07, p_fixed=meshgen.boundary_nodes(m))
+        st = o.init_state(u, p)
+        for _ in range(warmup):
+            st = o.step(st, DT, cg_iters=CG_ITERS)
+        times = []
+        for _ in range(steps):
+            t0 = time.perf_counter()
+            st = o.step(st, DT, cg_iters=CG_ITERS)
+            times.append(time.perf_counter() - t0)
+    return m.n_elements, times
+
+
+def run_reference(args):
+    """Reference arm: the CPU restatement of the path (oracle port; the
+    reference package has no NS step to run), one single-threaded process per
+    host core, each stepping an independent replica of a bounded C2 sample."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = min(os.cpu_count() or 1, 64)
+    steps, warmup = max(1, min(args.steps, 3)), 1
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_ref_worker, [(steps, warmup, i) for i in range(cores)])
+    n_el = res[0][0]
+    per_step = [max(r[1][s] for r in res) for s in range(steps)]
+    value = n_el * cores * steps / sum(per_step) / 1e6
+    sample = (f"oracle/fem.py FlowOracle on {cores} processes x jittered Kuhn TET04 20^3 cells ({n_el} elements "
+              f"each), {steps} timed steps after {warmup} warm-up, full step with CG {CG_ITERS} it")
+    out = {"impl": "reference", "metric": "M element-steps/s per time step (assembly + CG)",
+           "value": round(value, 5), "unit": "M element-steps/s", "n_gpus": args.gpus, "steps": steps,
+           "warmup": warmup, "ms_per_step": round(1e3 * sum(per_step) / steps, 3), "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": "C2 sample (BASELINE configs[1] algorithm, bounded size)", "cg_iters": CG_ITERS,
+                      "parallelism": f"{cores} CPU processes"},
+           "cpu_baseline": {"value": round(value, 5), "unit": "M element-steps/s", "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": round(value, 5), "unit": "M element-steps/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_native(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,198 @@
+/*
+ * alyab200.h — C ABI of libalyab200.so, the B200 (sm_100a) hot path of the
+ * arXiv 2005.05899 (Alya) fractional-step explicit-RK FE Navier-Stokes step.
+ *
+ * The reference package (coexbal 0.1.0) is pure Python; its "operator API" is
+ * the set of functions listed against each entry point below.  Every entry
+ * point here replaces one of them (or one of the time-step pieces the paper
+ * describes and the reference leaves out) and is what a ctypes
+ * binding on the reference side would call.
+ *
+ * ABI rules
+ *  - plain C types only; every array argument is a DEVICE pointer owned by
+ *    the caller (PyTorch tensors in the Python package); no allocation inside
+ *    the launch functions except where documented;
+ *  - every function returns 0 on success or a negative AB_E* code; the
+ *    message is available from ab_last_error() (thread-local);
+ *  - `stream` is a cudaStream_t passed as void*; all work is asynchronous on
+ *    it, nothing synchronises the host;
+ *  - "accumulated" outputs are added into (fp64 atomics): the caller zeroes
+ *    them (the fused node kernels below re-zero the buffers they consume).
+ *
+ * Layouts: node vectors are [n_nodes][4] f64 (x,y,z,pad /
+ * u,v,w,pad) so one 256-bit load fetches a node; connectivity is int32
+ * [n_elem][nnode] per category in the reference's VTK node order.
+ */
+#ifndef ALYAB200_H
+#define ALYAB200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AB_OK 0
+#define AB_EINVAL (-1)
+#define AB_ECUDA (-2)
+#define AB_ENOMEM (-3)
+
+/* Integration rules (kernel template parameter).  Names and values follow
+ * reference assembly.py:89-117 (tet1, tet4, hex8) plus pyr5/pri6. */
+#define AB_RULE_TET1 0
+#define AB_RULE_TET4 1
+#define AB_RULE_PYR5 2
+#define AB_RULE_PRI6 3
+#define AB_RULE_HEX8 4
+
+typedef struct ab_category {
+  int32_t rule;          /* AB_RULE_* */
+  int32_t pad_;
+  int64_t n_elem;
+  const int32_t* conn;   /* [n_elem][nnode] */
+} ab_category;
+
+typedef struct ab_mesh {
+  int64_t n_nodes;
+  const double* coords;  /* [n_nodes][4] */
+  double period[3];      /* box length of periodic axes, 0 = not periodic */
+  int32_t n_cat;
+  int32_t pad_;
+  ab_category cat[5];
+} ab_mesh;
+
+typedef struct ab_phys {
+  double rho;            /* density */
+  double mu;             /* molecular viscosity */
+  double c_vreman;       /* Vreman constant, 0 disables the SGS model */
+} ab_phys;
+
+/* Sliced-ELL matrix, slice height 32. */
+typedef struct ab_sell {
+  int64_t n_rows;
+  int64_t n_slices;
+  const int64_t* slice_ptr;  /* [n_slices+1], offsets in entries */
+  const int32_t* cols;       /* [slice_ptr[n_slices]], lane-innermost; padding col = row */
+  const double* vals;        /* same layout; padding 0 */
+} ab_sell;
+
+/* ---- housekeeping ------------------------------------------------------ */
+int ab_version(void);
+const char* ab_last_error(void);
+/* Number of kernels this library launched since load (evidence counter). */
+int64_t ab_launch_count(void);
+
+/* ---- K1: packed mass matrix + lumped mass -------------------------------
+ * Replaces build_packs' Jacobians + assemble_packs (reference
+ * assembly.py:129-141, :178-244) and scatter_global(...).row_sums()
+ * (assembly.py:306-333).  For category `cat`: Ae[e][i][j] =
+ * sum_g |detJ|_g w_g N_i N_j (Gauss ascending), J[e][g] = |detJ|_g, and
+ * ml[node] += sum_j Ae[e][i][j].  Each output pointer may be NULL.
+ * `tile` = elements per CTA (the pack size of the reference, <= 1024). */
+int ab_mass(const ab_mesh* mesh, int32_t cat, double* ae, double* jdet, double* ml,
+            int32_t tile, void* stream);
+
+/* Register node windows for the category whose connectivity pointer is
+ * `conn` (windowed scatter); blk_ptr == NULL clears them.
+ * block must be 128 (elements per CTA). */
+int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
+                   const int32_t* wptr, const uint16_t* wslot);
+
+/* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
+ * New entry point; rhs4 accumulated. */
+int ab_momentum_rhs(const ab_mesh* mesh, const ab_phys* phys, const double* u4, double* rhs4,
+                    void* stream);
+
+/* ---- K4: divergence  out[a] += scale * sum_e int N_a div(u) ------------- */
+int ab_divergence(const ab_mesh* mesh, const double* u4, double scale, double* out, void* stream);
+
+/* ---- K6: gradient  out4[a] += scale * sum_e int N_a grad(p) ------------- */
+int ab_gradient(const ab_mesh* mesh, const double* p, double scale, double* out4, void* stream);
+
+/* ---- Laplacian L_ab = int grad N_a . grad N_b ------------
+ * Values accumulated into a CSR whose pattern (row_ptr, sorted cols) the
+ * caller built from the connectivity. */
+int ab_laplacian_csr(const ab_mesh* mesh, const int64_t* row_ptr, const int32_t* cols, double* vals,
+                     void* stream);
+/* Dirichlet rows/cols -> identity (fixed[i] != 0), pattern kept. */
+int ab_csr_dirichlet(int64_t n_rows, const int64_t* row_ptr, const int32_t* cols, double* vals,
+                     const uint8_t* fixed, void* stream);
+/* CSR -> SELL-32 (slice_ptr prepared by the caller from per-slice widths). */
+int ab_csr_to_sell(int64_t n_rows, const int64_t* row_ptr, const int32_t* cols, const double* vals,
+                   const int64_t* slice_ptr, int32_t* sell_cols, double* sell_vals, double* diag,
+                   void* stream);
+/* y = A x */
+int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
+
+/* ---- K5: Jacobi-PCG kernels --------------------
+ * Workspace `w` = 8 vectors of n_rows doubles: x r z p0 p1 q dinv b (see
+ * DESIGN.md §4.3), `red` = 8 doubles of reduction results, `sc` = 8 doubles
+ * of solver scalars, `part` = partial-sum scratch (>= 2*ceil(n/256) doubles),
+ * `cnt` = 1 uint32 zero-initialised counter.  `own` (nullable) = per-row
+ * ownership weights for dot products of a decomposed domain.
+ *   init:  r = fixed ? 0 : b; b = 0; x = 0; z = dinv r; p_old = 0;
+ *          red[RZN] = r.z, red[RR] = r.r, sc[BB] = r.r, sc[RZ] = 0
+ *   spmv:  beta = sc[RZ] ? red[RZN]/sc[RZ] : 0;  p_new = z + beta p_old;
+ *          q = A p_new;  if dot: red[PQ] = p_new.q;  sc[RZ] = red[RZN]
+ *   dot:   red[PQ] = p.q; sc[RZ] = red[RZN]  (decomposed domains: spmv runs
+ *          with with_dot = 0, then the q interface sum, then dot)
+ *   update: alpha = red[PQ] ? sc[RZ]/red[PQ] : 0; x += alpha p; r -= alpha q;
+ *          z = dinv r; red[RZN] = r.z; red[RR] = r.r                      */
+#define AB_RED_RZN 0
+#define AB_RED_RR 1
+#define AB_RED_PQ 2
+#define AB_SC_RZ 0
+#define AB_SC_BB 1
+int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
+               double* x, double* r, double* z, double* p_old, const double* own, double* red, double* sc,
+               double* part, uint32_t* cnt, void* stream);
+int ab_cg_spmv(const ab_sell* a, const double* z, const double* p_old, double* p_new, double* q,
+               int32_t with_dot, const double* own, double* red, double* sc, double* part, uint32_t* cnt,
+               void* stream);
+int ab_cg_dot(int64_t n, const double* p, const double* q, const double* own, double* red, double* sc,
+              double* part, uint32_t* cnt, void* stream);
+/* sc[BB] = red[RR] (after the init sums are final / all-reduced) */
+int ab_cg_set_bb(double* red, double* sc, void* stream);
+int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r,
+                 double* z, const double* own, double* red, const double* sc, double* part, uint32_t* cnt,
+                 void* stream);
+
+/* ---- K3: fused RK stage update (one HBM pass) -------------
+ *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */
+int ab_rk_stage(int64_t n, double a, double b, double k, const double* u0, const double* uprev,
+                double* rhs, const double* gp, const double* minv, double* uout, void* stream);
+/* ---- K7: velocity correction + pressure increment --
+ *   uout = uin - k*minv*gd; p += dp; gp += gd; gd = 0.  (uin may == uout) */
+int ab_correct(int64_t n, double k, const double* uin, double* uout, double* gd, const double* minv,
+               double* p, const double* dp, double* gp, void* stream);
+/* Dirichlet velocity values on a node list: u4[idx[i]][c] = vals[i][c] where mask bit c set. */
+int ab_apply_velocity_bc(int64_t n_fixed, const int32_t* idx, const uint8_t* mask, const double* vals,
+                         double* u4, void* stream);
+/* minv = 1/ml */
+int ab_reciprocal(int64_t n, const double* in, double* out, void* stream);
+
+/* Ordered segmented sum out[s] = sum_{k in [seg_ptr[s], seg_ptr[s+1])} vals[k],
+ * left to right: the global COO accumulation of scatter_global
+ * (reference assembly.py:317-333) done bit-exactly on the device. */
+int ab_segment_sum(int64_t n_seg, const int64_t* seg_ptr, const double* vals, double* out, void* stream);
+
+/* ---- interface halo ------------------------
+ * pack:   buf[i*ncomp + c] = field[idx[i]*stride + c]
+ * unpack: field[idx[i]*stride + c] += buf[i*ncomp + c]                    */
+int ab_halo_pack(int64_t n, const int32_t* idx, const double* field, int32_t stride, int32_t ncomp,
+                 double* buf, void* stream);
+int ab_halo_unpack_add(int64_t n, const int32_t* idx, const double* buf, int32_t stride, int32_t ncomp,
+                       double* field, void* stream);
+
+/* ---- decomposition (reference mesh.py:371-384, sfc.py:114-148, :184-192) -
+ * centroid[e] = (sum_a x_a)/nnode in node order (matches numpy mean);
+ * keys = Hilbert index of floor((c - lo)/span * 2^level) clipped.         */
+int ab_centroids(const ab_mesh* mesh, int32_t cat, double* out, void* stream);
+int ab_hilbert_keys(int64_t n, const double* centroids, const double* lo, const double* span,
+                    int32_t level, int64_t* keys, void* stream);
+int ab_hilbert_cells(int64_t n, const int64_t* cells, int32_t level, int64_t* keys, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ALYAB200_H */

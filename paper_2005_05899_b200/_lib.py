@@ -1,0 +1,112 @@
+"""ctypes binding of libalyab200.so (include/alyab200.h).
+
+There is no fallback: if the shared object is missing or does not load, every
+entry point of the package raises.  ``call`` turns a negative status into a
+``RuntimeError`` carrying ``ab_last_error()``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libalyab200.so"
+
+RULE_ID = {"tet1": 0, "tet4": 1, "pyr5": 2, "pri6": 3, "hex8": 4}
+
+vp = C.c_void_p
+i32 = C.c_int32
+i64 = C.c_int64
+f64 = C.c_double
+
+
+class AbCategory(C.Structure):
+    _fields_ = [("rule", i32), ("pad_", i32), ("n_elem", i64), ("conn", vp)]
+
+
+class AbMesh(C.Structure):
+    _fields_ = [("n_nodes", i64), ("coords", vp), ("period", f64 * 3), ("n_cat", i32), ("pad_", i32),
+                ("cat", AbCategory * 5)]
+
+
+class AbPhys(C.Structure):
+    _fields_ = [("rho", f64), ("mu", f64), ("c_vreman", f64)]
+
+
+class AbSell(C.Structure):
+    _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cols", vp), ("vals", vp)]
+
+
+P = C.POINTER
+_SIGS = {
+    "ab_version": ([], C.c_int),
+    "ab_last_error": ([], C.c_char_p),
+    "ab_launch_count": ([], i64),
+    "ab_set_windows": ([vp, i32, vp, vp, vp, vp], C.c_int),
+    "ab_mass": ([P(AbMesh), i32, vp, vp, vp, i32, vp], C.c_int),
+    "ab_momentum_rhs": ([P(AbMesh), P(AbPhys), vp, vp, vp], C.c_int),
+    "ab_divergence": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
+    "ab_gradient": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
+    "ab_laplacian_csr": ([P(AbMesh), vp, vp, vp, vp], C.c_int),
+    "ab_csr_dirichlet": ([i64, vp, vp, vp, vp, vp], C.c_int),
+    "ab_csr_to_sell": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
+    "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
+    "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),
+    "ab_reciprocal": ([i64, vp, vp, vp], C.c_int),
+    "ab_halo_pack": ([i64, vp, vp, i32, i32, vp, vp], C.c_int),
+    "ab_halo_unpack_add": ([i64, vp, vp, i32, i32, vp, vp], C.c_int),
+    "ab_segment_sum": ([i64, vp, vp, vp, vp], C.c_int),
+    "ab_centroids": ([P(AbMesh), i32, vp, vp], C.c_int),
+    "ab_hilbert_keys": ([i64, vp, vp, vp, i32, vp, vp], C.c_int),
+    "ab_hilbert_cells": ([i64, vp, i32, vp, vp], C.c_int),
+}
+
+EXPORTED = tuple(_SIGS)
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CDLL; raises if the library is missing."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"{LIB_PATH} is missing: run `python -m paper_2005_05899_b200.build` "
+                               "(there is no CPU fallback)")
+        dll = C.CDLL(str(LIB_PATH))
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(dll, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = dll
+    return _lib
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(lib(), name)(*args)
+    if rc != 0:
+        msg = lib().ab_last_error().decode(errors="replace")
+        raise RuntimeError(f"{name} failed ({rc}): {msg}")
+
+
+def launch_count() -> int:
+    return int(lib().ab_launch_count())
+
+
+def ptr(t) -> int | None:
+    """Raw device pointer of a tensor (None -> NULL)."""
+    if t is None:
+        return None
+    return t.data_ptr()
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = torch.cuda.current_stream() if stream is None else stream
+    return s.cuda_stream

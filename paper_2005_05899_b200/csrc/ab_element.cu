@@ -1,0 +1,765 @@
+// Element-loop kernels: K1 mass/lumped mass, K2 momentum RHS, K4 divergence,
+// K6 gradient, Laplacian values, centroids.
+//
+// One thread per element (the reference's pack lane, assembly.py:235-243;
+// the CTA is the pack), gather -> Gauss loop -> scatter.
+// Two scatter modes, chosen by measurement:
+//   * direct: fp64 reductions to global memory (REDG.E.ADD.F64) per node;
+//   * windowed: elements are processed in SFC-ordered blocks; each block
+//     writes its element contributions into shared-memory slots and then
+//     reduces them per unique node of the block's "node window" in a fixed
+//     order, issuing one global reduction per (block, node) instead of one
+//     per (element, node).
+#include "ab_common.cuh"
+#include "ab_tables.inc"
+
+namespace ab {
+
+template <int R> struct RuleT;
+template <> struct RuleT<AB_RULE_TET1> { static constexpr int NN = 4, NG = 1; static constexpr bool TET = true; };
+template <> struct RuleT<AB_RULE_TET4> { static constexpr int NN = 4, NG = 4; static constexpr bool TET = true; };
+template <> struct RuleT<AB_RULE_PYR5> { static constexpr int NN = 5, NG = 5; static constexpr bool TET = false; };
+template <> struct RuleT<AB_RULE_PRI6> { static constexpr int NN = 6, NG = 6; static constexpr bool TET = false; };
+template <> struct RuleT<AB_RULE_HEX8> { static constexpr int NN = 8, NG = 8; static constexpr bool TET = false; };
+
+// Kernel-side view of one category.
+struct CatP {
+  const double* __restrict__ coords;
+  const int32_t* __restrict__ conn;
+  int64_t n;
+  double L0, L1, L2;  // periods (0 = none)
+  int periodic;
+};
+
+// Node windows of a category (windowed scatter), see DESIGN.md §4.2.
+struct WinP {
+  const int64_t* __restrict__ blk_ptr;   // [n_blocks+1] offsets into wnode
+  const int32_t* __restrict__ wnode;     // window node ids
+  const int32_t* __restrict__ wptr;      // [n_win+1] offsets into wslot
+  const uint16_t* __restrict__ wslot;    // slot = local_elem*NN + a
+  int block;                             // elements per block (== blockDim.x)
+};
+
+template <int NN>
+__device__ __forceinline__ void load_conn(const int32_t* __restrict__ conn, int64_t e, int (&nd)[NN]) {
+  const int32_t* p = conn + e * NN;
+  if constexpr (NN == 4) {
+    int4 v = __ldg(reinterpret_cast<const int4*>(p));
+    nd[0] = v.x; nd[1] = v.y; nd[2] = v.z; nd[3] = v.w;
+  } else if constexpr (NN == 8) {
+    int4 v = __ldg(reinterpret_cast<const int4*>(p));
+    int4 w = __ldg(reinterpret_cast<const int4*>(p) + 1);
+    nd[0] = v.x; nd[1] = v.y; nd[2] = v.z; nd[3] = v.w;
+    nd[4] = w.x; nd[5] = w.y; nd[6] = w.z; nd[7] = w.w;
+  } else if constexpr (NN == 6) {
+    const int2* q = reinterpret_cast<const int2*>(p);
+    int2 a = __ldg(q), b = __ldg(q + 1), c = __ldg(q + 2);
+    nd[0] = a.x; nd[1] = a.y; nd[2] = b.x; nd[3] = b.y; nd[4] = c.x; nd[5] = c.y;
+  } else {
+#pragma unroll
+    for (int a = 0; a < NN; ++a) nd[a] = __ldg(p + a);
+  }
+}
+
+template <int NN>
+__device__ __forceinline__ void load_coords(const CatP& c, const int (&nd)[NN], double (&x)[NN][3]) {
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    d4 v = ld4_nc(c.coords + 4 * (int64_t)nd[a]);
+    x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
+  }
+  if (c.periodic) {  // minimum-image unwrap relative to node 0
+    const double L[3] = {c.L0, c.L1, c.L2};
+#pragma unroll
+    for (int a = 1; a < NN; ++a)
+#pragma unroll
+      for (int d = 0; d < 3; ++d)
+        if (L[d] > 0.0) {
+          double rel = x[a][d] - x[0][d];
+          x[a][d] = x[0][d] + (rel - L[d] * rint(rel / L[d]));
+        }
+  }
+}
+
+template <int NN>
+__device__ __forceinline__ void load_vec(const double* __restrict__ f4, const int (&nd)[NN], double (&u)[NN][3]) {
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    d4 v = ld4_nc(f4 + 4 * (int64_t)nd[a]);
+    u[a][0] = v.x; u[a][1] = v.y; u[a][2] = v.z;
+  }
+}
+
+__device__ __forceinline__ double det3(const double (&m)[3][3]) {
+  return m[0][0] * (m[1][1] * m[2][2] - m[1][2] * m[2][1]) - m[0][1] * (m[1][0] * m[2][2] - m[1][2] * m[2][0]) +
+         m[0][2] * (m[1][0] * m[2][1] - m[1][1] * m[2][0]);
+}
+
+// inv = J^-1 (cofactor form); returns det J.
+__device__ __forceinline__ double inv3(const double (&m)[3][3], double (&iv)[3][3]) {
+  double c00 = m[1][1] * m[2][2] - m[1][2] * m[2][1];
+  double c01 = m[0][2] * m[2][1] - m[0][1] * m[2][2];
+  double c02 = m[0][1] * m[1][2] - m[0][2] * m[1][1];
+  double c10 = m[1][2] * m[2][0] - m[1][0] * m[2][2];
+  double c11 = m[0][0] * m[2][2] - m[0][2] * m[2][0];
+  double c12 = m[0][2] * m[1][0] - m[0][0] * m[1][2];
+  double c20 = m[1][0] * m[2][1] - m[1][1] * m[2][0];
+  double c21 = m[0][1] * m[2][0] - m[0][0] * m[2][1];
+  double c22 = m[0][0] * m[1][1] - m[0][1] * m[1][0];
+  double det = m[0][0] * c00 + m[0][1] * c10 + m[0][2] * c20;
+  double id = 1.0 / det;
+  iv[0][0] = c00 * id; iv[0][1] = c01 * id; iv[0][2] = c02 * id;
+  iv[1][0] = c10 * id; iv[1][1] = c11 * id; iv[1][2] = c12 * id;
+  iv[2][0] = c20 * id; iv[2][1] = c21 * id; iv[2][2] = c22 * id;
+  return det;
+}
+
+// J[i][j] = sum_a x_a,i dN_a/dxi_j at Gauss point g.
+template <int R, int NN>
+__device__ __forceinline__ void jacobian(const double (&x)[NN][3], int g, double (&J)[3][3]) {
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) s = fma(x[a][i], c_dN[R][g][a][j], s);
+      J[i][j] = s;
+    }
+}
+
+// Physical gradients of the shape functions at Gauss point g; returns det J.
+template <int R, int NN>
+__device__ __forceinline__ double shape_grads(const double (&x)[NN][3], int g, double (&dNdx)[NN][3]) {
+  double J[3][3], iv[3][3];
+  if constexpr (RuleT<R>::TET) {
+    // affine: J columns are the edges x_{j+1}-x_0; dN/dxi known in closed form
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) J[i][j] = x[j + 1][i] - x[0][i];
+    double det = inv3(J, iv);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      dNdx[1][k] = iv[0][k];
+      dNdx[2][k] = iv[1][k];
+      dNdx[3][k] = iv[2][k];
+      dNdx[0][k] = -(iv[0][k] + iv[1][k] + iv[2][k]);
+    }
+    return det;
+  } else {
+    jacobian<R, NN>(x, g, J);
+    double det = inv3(J, iv);
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int k = 0; k < 3; ++k)
+        dNdx[a][k] = c_dN[R][g][a][0] * iv[0][k] + c_dN[R][g][a][1] * iv[1][k] + c_dN[R][g][a][2] * iv[2][k];
+    return det;
+  }
+}
+
+// |det J| at Gauss point g with the reference's formulas (edge matrix for
+// tets, assembly.py:131-133 / :276-277; trilinear J for others, :135-139).
+template <int R, int NN>
+__device__ __forceinline__ double abs_det(const double (&x)[NN][3], int g) {
+  double J[3][3];
+  if constexpr (RuleT<R>::TET) {
+#pragma unroll
+    for (int r = 0; r < 3; ++r)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) J[r][c] = x[r + 1][c] - x[0][c];
+  } else {
+    jacobian<R, NN>(x, g, J);
+  }
+  return fabs(det3(J));
+}
+
+// Vreman eddy viscosity: mu_t = rho c sqrt(B_beta / a:a),
+// alpha_ij = du_j/dx_i = G_ji, beta = Delta^2 alpha^T alpha.
+__device__ __forceinline__ double vreman(const double (&G)[3][3], double delta2, double rho, double c) {
+  double b[3][3], aa = 0.0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < 3; ++m) s = fma(G[i][m], G[j][m], s);  // sum_m alpha_mi alpha_mj
+      b[i][j] = delta2 * s;
+      aa = fma(G[i][j], G[i][j], aa);
+    }
+  double B = b[0][0] * b[1][1] - b[0][1] * b[0][1] + b[0][0] * b[2][2] - b[0][2] * b[0][2] + b[1][1] * b[2][2] -
+             b[1][2] * b[1][2];
+  B = fmax(B, 0.0);
+  return aa > 1e-30 ? rho * c * sqrt(B / aa) : 0.0;
+}
+
+// ---------------------------------------------------------------------------
+// Scatter of per-element contributions r[NN][NC] to a [n][STRIDE] node array.
+// ---------------------------------------------------------------------------
+template <int NN, int NC, int STRIDE>
+__device__ __forceinline__ void scatter_direct(double* __restrict__ out, const int (&nd)[NN],
+                                               const double (&r)[NN][NC]) {
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) red_add(out + (int64_t)nd[a] * STRIDE + c, r[a][c]);
+}
+
+// Windowed scatter: every thread of the block must call it (contains
+// __syncthreads); invalid lanes pass zeros.
+template <int NN, int NC, int STRIDE, int BLOCK>
+__device__ __forceinline__ void scatter_window(double* __restrict__ out, const WinP& w, const double (&r)[NN][NC]) {
+  extern __shared__ double slots[];  // [BLOCK*NN][NC]
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) slots[(threadIdx.x * NN + a) * NC + c] = r[a][c];
+  __syncthreads();
+  const int64_t b0 = w.blk_ptr[blockIdx.x], b1 = w.blk_ptr[blockIdx.x + 1];
+  for (int64_t k = b0 + threadIdx.x; k < b1; k += BLOCK) {
+    const int node = __ldg(w.wnode + k);
+    const int s0 = __ldg(w.wptr + k), s1 = __ldg(w.wptr + k + 1);
+    double acc[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) acc[c] = 0.0;
+    for (int s = s0; s < s1; ++s) {
+      const int slot = __ldg(w.wslot + s);
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] += slots[slot * NC + c];
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) red_add(out + (int64_t)node * STRIDE + c, acc[c]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K1: mass matrix / Jacobians / lumped mass
+// ---------------------------------------------------------------------------
+template <int R>
+__global__ void k_mass(CatP c, double* __restrict__ ae, double* __restrict__ jdet, double* __restrict__ ml) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.n) return;
+  int nd[NN];
+  load_conn<NN>(c.conn, e, nd);
+  double x[NN][3];
+  load_coords<NN>(c, nd, x);
+  double m[NN][NN];
+#pragma unroll
+  for (int i = 0; i < NN; ++i)
+#pragma unroll
+    for (int j = 0; j < NN; ++j) m[i][j] = 0.0;
+  double dtet = RuleT<R>::TET ? abs_det<R, NN>(x, 0) : 0.0;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    const double J = RuleT<R>::TET ? dtet : abs_det<R, NN>(x, g);
+    if (jdet) jdet[e * NG + g] = J;
+    const double jw = J * c_w[R][g];
+#pragma unroll
+    for (int i = 0; i < NN; ++i)
+#pragma unroll
+      for (int j = 0; j < NN; ++j) m[i][j] += jw * (c_N[R][g][i] * c_N[R][g][j]);
+  }
+  if (ae) {
+    double* o = ae + e * NN * NN;
+#pragma unroll
+    for (int i = 0; i < NN; ++i)
+#pragma unroll
+      for (int j = 0; j < NN; ++j) o[i * NN + j] = m[i][j];
+  }
+  if (ml) {
+#pragma unroll
+    for (int i = 0; i < NN; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int j = 0; j < NN; ++j) s += m[i][j];
+      red_add(ml + nd[i], s);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: momentum RHS  R_a -= int rho N_a [2 eps(u) u + div(u) u] + 2 (mu+mu_t) eps : grad N_a
+// ---------------------------------------------------------------------------
+template <int R, int NN>
+__device__ __forceinline__ void momentum_element(const CatP& c, const ab_phys ph, const double* __restrict__ u4,
+                                                 int64_t e, int (&nd)[NN], double (&r)[NN][3]) {
+  constexpr int NG = RuleT<R>::NG;
+  load_conn<NN>(c.conn, e, nd);
+  double x[NN][3], u[NN][3];
+  load_coords<NN>(c, nd, x);
+  load_vec<NN>(u4, nd, u);
+#pragma unroll
+  for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
+
+  if constexpr (RuleT<R>::TET) {
+    double dNdx[NN][3];
+    const double det = shape_grads<R, NN>(x, 0, dNdx);
+    const double adet = fabs(det);
+    double wsum = 0.0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) wsum += c_w[R][g];
+    const double vol = adet * wsum;
+    double G[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        double s = 0.0;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) s = fma(u[a][i], dNdx[a][j], s);
+        G[i][j] = s;
+      }
+    const double div = G[0][0] + G[1][1] + G[2][2];
+    double mu_eff = ph.mu;
+    if (ph.c_vreman > 0.0) {
+      const double d = cbrt(vol);
+      mu_eff += vreman(G, d * d, ph.rho, ph.c_vreman);
+    }
+    // A = G + G^T + div I  (c = A u_g);  sigma = 2 mu_eff eps V
+    double A[3][3], sg[3][3];
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const double s = G[i][j] + G[j][i];
+        A[i][j] = s + (i == j ? div : 0.0);
+        sg[i][j] = mu_eff * s * vol;  // 2 mu eps_ij vol
+      }
+    // m_a = sum_g w_g N_a(g) u_g   (convective term is linear in u_g here)
+    double mv[NN][3];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) mv[a][0] = mv[a][1] = mv[a][2] = 0.0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      double ug[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int b = 0; b < NN; ++b)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ug[i] = fma(c_N[R][g][b], u[b][i], ug[i]);
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        const double wn = c_w[R][g] * c_N[R][g][a];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) mv[a][i] = fma(wn, ug[i], mv[a][i]);
+      }
+    }
+    const double rdet = ph.rho * adet;
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double cv = A[i][0] * mv[a][0] + A[i][1] * mv[a][1] + A[i][2] * mv[a][2];
+        double vs = sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
+        r[a][i] = -(rdet * cv + vs);
+      }
+  } else {
+    double delta2 = 0.0;
+    if (ph.c_vreman > 0.0) {
+      double vol = 0.0;
+#pragma unroll
+      for (int g = 0; g < NG; ++g) vol += abs_det<R, NN>(x, g) * c_w[R][g];
+      const double d = cbrt(vol);
+      delta2 = d * d;
+    }
+#pragma unroll 1
+    for (int g = 0; g < NG; ++g) {
+      double dNdx[NN][3];
+      const double dV = fabs(shape_grads<R, NN>(x, g, dNdx)) * c_w[R][g];
+      double ug[3] = {0.0, 0.0, 0.0}, G[3][3];
+#pragma unroll
+      for (int b = 0; b < NN; ++b)
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ug[i] = fma(c_N[R][g][b], u[b][i], ug[i]);
+#pragma unroll
+      for (int i = 0; i < 3; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          double s = 0.0;
+#pragma unroll
+          for (int a = 0; a < NN; ++a) s = fma(u[a][i], dNdx[a][j], s);
+          G[i][j] = s;
+        }
+      const double div = G[0][0] + G[1][1] + G[2][2];
+      double mu_eff = ph.mu;
+      if (ph.c_vreman > 0.0) mu_eff += vreman(G, delta2, ph.rho, ph.c_vreman);
+      double cv[3], sg[3][3];
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        double s = div * ug[i];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const double e2 = G[i][j] + G[j][i];
+          s = fma(e2, ug[j], s);
+          sg[i][j] = mu_eff * e2 * dV;
+        }
+        cv[i] = ph.rho * dV * s;
+      }
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int i = 0; i < 3; ++i)
+          r[a][i] -= c_N[R][g][a] * cv[i] + sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
+    }
+  }
+}
+
+template <int R, int BLOCK, bool WIN>
+__global__ void __launch_bounds__(BLOCK) k_momentum(CatP c, ab_phys ph, const double* __restrict__ u4,
+                                                    double* __restrict__ rhs4, WinP w) {
+  constexpr int NN = RuleT<R>::NN;
+  const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  int nd[NN];
+  double r[NN][3];
+  if (e < c.n) {
+    momentum_element<R, NN>(c, ph, u4, e, nd, r);
+    if constexpr (!WIN) scatter_direct<NN, 3, 4>(rhs4, nd, r);
+  } else {
+#pragma unroll
+    for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
+  }
+  if constexpr (WIN) scatter_window<NN, 3, 4, BLOCK>(rhs4, w, r);
+}
+
+// ---------------------------------------------------------------------------
+// K4 divergence / K6 gradient  (int N_a div u, int N_a grad p)
+// ---------------------------------------------------------------------------
+template <int R, int BLOCK, bool WIN>
+__global__ void __launch_bounds__(BLOCK) k_divergence(CatP c, const double* __restrict__ u4, double scale,
+                                                      double* __restrict__ out, WinP w) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  int nd[NN];
+  double r[NN][1];
+#pragma unroll
+  for (int a = 0; a < NN; ++a) r[a][0] = 0.0;
+  if (e < c.n) {
+    load_conn<NN>(c.conn, e, nd);
+    double x[NN][3], u[NN][3];
+    load_coords<NN>(c, nd, x);
+    load_vec<NN>(u4, nd, u);
+#pragma unroll 1
+    for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+      double dNdx[NN][3];
+      const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
+      double div = 0.0;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) div += u[a][0] * dNdx[a][0] + u[a][1] * dNdx[a][1] + u[a][2] * dNdx[a][2];
+      if constexpr (RuleT<R>::TET) {
+#pragma unroll
+        for (int gg = 0; gg < NG; ++gg) {
+          const double f = scale * adet * c_w[R][gg] * div;
+#pragma unroll
+          for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][gg][a], f, r[a][0]);
+        }
+      } else {
+        const double f = scale * adet * c_w[R][g] * div;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][g][a], f, r[a][0]);
+      }
+    }
+    if constexpr (!WIN) scatter_direct<NN, 1, 1>(out, nd, r);
+  }
+  if constexpr (WIN) scatter_window<NN, 1, 1, BLOCK>(out, w, r);
+}
+
+template <int R, int BLOCK, bool WIN>
+__global__ void __launch_bounds__(BLOCK) k_gradient(CatP c, const double* __restrict__ p, double scale,
+                                                    double* __restrict__ out4, WinP w) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
+  int nd[NN];
+  double r[NN][3];
+#pragma unroll
+  for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
+  if (e < c.n) {
+    load_conn<NN>(c.conn, e, nd);
+    double x[NN][3], pe[NN];
+    load_coords<NN>(c, nd, x);
+#pragma unroll
+    for (int a = 0; a < NN; ++a) pe[a] = __ldg(p + nd[a]);
+#pragma unroll 1
+    for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+      double dNdx[NN][3];
+      const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
+      double gp[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int k = 0; k < 3; ++k) gp[k] = fma(pe[a], dNdx[a][k], gp[k]);
+#pragma unroll
+      for (int gg = 0; gg < (RuleT<R>::TET ? NG : 1); ++gg) {
+        const int gi = RuleT<R>::TET ? gg : g;
+        const double f = scale * adet * c_w[R][gi];
+#pragma unroll
+        for (int a = 0; a < NN; ++a) {
+          const double fn = f * c_N[R][gi][a];
+#pragma unroll
+          for (int k = 0; k < 3; ++k) r[a][k] = fma(fn, gp[k], r[a][k]);
+        }
+      }
+    }
+    if constexpr (!WIN) scatter_direct<NN, 3, 4>(out4, nd, r);
+  }
+  if constexpr (WIN) scatter_window<NN, 3, 4, BLOCK>(out4, w, r);
+}
+
+// ---------------------------------------------------------------------------
+// Laplacian values into a CSR pattern (setup)
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int64_t csr_find(const int64_t* __restrict__ rp, const int32_t* __restrict__ cols, int row,
+                                            int col) {
+  int64_t lo = rp[row], hi = rp[row + 1] - 1;
+  while (lo <= hi) {
+    int64_t mid = (lo + hi) >> 1;
+    int v = cols[mid];
+    if (v == col) return mid;
+    if (v < col) lo = mid + 1; else hi = mid - 1;
+  }
+  return -1;
+}
+
+template <int R>
+__global__ void k_laplacian(CatP c, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                            double* __restrict__ vals) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.n) return;
+  int nd[NN];
+  load_conn<NN>(c.conn, e, nd);
+  double x[NN][3];
+  load_coords<NN>(c, nd, x);
+  double le[NN][NN];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) le[a][b] = 0.0;
+#pragma unroll 1
+  for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+    double dNdx[NN][3];
+    double dV = fabs(shape_grads<R, NN>(x, g, dNdx));
+    if constexpr (RuleT<R>::TET) {
+      double ws = 0.0;
+      for (int gg = 0; gg < NG; ++gg) ws += c_w[R][gg];
+      dV *= ws;
+    } else {
+      dV *= c_w[R][g];
+    }
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int b = 0; b < NN; ++b)
+        le[a][b] += dV * (dNdx[a][0] * dNdx[b][0] + dNdx[a][1] * dNdx[b][1] + dNdx[a][2] * dNdx[b][2]);
+  }
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) {
+      int64_t pos = csr_find(rp, cols, nd[a], nd[b]);
+      if (pos >= 0) red_add(vals + pos, le[a][b]);
+    }
+}
+
+// centroid = (sum_a x_a) / nnode, sequential in node order (numpy mean over
+// axis 0 of the (nnode,3) gather, reference mesh.py:375).
+template <int R>
+__global__ void k_centroids(CatP c, double* __restrict__ out) {
+  constexpr int NN = RuleT<R>::NN;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.n) return;
+  int nd[NN];
+  load_conn<NN>(c.conn, e, nd);
+  double s[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    d4 v = ld4_nc(c.coords + 4 * (int64_t)nd[a]);
+    s[0] = __dadd_rn(s[0], v.x);
+    s[1] = __dadd_rn(s[1], v.y);
+    s[2] = __dadd_rn(s[2], v.z);
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) out[e * 3 + d] = __ddiv_rn(s[d], (double)NN);
+}
+
+// ---------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------
+static CatP cat_params(const ab_mesh* m, int k) {
+  CatP c;
+  c.coords = m->coords;
+  c.conn = m->cat[k].conn;
+  c.n = m->cat[k].n_elem;
+  c.L0 = m->period[0];
+  c.L1 = m->period[1];
+  c.L2 = m->period[2];
+  c.periodic = (c.L0 > 0.0 || c.L1 > 0.0 || c.L2 > 0.0) ? 1 : 0;
+  return c;
+}
+
+static int valid_mesh(const ab_mesh* m) {
+  if (!m || !m->coords || m->n_cat < 0 || m->n_cat > 5) return fail("invalid ab_mesh");
+  for (int k = 0; k < m->n_cat; ++k) {
+    if (m->cat[k].rule < 0 || m->cat[k].rule > 4) return fail("invalid rule id in ab_mesh");
+    if (m->cat[k].n_elem > 0 && !m->cat[k].conn) return fail("null connectivity");
+  }
+  return AB_OK;
+}
+
+// Dispatch a functor templated on the rule id.
+template <class F>
+static int dispatch_rule(int rule, F&& f) {
+  switch (rule) {
+    case AB_RULE_TET1: return f(std::integral_constant<int, AB_RULE_TET1>{});
+    case AB_RULE_TET4: return f(std::integral_constant<int, AB_RULE_TET4>{});
+    case AB_RULE_PYR5: return f(std::integral_constant<int, AB_RULE_PYR5>{});
+    case AB_RULE_PRI6: return f(std::integral_constant<int, AB_RULE_PRI6>{});
+    case AB_RULE_HEX8: return f(std::integral_constant<int, AB_RULE_HEX8>{});
+  }
+  return fail("unknown rule");
+}
+
+static constexpr int kBlock = 128;
+
+// Windows are attached per category through ab_set_windows (host registry
+// keyed by the connectivity pointer, so the ab_mesh struct stays plain).
+struct WinEntry { const int32_t* conn; WinP w; };
+static WinEntry g_win[64];
+static int g_nwin = 0;
+
+static bool find_win(const int32_t* conn, WinP* out) {
+  for (int i = 0; i < g_nwin; ++i)
+    if (g_win[i].conn == conn) { *out = g_win[i].w; return true; }
+  return false;
+}
+
+}  // namespace ab
+
+using namespace ab;
+
+extern "C" {
+
+// Register (or clear with blk_ptr == NULL) the node windows of a category.
+int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
+                   const int32_t* wptr, const uint16_t* wslot) {
+  for (int i = 0; i < g_nwin; ++i)
+    if (g_win[i].conn == conn) {
+      if (!blk_ptr) { g_win[i] = g_win[--g_nwin]; return AB_OK; }
+      g_win[i].w = WinP{blk_ptr, wnode, wptr, wslot, block};
+      return AB_OK;
+    }
+  if (!blk_ptr) return AB_OK;
+  if (block != kBlock) return fail("ab_set_windows: block must be 128");
+  if (g_nwin >= 64) return fail("ab_set_windows: registry full");
+  g_win[g_nwin++] = WinEntry{conn, WinP{blk_ptr, wnode, wptr, wslot, block}};
+  return AB_OK;
+}
+
+int ab_mass(const ab_mesh* m, int32_t k, double* ae, double* jdet, double* ml, int32_t tile, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  if (k < 0 || k >= m->n_cat) return fail("ab_mass: category out of range");
+  if (tile < 1 || tile > 1024) return fail("ab_mass: tile must be in [1, 1024]");
+  CatP c = cat_params(m, k);
+  if (c.n == 0) return AB_OK;
+  return dispatch_rule(m->cat[k].rule, [&](auto r) {
+    k_mass<decltype(r)::value><<<grid_for(c.n, tile), tile, 0, S(stream)>>>(c, ae, jdet, ml);
+    return check_launch("ab_mass");
+  });
+}
+
+int ab_momentum_rhs(const ab_mesh* m, const ab_phys* ph, const double* u4, double* rhs4, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  if (!ph || !u4 || !rhs4) return fail("ab_momentum_rhs: null argument");
+  for (int k = 0; k < m->n_cat; ++k) {
+    CatP c = cat_params(m, k);
+    if (c.n == 0) continue;
+    WinP w{};
+    const bool win = find_win(c.conn, &w);
+    int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
+      constexpr int R = decltype(r)::value;
+      constexpr int NN = RuleT<R>::NN;
+      if (win) {
+        size_t sm = sizeof(double) * kBlock * NN * 3;
+        k_momentum<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sm, S(stream)>>>(c, *ph, u4, rhs4, w);
+      } else {
+        k_momentum<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, *ph, u4, rhs4, w);
+      }
+      return check_launch("ab_momentum_rhs");
+    });
+    if (rc) return rc;
+  }
+  return AB_OK;
+}
+
+int ab_divergence(const ab_mesh* m, const double* u4, double scale, double* out, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  for (int k = 0; k < m->n_cat; ++k) {
+    CatP c = cat_params(m, k);
+    if (c.n == 0) continue;
+    WinP w{};
+    const bool win = find_win(c.conn, &w);
+    int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
+      constexpr int R = decltype(r)::value;
+      constexpr int NN = RuleT<R>::NN;
+      if (win)
+        k_divergence<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sizeof(double) * kBlock * NN, S(stream)>>>(
+            c, u4, scale, out, w);
+      else
+        k_divergence<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, u4, scale, out, w);
+      return check_launch("ab_divergence");
+    });
+    if (rc) return rc;
+  }
+  return AB_OK;
+}
+
+int ab_gradient(const ab_mesh* m, const double* p, double scale, double* out4, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  for (int k = 0; k < m->n_cat; ++k) {
+    CatP c = cat_params(m, k);
+    if (c.n == 0) continue;
+    WinP w{};
+    const bool win = find_win(c.conn, &w);
+    int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
+      constexpr int R = decltype(r)::value;
+      constexpr int NN = RuleT<R>::NN;
+      if (win)
+        k_gradient<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sizeof(double) * kBlock * NN * 3,
+                                      S(stream)>>>(c, p, scale, out4, w);
+      else
+        k_gradient<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, p, scale, out4, w);
+      return check_launch("ab_gradient");
+    });
+    if (rc) return rc;
+  }
+  return AB_OK;
+}
+
+int ab_laplacian_csr(const ab_mesh* m, const int64_t* rp, const int32_t* cols, double* vals, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  for (int k = 0; k < m->n_cat; ++k) {
+    CatP c = cat_params(m, k);
+    if (c.n == 0) continue;
+    int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
+      k_laplacian<decltype(r)::value><<<grid_for(c.n, 128), 128, 0, S(stream)>>>(c, rp, cols, vals);
+      return check_launch("ab_laplacian_csr");
+    });
+    if (rc) return rc;
+  }
+  return AB_OK;
+}
+
+int ab_centroids(const ab_mesh* m, int32_t k, double* out, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  if (k < 0 || k >= m->n_cat) return fail("ab_centroids: category out of range");
+  CatP c = cat_params(m, k);
+  c.periodic = 0;  // the reference averages raw node coordinates
+  if (c.n == 0) return AB_OK;
+  return dispatch_rule(m->cat[k].rule, [&](auto r) {
+    k_centroids<decltype(r)::value><<<grid_for(c.n, 256), 256, 0, S(stream)>>>(c, out);
+    return check_launch("ab_centroids");
+  });
+}
+
+}  // extern "C"

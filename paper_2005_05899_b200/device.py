@@ -1,0 +1,167 @@
+"""Device-resident mesh: the HBM layout every kernel reads.
+
+* ``coords4``: f64 [N][4] (x, y, z, 0) — one 256-bit load per node;
+* per category: int32 connectivity [E_k][n_k] (reference VTK node order) and
+  the int64 global element ids of its rows;
+* optional SFC reordering of the elements of each category (Hilbert order of
+  the centroids), which makes consecutive elements spatially compact so
+  node gathers hit L2 and the node windows of the windowed scatter are small;
+* optional node windows (``ab_set_windows``) per category, built once on the
+  GPU with a stable sort of (block, node) keys.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import AbMesh, AbCategory, RULE_ID, call, ptr, stream_handle
+from .meshgen import MeshArrays, NODE_COUNT, RULE_KIND
+
+WINDOW_BLOCK = 128
+
+
+class DeviceMesh:
+    def __init__(self, mesh: MeshArrays, device="cuda", reorder: str | None = None, windows: bool = False):
+        if not torch.cuda.is_available():
+            raise RuntimeError("DeviceMesh needs a CUDA device (there is no CPU fallback)")
+        self.device = torch.device(device)
+        self.host = mesh
+        self.n_nodes = mesh.n_nodes
+        c4 = np.zeros((mesh.n_nodes, 4), dtype=np.float64)
+        c4[:, :3] = mesh.coords
+        self.coords4 = torch.from_numpy(c4).to(self.device)
+        self.period = np.asarray(mesh.period, dtype=np.float64)
+        self.rules, self.conn, self.ids = [], [], []
+        for _tag, rule, conn, ids in mesh.categories():
+            self.rules.append(rule)
+            self.conn.append(torch.from_numpy(np.ascontiguousarray(conn, dtype=np.int32)).to(self.device))
+            self.ids.append(torch.from_numpy(np.asarray(ids, dtype=np.int64)).to(self.device))
+        self._win = []
+        self._build_struct()
+        if reorder == "sfc":
+            self.reorder_sfc()
+        if windows:
+            self.build_windows()
+
+    # -- C struct -------------------------------------------------------------
+    def _build_struct(self):
+        m = AbMesh()
+        m.n_nodes = self.n_nodes
+        m.coords = ptr(self.coords4)
+        for d in range(3):
+            m.period[d] = float(self.period[d])
+        m.n_cat = len(self.rules)
+        for k, (rule, conn) in enumerate(zip(self.rules, self.conn)):
+            m.cat[k] = AbCategory(rule=RULE_ID[rule], pad_=0, n_elem=conn.shape[0], conn=ptr(conn))
+        self.struct = m
+
+    @property
+    def n_elements(self) -> int:
+        return int(sum(c.shape[0] for c in self.conn))
+
+    def element_counts(self):
+        return {r: int(c.shape[0]) for r, c in zip(self.rules, self.conn)}
+
+    def sub(self, k: int) -> AbMesh:
+        """ab_mesh restricted to category k (for per-category launches)."""
+        m = AbMesh()
+        m.n_nodes = self.n_nodes
+        m.coords = ptr(self.coords4)
+        for d in range(3):
+            m.period[d] = float(self.period[d])
+        m.n_cat = 1
+        m.cat[0] = self.struct.cat[k]
+        return m
+
+    # -- SFC ordering ---------------------------------------------------------
+    def centroids(self, k: int) -> torch.Tensor:
+        out = torch.empty((self.conn[k].shape[0], 3), dtype=torch.float64, device=self.device)
+        call("ab_centroids", C_ref(self.struct), k, ptr(out), stream_handle())
+        return out
+
+    def reorder_sfc(self, level: int = 10):
+        """Sort the elements of each category by the Hilbert key of their
+        centroid (stable, so ties keep generator order)."""
+        self.clear_windows()
+        cents = [self.centroids(k) for k in range(len(self.rules))]
+        allc = torch.cat(cents)
+        lo = allc.min(dim=0).values
+        hi = allc.max(dim=0).values
+        span = torch.clamp(hi - lo, min=1e-300) * (1 + 1e-12)
+        for k, c in enumerate(cents):
+            keys = torch.empty(c.shape[0], dtype=torch.int64, device=self.device)
+            call("ab_hilbert_keys", c.shape[0], ptr(c), ptr(lo), ptr(span), level, ptr(keys), stream_handle())
+            order = torch.sort(keys, stable=True).indices
+            self.conn[k] = self.conn[k][order].contiguous()
+            self.ids[k] = self.ids[k][order].contiguous()
+        self._build_struct()
+
+    # -- node windows ---------------------------------------------------------
+    def build_windows(self):
+        self.clear_windows()
+        B = WINDOW_BLOCK
+        N = self.n_nodes
+        for k, conn in enumerate(self.conn):
+            E, nn = conn.shape
+            if E == 0:
+                self._win.append(None)
+                continue
+            e = torch.arange(E, device=self.device, dtype=torch.int64)
+            blk = (e // B).repeat_interleave(nn)
+            slot = ((e % B) * nn).repeat_interleave(nn) + torch.arange(nn, device=self.device).repeat(E)
+            node = conn.reshape(-1).to(torch.int64)
+            key = blk * N + node
+            order = torch.sort(key, stable=True).indices
+            ks = key[order]
+            start = torch.ones_like(ks, dtype=torch.bool)
+            start[1:] = ks[1:] != ks[:-1]
+            starts = torch.nonzero(start).squeeze(1)
+            wnode = (ks[starts] % N).to(torch.int32).contiguous()
+            wblk = ks[starts] // N
+            wptr = torch.cat([starts, torch.tensor([ks.numel()], device=self.device)]).to(torch.int32).contiguous()
+            wslot = slot[order].to(torch.int16).contiguous()
+            nblk = (E + B - 1) // B
+            blk_ptr = torch.searchsorted(wblk, torch.arange(nblk + 1, device=self.device, dtype=torch.int64))
+            blk_ptr = blk_ptr.to(torch.int64).contiguous()
+            w = (blk_ptr, wnode, wptr, wslot)
+            self._win.append(w)
+            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot))
+        self.windows = True
+
+    def window_stats(self):
+        out = {}
+        for rule, conn, w in zip(self.rules, self.conn, self._win):
+            if w is None:
+                continue
+            out[rule] = {"refs": int(conn.numel()), "window_nodes": int(w[1].numel()),
+                         "reduction": float(conn.numel()) / max(1, int(w[1].numel()))}
+        return out
+
+    def clear_windows(self):
+        for conn, w in zip(self.conn, self._win):
+            if w is not None:
+                call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None)
+        self._win = []
+        self.windows = False
+
+    def __del__(self):
+        try:
+            self.clear_windows()
+        except Exception:
+            pass
+
+
+def C_ref(struct):
+    import ctypes
+    return ctypes.byref(struct)
+
+
+def nodes_as4(x: torch.Tensor) -> torch.Tensor:
+    """(N,3) -> contiguous (N,4) f64 with zero pad (no-op for (N,4))."""
+    if x.dim() == 2 and x.shape[1] == 4 and x.is_contiguous() and x.dtype == torch.float64:
+        return x
+    out = torch.zeros((x.shape[0], 4), dtype=torch.float64, device=x.device)
+    out[:, :3] = x[:, :3]
+    return out

@@ -1,0 +1,192 @@
+"""Pressure Laplacian and Jacobi-PCG — new entry points in the reference's
+style: ``assemble_laplacian(mesh) -> SellMatrix`` and
+``pcg_solve(A, b, x0, tol, max_it) -> (x, iters, res)``.
+
+The Laplacian L_ab = sum_e int grad N_a . grad N_b is assembled once
+(Algorithm 1 line 1): the CSR pattern comes from a GPU sort of
+the element (row, col) pairs, values from ``ab_laplacian_csr``, Dirichlet rows
+and columns become identity (``ab_csr_dirichlet``), and the matrix is stored
+as SELL-32 for the solver (``ab_csr_to_sell``).  The CG loop (PAPER.md:219,
+:329-330) is two fused kernels per iteration with all scalars on the device
+(``ab_cg_spmv`` + ``ab_cg_update``); in a decomposed domain the SpMV result
+is interface-summed and the dots all-reduced between them (DESIGN.md §4.3/§5).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import torch
+
+from ._lib import AbSell, call, ptr, stream_handle
+from .device import DeviceMesh
+
+
+@dataclass
+class SellMatrix:
+    n_rows: int
+    slice_ptr: torch.Tensor   # int64 [n_slices+1]
+    cols: torch.Tensor        # int32
+    vals: torch.Tensor        # f64
+    diag: torch.Tensor        # f64 [n_rows]
+    csr: tuple | None = None  # (row_ptr int64, cols int32, vals f64), kept for tests/export
+
+    def __post_init__(self):
+        self.struct = AbSell(n_rows=self.n_rows, n_slices=self.slice_ptr.numel() - 1,
+                             slice_ptr=ptr(self.slice_ptr), cols=ptr(self.cols), vals=ptr(self.vals))
+
+    @property
+    def nnz_stored(self) -> int:
+        return int(self.vals.numel())
+
+    @property
+    def nnz(self) -> int:
+        return int(self.csr[1].numel()) if self.csr is not None else -1
+
+    def matvec(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        y = torch.empty_like(x) if out is None else out
+        call("ab_sell_spmv", ctypes.byref(self.struct), ptr(x), ptr(y), stream_handle())
+        return y
+
+
+def csr_pattern(dm: DeviceMesh):
+    """Unique (row, col) pairs of all element node pairs, row-major sorted."""
+    N = dm.n_nodes
+    keys = []
+    for conn in dm.conn:
+        c = conn.to(torch.int64)
+        nn = c.shape[1]
+        rows = c.repeat_interleave(nn, dim=1).reshape(-1)
+        cols = c.repeat(1, nn).reshape(-1)
+        keys.append(torch.unique(rows * N + cols))
+    key = torch.unique(torch.cat(keys))
+    rows = key // N
+    cols = (key % N).to(torch.int32)
+    counts = torch.bincount(rows, minlength=N)
+    row_ptr = torch.zeros(N + 1, dtype=torch.int64, device=key.device)
+    row_ptr[1:] = torch.cumsum(counts, 0)
+    return row_ptr, cols.contiguous()
+
+
+def csr_to_sell(n: int, row_ptr, cols, vals) -> SellMatrix:
+    dev = vals.device
+    nnz_row = row_ptr[1:] - row_ptr[:-1]
+    n_slices = (n + 31) // 32
+    padded = torch.zeros(n_slices * 32, dtype=torch.int64, device=dev)
+    padded[:n] = nnz_row
+    width = padded.view(n_slices, 32).max(dim=1).values
+    slice_ptr = torch.zeros(n_slices + 1, dtype=torch.int64, device=dev)
+    slice_ptr[1:] = torch.cumsum(width * 32, 0)
+    total = int(slice_ptr[-1].item())
+    scols = torch.empty(total, dtype=torch.int32, device=dev)
+    svals = torch.empty(total, dtype=torch.float64, device=dev)
+    diag = torch.empty(n, dtype=torch.float64, device=dev)
+    call("ab_csr_to_sell", n, ptr(row_ptr), ptr(cols), ptr(vals), ptr(slice_ptr), ptr(scols), ptr(svals),
+         ptr(diag), stream_handle())
+    return SellMatrix(n_rows=n, slice_ptr=slice_ptr, cols=scols, vals=svals, diag=diag,
+                      csr=(row_ptr, cols, vals))
+
+
+def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
+    """Assemble L (SPD after Dirichlet rows/cols of ``fixed`` -> identity)."""
+    dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
+    row_ptr, cols = csr_pattern(dm)
+    vals = torch.zeros(cols.numel(), dtype=torch.float64, device=dm.device)
+    call("ab_laplacian_csr", ctypes.byref(dm.struct), ptr(row_ptr), ptr(cols), ptr(vals), stream_handle())
+    if fixed is not None:
+        f8 = fixed.to(device=dm.device, dtype=torch.uint8).contiguous()
+        call("ab_csr_dirichlet", dm.n_nodes, ptr(row_ptr), ptr(cols), ptr(vals), ptr(f8), stream_handle())
+    return csr_to_sell(dm.n_nodes, row_ptr, cols, vals)
+
+
+class PCG:
+    """Jacobi-PCG workspace bound to one matrix (no per-solve allocation).
+
+    ``halo`` (optional) is an interface exchanger with ``sum_(tensor, ncomp,
+    stride)`` and ``allreduce_(tensor)``; ``own`` holds per-row ownership
+    weights so duplicated interface rows count once in the dots.
+    """
+
+    def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
+                 own: torch.Tensor | None = None, halo=None):
+        self.A = A
+        n = A.n_rows
+        dev = A.vals.device
+        self.n = n
+        self.dinv = dinv
+        self.fixed = None if fixed is None else fixed.to(device=dev, dtype=torch.uint8).contiguous()
+        self.own = own
+        self.halo = halo
+        z = lambda: torch.zeros(n, dtype=torch.float64, device=dev)  # noqa: E731
+        self.x, self.r, self.zv, self.p0, self.p1, self.q = z(), z(), z(), z(), z(), z()
+        nb = (n + 255) // 256
+        self.part = torch.zeros(2 * nb + 8, dtype=torch.float64, device=dev)
+        self.red = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
+        self.cnt = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.launches_per_iter = 2 if halo is None else 3
+        self.mark = None  # optional event recorder (FlowSolver._mark)
+
+    def _m(self, name):
+        import contextlib
+        return self.mark(name) if self.mark is not None else contextlib.nullcontext()
+
+    def solve(self, b: torch.Tensor, maxit: int, tol: float = 0.0, check_every: int = 1, zero_b: bool = True):
+        """x = A^-1 b (x0 = 0).  With tol == 0 runs exactly ``maxit``
+        iterations without host synchronisation (CUDA-graph capturable).
+        ``zero_b`` re-zeroes b (it is an accumulation buffer of K4)."""
+        s = stream_handle()
+        A = ctypes.byref(self.A.struct)
+        call("ab_cg_init", self.n, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
+             ptr(self.x), ptr(self.r), ptr(self.zv), ptr(self.p0), ptr(self.own), ptr(self.red), ptr(self.sc),
+             ptr(self.part), ptr(self.cnt), s)
+        if self.halo is not None:
+            self.halo.allreduce_(self.red[0:2])
+        call("ab_cg_set_bb", ptr(self.red), ptr(self.sc), s)
+        pold, pnew = self.p0, self.p1
+        it = 0
+        while it < maxit:
+            if tol > 0 and it % check_every == 0:
+                rr, bb = float(self.red[1].item()), float(self.sc[1].item())
+                if bb == 0.0 or math.sqrt(rr / bb) <= tol:
+                    break
+            if self.halo is None:
+                with self._m("K5_cg_spmv"):
+                    call("ab_cg_spmv", A, ptr(self.zv), ptr(pold), ptr(pnew), ptr(self.q), 1, ptr(self.own),
+                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+            else:
+                call("ab_cg_spmv", A, ptr(self.zv), ptr(pold), ptr(pnew), ptr(self.q), 0, ptr(self.own),
+                     ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                self.halo.sum_(self.q, 1, 1)
+                call("ab_cg_dot", self.n, ptr(pnew), ptr(self.q), ptr(self.own), ptr(self.red), ptr(self.sc),
+                     ptr(self.part), ptr(self.cnt), s)
+                self.halo.allreduce_(self.red[2:3])
+            with self._m("K5_cg_update"):
+                call("ab_cg_update", self.n, ptr(pnew), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
+                     ptr(self.zv), ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+            if self.halo is not None:
+                self.halo.allreduce_(self.red[0:2])
+            pold, pnew = pnew, pold
+            it += 1
+        return self.x, it
+
+    def residual(self) -> float:
+        rr, bb = float(self.red[1].item()), float(self.sc[1].item())
+        return math.sqrt(rr / bb) if bb > 0 else 0.0
+
+
+def pcg_solve(A: SellMatrix, b: torch.Tensor, x0=None, tol: float = 1e-10, max_it: int = 1000,
+              fixed: torch.Tensor | None = None):
+    """Drop-in style solve: returns (x, iterations, ||r||/||b||)."""
+    dinv = 1.0 / A.diag
+    solver = PCG(A, dinv, fixed=fixed)
+    rhs = b.clone()
+    if x0 is not None:
+        rhs = rhs - A.matvec(x0)
+    x, it = solver.solve(rhs, max_it, tol=tol, zero_b=False)
+    x = x.clone()
+    if x0 is not None:
+        x = x + x0
+    return x, it, solver.residual()

@@ -1,0 +1,250 @@
+"""The fractional-step explicit-RK time step (Algorithm 1)
+on the GPU — new entry points ``time_step`` / ``run`` in the reference's
+functional style, backed by :class:`FlowSolver`.
+
+Per step (the CPU restatement is oracle/fem.py:FlowOracle):
+
+    for s in 1..3 (SSP-RK3 stage form):
+        K2  R_s = R(u_{s-1})                          ab_momentum_rhs  (+ interface sum)
+        K3  u_s = a_s u^n + b_s (u_{s-1} + dt/rho M_L^-1 (R_s - G p^n))   ab_rk_stage
+            velocity Dirichlet values                 ab_apply_velocity_bc
+    K4  b = -(rho/dt) D u_3                           ab_divergence    (+ interface sum)
+    K5  L' dp = b, Jacobi-PCG                         ab_cg_*          (+ halo / all-reduce)
+    K6  G dp                                          ab_gradient      (+ interface sum)
+    K7  u^{n+1} = u_3 - dt/rho M_L^-1 G dp; p += dp; Gp += G dp        ab_correct
+
+With a fixed CG iteration count the whole step is free of host
+synchronisation and is captured once into a CUDA graph and replayed.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from ._lib import AbPhys, call, ptr, stream_handle
+from .device import DeviceMesh, nodes_as4
+from .meshgen import MeshArrays
+from .solver import PCG, assemble_laplacian
+
+RK3_A = (0.0, 0.75, 1.0 / 3.0)
+RK3_B = (1.0, 0.25, 2.0 / 3.0)
+
+
+@dataclass
+class FlowParams:
+    rho: float = 1.0
+    mu: float = 1.0
+    c_vreman: float = 0.0
+
+    def struct(self) -> AbPhys:
+        return AbPhys(rho=self.rho, mu=self.mu, c_vreman=self.c_vreman)
+
+
+class FlowSolver:
+    """Owns the device state and workspaces of one (sub)domain.
+
+    ``halo`` (optional, :class:`halo.HaloExchanger`) sums interface-node
+    values across ranks and all-reduces the CG scalars; ``own`` gives the
+    per-node ownership weights for the dots.
+    """
+
+    def __init__(self, mesh, params: FlowParams | None = None, p_fixed=None, u_fixed=None, u_fixed_values=None,
+                 windows: bool = True, reorder: str | None = "sfc", halo=None, own=None):
+        self.params = params or FlowParams()
+        self.phys = self.params.struct()
+        self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows)
+        dm = self.dm
+        n = dm.n_nodes
+        dev = dm.device
+        self.n = n
+        self.halo = halo
+        s = stream_handle()
+        # lumped mass (K1, ml only) and its inverse
+        self.ml = torch.zeros(n, dtype=torch.float64, device=dev)
+        for k in range(len(dm.rules)):
+            call("ab_mass", ctypes.byref(dm.struct), k, None, None, ptr(self.ml), 128, s)
+        if halo is not None:
+            halo.sum_(self.ml, 1, 1)
+        self.minv = torch.empty_like(self.ml)
+        call("ab_reciprocal", n, ptr(self.ml), ptr(self.minv), s)
+        # pressure Laplacian with Dirichlet rows, Jacobi diagonal
+        pf = np.zeros(n, bool) if p_fixed is None else np.asarray(p_fixed, bool)
+        self.p_fixed = torch.from_numpy(pf.astype(np.uint8)).to(dev)
+        self.L = assemble_laplacian(dm, self.p_fixed if pf.any() else None)
+        diag = self.L.diag.clone()
+        if halo is not None:
+            halo.sum_(diag, 1, 1)
+            if pf.any():  # fixed rows are identity on every rank
+                diag[self.p_fixed.bool()] = 1.0
+        self.dinv = torch.empty_like(diag)
+        call("ab_reciprocal", n, ptr(diag), ptr(self.dinv), s)
+        self.own = own
+        self.pcg = PCG(self.L, self.dinv, fixed=self.p_fixed if pf.any() else None, own=own, halo=halo)
+        # velocity Dirichlet nodes (sparse list)
+        if u_fixed is not None and np.any(u_fixed):
+            uf = np.asarray(u_fixed, bool).reshape(n, 3)
+            idx = np.nonzero(uf.any(axis=1))[0]
+            mask = (uf[idx, 0] * 1 + uf[idx, 1] * 2 + uf[idx, 2] * 4).astype(np.uint8)
+            vals = np.zeros((n, 3)) if u_fixed_values is None else np.asarray(u_fixed_values, float).reshape(n, 3)
+            self.bc_idx = torch.from_numpy(idx.astype(np.int32)).to(dev)
+            self.bc_mask = torch.from_numpy(mask).to(dev)
+            self.bc_vals = torch.from_numpy(np.ascontiguousarray(vals[idx])).to(dev)
+        else:
+            self.bc_idx = None
+        z4 = lambda: torch.zeros((n, 4), dtype=torch.float64, device=dev)  # noqa: E731
+        self.U0, self.U, self.R, self.GP, self.GD = z4(), z4(), z4(), z4(), z4()
+        self.P = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.B = torch.zeros(n, dtype=torch.float64, device=dev)
+        self.graph = None
+        self.graph_key = None
+        self.last_cg_iters = 0
+        self.timeline = None  # list of (name, start, end) CUDA events when profiling
+
+    # -- state ----------------------------------------------------------------
+    def set_state(self, u, p):
+        u = torch.as_tensor(u, dtype=torch.float64, device=self.dm.device)
+        self.U0.copy_(nodes_as4(u))
+        self.P.copy_(torch.as_tensor(p, dtype=torch.float64, device=self.dm.device))
+        self._bc(self.U0)
+        self.GP.zero_()
+        call("ab_gradient", ctypes.byref(self.dm.struct), ptr(self.P), 1.0, ptr(self.GP), stream_handle())
+        if self.halo is not None:
+            self.halo.sum_(self.GP, 3, 4)
+
+    @property
+    def u(self) -> torch.Tensor:
+        return self.U0[:, :3]
+
+    @property
+    def p(self) -> torch.Tensor:
+        return self.P
+
+    def _bc(self, u4):
+        if self.bc_idx is not None:
+            call("ab_apply_velocity_bc", self.bc_idx.numel(), ptr(self.bc_idx), ptr(self.bc_mask), ptr(self.bc_vals),
+                 ptr(u4), stream_handle())
+
+    # -- operators ------------------------------------------------------------
+    def momentum(self, u4, out4):
+        call("ab_momentum_rhs", ctypes.byref(self.dm.struct), ctypes.byref(self.phys), ptr(u4), ptr(out4),
+             stream_handle())
+        if self.halo is not None:
+            self.halo.sum_(out4, 3, 4)
+
+    # -- one time step ----------------------------------------------------------
+    def _mark(self, name):
+        """Context manager recording CUDA events around a launch when
+        ``self.timeline`` is a list (bench.py's per-kernel breakdown)."""
+        solver = self
+
+        class _M:
+            def __enter__(self_inner):
+                if solver.timeline is not None:
+                    self_inner.a = torch.cuda.Event(enable_timing=True)
+                    self_inner.a.record()
+
+            def __exit__(self_inner, *exc):
+                if solver.timeline is not None:
+                    b = torch.cuda.Event(enable_timing=True)
+                    b.record()
+                    solver.timeline.append((name, self_inner.a, b))
+        return _M()
+
+    def _step_body(self, dt: float, cg_iters: int, cg_tol: float):
+        s = stream_handle()
+        dm = self.dm
+        rho = self.params.rho
+        k = dt / rho
+        for st in range(3):
+            uin = self.U0 if st == 0 else self.U
+            with self._mark("K2_momentum"):
+                call("ab_momentum_rhs", ctypes.byref(dm.struct), ctypes.byref(self.phys), ptr(uin), ptr(self.R), s)
+            if self.halo is not None:
+                self.halo.sum_(self.R, 3, 4)
+            with self._mark("K3_rk_stage"):
+                call("ab_rk_stage", self.n, RK3_A[st], RK3_B[st], k, ptr(self.U0), ptr(uin), ptr(self.R),
+                     ptr(self.GP), ptr(self.minv), ptr(self.U), s)
+            self._bc(self.U)
+        with self._mark("K4_divergence"):
+            call("ab_divergence", ctypes.byref(dm.struct), ptr(self.U), -rho / dt, ptr(self.B), s)
+        if self.halo is not None:
+            self.halo.sum_(self.B, 1, 1)
+        self.pcg.mark = self._mark
+        x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
+        self.last_cg_iters = it
+        with self._mark("K6_gradient"):
+            call("ab_gradient", ctypes.byref(dm.struct), ptr(x), 1.0, ptr(self.GD), s)
+        if self.halo is not None:
+            self.halo.sum_(self.GD, 3, 4)
+        with self._mark("K7_correct"):
+            call("ab_correct", self.n, k, ptr(self.U), ptr(self.U0), ptr(self.GD), ptr(self.minv), ptr(self.P),
+                 ptr(x), ptr(self.GP), s)
+        self._bc(self.U0)
+
+    def step_host(self, u_host: torch.Tensor, p_host: torch.Tensor, dt: float, cg_iters: int = 50,
+                  graph: bool = True):
+        """End-to-end call with HOST buffers (pinned for async copies): upload
+        (u, p), advance one step, download (u, p) in place."""
+        self.U0[:, :3].copy_(u_host, non_blocking=True)
+        self.P.copy_(p_host, non_blocking=True)
+        self.GP.zero_()
+        call("ab_gradient", ctypes.byref(self.dm.struct), ptr(self.P), 1.0, ptr(self.GP), stream_handle())
+        if self.halo is not None:
+            self.halo.sum_(self.GP, 3, 4)
+        self.step(dt, cg_iters, graph=graph)
+        u_host.copy_(self.U0[:, :3], non_blocking=True)
+        p_host.copy_(self.P, non_blocking=True)
+
+    def step(self, dt: float, cg_iters: int = 50, cg_tol: float = 0.0, graph: bool = False):
+        """Advance one step.  ``graph=True`` (fixed iterations, no halo)
+        captures the step once and replays the CUDA graph afterwards."""
+        if graph and cg_tol == 0.0 and self.halo is None:
+            key = (dt, cg_iters)
+            if self.graph is None or self.graph_key != key:
+                self.capture(dt, cg_iters)
+            self.graph.replay()
+            self.last_cg_iters = cg_iters
+            return
+        self._step_body(dt, cg_iters, cg_tol)
+
+    def capture(self, dt: float, cg_iters: int):
+        # snapshot the state: capture runs the body once on a side stream
+        saved = [t.clone() for t in (self.U0, self.P, self.GP)]
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            self._step_body(dt, cg_iters, 0.0)  # warm-up outside capture
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self._step_body(dt, cg_iters, 0.0)
+        for t, v in zip((self.U0, self.P, self.GP), saved):
+            t.copy_(v)
+        self.graph = g
+        self.graph_key = (dt, cg_iters)
+
+    def launches_per_step(self, cg_iters: int) -> int:
+        """Kernels of this library launched by one step (no halo)."""
+        ncat = len(self.dm.rules)
+        bc = 1 if self.bc_idx is not None else 0
+        return 3 * (ncat + 1 + bc) + ncat + (2 + 2 * cg_iters) + ncat + 1 + bc
+
+
+def time_step(solver: FlowSolver, dt: float, cg_iters: int = 50, cg_tol: float = 0.0):
+    """One fractional step; returns (u, p) views of the device state."""
+    solver.step(dt, cg_iters, cg_tol)
+    return solver.u, solver.p
+
+
+def run(mesh, u0, p0, n_steps: int, dt: float, params: FlowParams | None = None, cg_iters: int = 50,
+        cg_tol: float = 0.0, **kw):
+    """Build a solver for ``mesh``, set (u0, p0) and advance ``n_steps``."""
+    solver = mesh if isinstance(mesh, FlowSolver) else FlowSolver(mesh, params, **kw)
+    solver.set_state(u0, p0)
+    for _ in range(n_steps):
+        solver.step(dt, cg_iters, cg_tol)
+    return solver

@@ -1,0 +1,182 @@
+"""Generate the golden vectors that pin the oracle and the GPU path to the
+reference's own implementation.
+
+Runs ONLY in the build container, where the reference is importable from
+/root/reference/pkg/src.  The outputs are small committed
+fixtures; nothing on the GPU box reads /root/reference.
+
+    python tests/golden/make_golden.py
+
+Fixtures:
+  reference_mass.npz   meshes + reference assemble_reference / assemble_packs /
+                       build_packs Jacobians / scatter_global COO + row sums
+                       (reference assembly.py:178-333)
+  reference_sfc.npz    hilbert_keys_batch / hilbert_decode / project_to_bins /
+                       split_1d / partition_chunked outputs (reference sfc.py)
+  reference_balance.json  compute_metrics examples (reference balance.py:82-92)
+"""
+
+from __future__ import annotations
+
+import json
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg/src")
+HERE = Path(__file__).resolve().parent
+sys.path.insert(0, str(REF))
+sys.path.insert(0, str(HERE.parents[1]))
+
+import coexbal  # noqa: E402
+from coexbal import assembly as ra  # noqa: E402
+from coexbal import balance as rb  # noqa: E402
+from coexbal import mesh as rm  # noqa: E402
+from coexbal import sfc as rs  # noqa: E402
+from coexbal.fixtures import fixture_mesh_10k as load_fixture_mesh  # noqa: E402
+
+from paper_2005_05899_b200 import meshgen  # noqa: E402
+
+
+def connected_mixed_mesh(seed=7):
+    """Jittered Kuhn-tet box + disjoint hex box, elements shuffled so ids do not
+    follow categories; a few tets use the 1-point rule (category tet1)."""
+    tb = meshgen.box_tets(3, 3, 2, jitter=0.2, seed=seed)
+    hb = meshgen.box_hexes(2, 2, 3, lengths=(0.7, 0.9, 1.1), origin=(1.5, 0.1, -0.2))
+    rng = np.random.default_rng(seed)
+    hcoords = hb.coords + rng.uniform(-0.05, 0.05, hb.coords.shape)  # non-affine hexes
+    nodes = np.concatenate([tb.coords, hcoords])
+    off = tb.n_nodes
+    elems = [("tet", tuple(int(c) for c in row)) for row in tb.conn["tet4"]]
+    elems += [("hex", tuple(int(c) + off for c in row)) for row in hb.conn["hex8"]]
+    perm = rng.permutation(len(elems))
+    full = []
+    for k, i in enumerate(perm):
+        kind, conn = elems[i]
+        rule = "tet1" if (kind == "tet" and k % 7 == 3) else rm.ElementKind(kind).default_rule
+        full.append(rm.FullElement(kind=rm.ElementKind(kind), conn=conn, rule=rule))
+    return rm.FullMesh(nodes=nodes, elements=tuple(full))
+
+
+def pack_mesh(full):
+    """FullMesh -> flat arrays (kind tag, rule, conn padded to 8)."""
+    n = len(full.elements)
+    conn = np.full((n, 8), -1, dtype=np.int64)
+    kinds, rules = [], []
+    for i, e in enumerate(full.elements):
+        conn[i, : len(e.conn)] = e.conn
+        kinds.append(e.kind.value)
+        rules.append(e.rule)
+    return conn, np.array(kinds), np.array(rules)
+
+
+def mass_fixture(prefix, full, out):
+    conn, kinds, rules = pack_mesh(full)
+    out[f"{prefix}_nodes"] = full.nodes
+    out[f"{prefix}_conn"] = conn
+    out[f"{prefix}_kinds"] = kinds
+    out[f"{prefix}_rules"] = rules
+    ref = ra.assemble_reference(full)
+    ae = np.zeros((len(full.elements), 8, 8))
+    for i, m in ref.items():
+        ae[i, : m.shape[0], : m.shape[1]] = m
+    out[f"{prefix}_ae_reference"] = ae
+    for size in (1, 5, 32):
+        ps = ra.build_packs(full, size)
+        got = ra.assemble_packs(ps)
+        arr = np.zeros_like(ae)
+        for i, m in got.items():
+            arr[i, : m.shape[0], : m.shape[1]] = m
+        out[f"{prefix}_ae_packs{size}"] = arr
+    ps = ra.build_packs(full, 4)
+    J = np.zeros((len(full.elements), 8))
+    order = []
+    for p in ps.packs:
+        for lane in range(p.valid_count):
+            eid = int(p.element_ids[lane])
+            J[eid, : p.category.ngaus] = p.jacobian[lane]
+            order.append(eid)
+        out.setdefault(f"{prefix}_pack_valid", [])
+    out[f"{prefix}_jacobian"] = J
+    out[f"{prefix}_pack_order"] = np.array(order, dtype=np.int64)
+    out[f"{prefix}_pack_counts"] = np.array([p.valid_count for p in ps.packs], dtype=np.int64)
+    out.pop(f"{prefix}_pack_valid", None)
+    coo = ra.scatter_global(ref, full)
+    out[f"{prefix}_coo_rows"] = coo.rows
+    out[f"{prefix}_coo_cols"] = coo.cols
+    out[f"{prefix}_coo_vals"] = coo.values
+    out[f"{prefix}_row_sums"] = coo.row_sums()
+    out[f"{prefix}_total"] = np.array(coo.total())
+    pm = rm.partition_mesh_from_full(full)
+    out[f"{prefix}_centroids"] = pm.centroid_array()
+    out[f"{prefix}_weights"] = pm.weight_array()
+
+
+def sfc_fixture(out):
+    rng = np.random.default_rng(20200131)
+    for level in (1, 3, 8, 20):
+        side = 1 << level
+        cells = rng.integers(0, side, size=(512, 3), dtype=np.int64)
+        out[f"hk_cells_L{level}"] = cells
+        out[f"hk_keys_L{level}"] = rs.hilbert_keys_batch(cells, level)
+        keys = rng.integers(0, 1 << (3 * level), size=64, dtype=np.int64)
+        out[f"hd_keys_L{level}"] = keys
+        out[f"hd_cells_L{level}"] = np.array([rs.hilbert_decode(int(k), level) for k in keys], dtype=np.int64)
+    # partitions of the fixture mesh (seed 20200131, fixtures/__init__.py:13)
+    m = load_fixture_mesh()
+    out["fx_centroids"] = m.centroid_array()
+    out["fx_weights"] = m.weight_array()
+    out["fx_ids"] = m.id_array()
+    out["fx_box_lo"] = np.array(m.bounding_box.lo)
+    out["fx_box_hi"] = np.array(m.bounding_box.hi)
+    cases = []
+    for level in (4, 8):
+        cfg = rs.SfcConfig(level=level)
+        seq = rs.project_to_bins(m, cfg)
+        out[f"fx_bins_keys_L{level}"] = seq.keys
+        out[f"fx_bins_weights_L{level}"] = seq.weights
+        for P, lam in ((1, None), (2, None), (3, [0.5, 1.2, 1.3]), (8, None),
+                       (8, list(np.linspace(0.3, 1.7, 8)))):
+            if lam is not None:
+                lam = np.array(lam) * P / np.sum(lam)
+            part = rs.split_1d(seq, P, lam)
+            tag = f"L{level}_P{P}_{'lam' if lam is not None else 'uni'}"
+            cases.append(tag)
+            out[f"fx_cut_{tag}"] = part.cut_bins
+            out[f"fx_subw_{tag}"] = part.subdomain_weights
+            ids = np.array(sorted(part.assignment), dtype=np.int64)
+            out[f"fx_assign_{tag}"] = np.array([part.assignment[i] for i in ids], dtype=np.int64)
+            out[f"fx_lam_{tag}"] = np.ones(P) if lam is None else lam
+            for nch in (2, 8):
+                pc = rs.partition_chunked(m, cfg, P, lam, n_chunks=nch)
+                assert pc == part
+    out["fx_cases"] = np.array(cases)
+
+
+def balance_fixture():
+    rng = np.random.default_rng(5)
+    ex = []
+    for _ in range(8):
+        t = rng.uniform(0.5, 3.0, size=int(rng.integers(1, 9)))
+        mtr = rb.compute_metrics(rb.TimingSample(iteration=1, times=t))
+        ex.append({"times": t.tolist(), "mean": mtr.mean, "imbalance": mtr.imbalance, "lb": mtr.lb,
+                   "per_rank": mtr.per_rank.tolist(), "deviations": mtr.deviations.tolist()})
+    return ex
+
+
+def main():
+    out: dict = {}
+    mass_fixture("mixed", connected_mixed_mesh(), out)
+    mass_fixture("soup", rm.generate_synthetic_full_mesh(300, hex_fraction=0.3, seed=3), out)
+    np.savez_compressed(HERE / "reference_mass.npz", **out)
+    out = {}
+    sfc_fixture(out)
+    np.savez_compressed(HERE / "reference_sfc.npz", **out)
+    (HERE / "reference_balance.json").write_text(json.dumps(
+        {"reference_version": coexbal.__version__, "examples": balance_fixture()}, indent=1))
+    print("wrote fixtures to", HERE)
+
+
+if __name__ == "__main__":
+    main()
