@@ -663,7 +663,13 @@ int ab_mass(const ab_mesh* m, int32_t k, double* ae, double* jdet, double* ml, i
   CatP c = cat_params(m, k);
   if (c.n == 0) return AB_OK;
   return dispatch_rule(m->cat[k].rule, [&](auto r) {
-    k_mass<decltype(r)::value><<<grid_for(c.n, tile), tile, 0, S(stream)>>>(c, ae, jdet, ml);
+    // the pack (CTA tile) is capped by what the kernel's registers allow;
+    // per-element results do not depend on it
+    cudaFuncAttributes fa;
+    int t = tile;
+    if (cudaFuncGetAttributes(&fa, k_mass<decltype(r)::value>) == cudaSuccess && t > fa.maxThreadsPerBlock)
+      t = fa.maxThreadsPerBlock & ~31;
+    k_mass<decltype(r)::value><<<grid_for(c.n, t), t, 0, S(stream)>>>(c, ae, jdet, ml);
     return check_launch("ab_mass");
   });
 }
