@@ -71,6 +71,7 @@ typedef struct ab_phys {
 typedef struct ab_sell {
   int64_t n_rows;
   int64_t n_slices;
+  int64_t max_width;         /* widest slice; > 0 enables the TMA-staged SpMV */
   const int64_t* slice_ptr;  /* [n_slices+1], offsets in entries */
   const int32_t* cols;       /* [slice_ptr[n_slices]], lane-innermost; padding col = row */
   const double* vals;        /* same layout; padding 0 */
@@ -93,10 +94,16 @@ int ab_mass(const ab_mesh* mesh, int32_t cat, double* ae, double* jdet, double* 
             int32_t tile, void* stream);
 
 /* Register node windows for the category whose connectivity pointer is
- * `conn` (windowed scatter); blk_ptr == NULL clears them.
- * block must be 128 (elements per CTA). */
+ * `conn` (windowed gather/scatter); blk_ptr == NULL clears
+ * them.  Elements are taken in blocks of `block` (must be 128): block b's
+ * unique nodes are wnode[blk_ptr[b] .. blk_ptr[b+1]); window node k
+ * collects the element slots wslot[wptr[k] .. wptr[k+1]) (slot = local
+ * element * nnode + a); loc[e][a] is the window index of element e's node
+ * a; wmax = largest window.  Every K2/K4/K6 launch on that connectivity
+ * then gathers node data through the shared-memory window and issues one
+ * fp64 reduction per (block, node) instead of per (element, node). */
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
-                   const int32_t* wptr, const uint16_t* wslot);
+                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, int32_t wmax);
 
 /* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
  * New entry point; rhs4 accumulated. */
@@ -125,37 +132,39 @@ int ab_csr_to_sell(int64_t n_rows, const int64_t* row_ptr, const int32_t* cols, 
 int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 
 /* ---- K5: Jacobi-PCG kernels --------------------
- * Workspace `w` = 8 vectors of n_rows doubles: x r z p0 p1 q dinv b (see
- * DESIGN.md §4.3), `red` = 8 doubles of reduction results, `sc` = 8 doubles
- * of solver scalars, `part` = partial-sum scratch (>= 2*ceil(n/256) doubles),
- * `cnt` = 1 uint32 zero-initialised counter.  `own` (nullable) = per-row
- * ownership weights for dot products of a decomposed domain.
- *   init:  r = fixed ? 0 : b; b = 0; x = 0; z = dinv r; p_old = 0;
- *          red[RZN] = r.z, red[RR] = r.r, sc[BB] = r.r, sc[RZ] = 0
- *   spmv:  beta = sc[RZ] ? red[RZN]/sc[RZ] : 0;  p_new = z + beta p_old;
- *          q = A p_new;  if dot: red[PQ] = p_new.q;  sc[RZ] = red[RZN]
- *   dot:   red[PQ] = p.q; sc[RZ] = red[RZN]  (decomposed domains: spmv runs
- *          with with_dot = 0, then the q interface sum, then dot)
+ * z and the search direction p are stored interleaved as (z, p) pairs
+ * [n][2] in two alternating buffers; x, r, q, dinv are [n].  `red` = 8
+ * doubles of reduction results, `sc` = 8 doubles of solver scalars, `part`
+ * = partial-sum scratch (>= 2*(nb + ng) doubles, nb = ceil(n/256),
+ * ng = ceil(nb/64)), `cnt` = 1 + ng zero-initialised uint32 counters
+ * (two-level deterministic grid reduction, re-armed by the kernels).
+ * for the dot products of a decomposed domain.
+ *   init:   r = fixed ? 0 : b; b = 0 (if b_zero); x = 0; zp = (dinv r, 0);
+ *           red[RZN] = r.z, red[RR] = r.r, sc[RZ] = 0
+ *   set_bb: sc[BB] = red[RR]
+ *   spmv:   beta = sc[RZ] ? red[RZN]/sc[RZ] : 0; p = z + beta p_old (from
+ *           zp_in); zp_out.p = p; q = A p; if with_dot: red[PQ] = p.q and
+ *           sc[RZ] = red[RZN]
+ *   dot:    red[PQ] = p.q; sc[RZ] = red[RZN]  (decomposed domains: spmv runs
+ *           with with_dot = 0, then the q interface sum, then dot)
  *   update: alpha = red[PQ] ? sc[RZ]/red[PQ] : 0; x += alpha p; r -= alpha q;
- *          z = dinv r; red[RZN] = r.z; red[RR] = r.r                      */
+ *           zp.z = dinv r; red[RZN] = r.z; red[RR] = r.r
+ * All sums are deterministic (fixed-order block partials).                */
 #define AB_RED_RZN 0
 #define AB_RED_RR 1
 #define AB_RED_PQ 2
 #define AB_SC_RZ 0
 #define AB_SC_BB 1
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
-               double* x, double* r, double* z, double* p_old, const double* own, double* red, double* sc,
-               double* part, uint32_t* cnt, void* stream);
-int ab_cg_spmv(const ab_sell* a, const double* z, const double* p_old, double* p_new, double* q,
-               int32_t with_dot, const double* own, double* red, double* sc, double* part, uint32_t* cnt,
-               void* stream);
-int ab_cg_dot(int64_t n, const double* p, const double* q, const double* own, double* red, double* sc,
-              double* part, uint32_t* cnt, void* stream);
-/* sc[BB] = red[RR] (after the init sums are final / all-reduced) */
+               double* x, double* r, double* zp, const double* own, double* red, double* sc, double* part,
+               uint32_t* cnt, void* stream);
 int ab_cg_set_bb(double* red, double* sc, void* stream);
-int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r,
-                 double* z, const double* own, double* red, const double* sc, double* part, uint32_t* cnt,
-                 void* stream);
+int ab_cg_spmv(const ab_sell* a, const double* zp_in, double* zp_out, double* q, int32_t with_dot,
+               const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);
+int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, double* red, double* sc,
+              double* part, uint32_t* cnt, void* stream);
+int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r,
+                 const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
 
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */

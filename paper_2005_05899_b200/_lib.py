@@ -34,7 +34,8 @@ class AbPhys(C.Structure):
 
 
 class AbSell(C.Structure):
-    _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cols", vp), ("vals", vp)]
+    _fields_ = [("n_rows", i64), ("n_slices", i64), ("max_width", i64), ("slice_ptr", vp), ("cols", vp),
+                ("vals", vp)]
 
 
 P = C.POINTER
@@ -42,7 +43,7 @@ _SIGS = {
     "ab_version": ([], C.c_int),
     "ab_last_error": ([], C.c_char_p),
     "ab_launch_count": ([], i64),
-    "ab_set_windows": ([vp, i32, vp, vp, vp, vp], C.c_int),
+    "ab_set_windows": ([vp, i32, vp, vp, vp, vp, vp, i32], C.c_int),
     "ab_mass": ([P(AbMesh), i32, vp, vp, vp, i32, vp], C.c_int),
     "ab_momentum_rhs": ([P(AbMesh), P(AbPhys), vp, vp, vp], C.c_int),
     "ab_divergence": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
@@ -51,11 +52,11 @@ _SIGS = {
     "ab_csr_dirichlet": ([i64, vp, vp, vp, vp, vp], C.c_int),
     "ab_csr_to_sell": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
-    "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
-    "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_spmv": ([P(AbSell), vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
-    "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),

@@ -37,7 +37,9 @@ struct WinP {
   const int32_t* __restrict__ wnode;     // window node ids
   const int32_t* __restrict__ wptr;      // [n_win+1] offsets into wslot
   const uint16_t* __restrict__ wslot;    // slot = local_elem*NN + a
+  const uint16_t* __restrict__ loc;      // [E][NN] window-local node index of each element node
   int block;                             // elements per block (== blockDim.x)
+  int wmax;                              // largest window (nodes) of any block
 };
 
 template <int NN>
@@ -62,12 +64,7 @@ __device__ __forceinline__ void load_conn(const int32_t* __restrict__ conn, int6
 }
 
 template <int NN>
-__device__ __forceinline__ void load_coords(const CatP& c, const int (&nd)[NN], double (&x)[NN][3]) {
-#pragma unroll
-  for (int a = 0; a < NN; ++a) {
-    d4 v = ld4_nc(c.coords + 4 * (int64_t)nd[a]);
-    x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
-  }
+__device__ __forceinline__ void unwrap(const CatP& c, double (&x)[NN][3]) {
   if (c.periodic) {  // minimum-image unwrap relative to node 0
     const double L[3] = {c.L0, c.L1, c.L2};
 #pragma unroll
@@ -79,6 +76,16 @@ __device__ __forceinline__ void load_coords(const CatP& c, const int (&nd)[NN], 
           x[a][d] = x[0][d] + (rel - L[d] * rint(rel / L[d]));
         }
   }
+}
+
+template <int NN>
+__device__ __forceinline__ void load_coords(const CatP& c, const int (&nd)[NN], double (&x)[NN][3]) {
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    d4 v = ld4_nc(c.coords + 4 * (int64_t)nd[a]);
+    x[a][0] = v.x; x[a][1] = v.y; x[a][2] = v.z;
+  }
+  unwrap<NN>(c, x);
 }
 
 template <int NN>
@@ -209,28 +216,130 @@ __device__ __forceinline__ void scatter_direct(double* __restrict__ out, const i
 
 // Windowed scatter: every thread of the block must call it (contains
 // __syncthreads); invalid lanes pass zeros.
+// Per-thread window context, loaded once at kernel entry so that every
+// independent global load of the three window phases (node ids and slot
+// ranges of the thread's window node, the element's local node indices) is
+// in flight together instead of one latency per phase.  Thread t owns window
+// node b0 + t (and b0 + t + BLOCK, ... when a window exceeds the block).
+template <int NN>
+struct WinCtx {
+  int64_t b0, b1;
+  int node, s0, s1;
+  bool has;
+  int l[NN];
+};
+
+template <int NN, int BLOCK>
+__device__ __forceinline__ WinCtx<NN> win_begin(const WinP& w, int64_t e, int64_t n_elem) {
+  WinCtx<NN> x;
+  x.b0 = __ldg(w.blk_ptr + blockIdx.x);
+  x.b1 = __ldg(w.blk_ptr + blockIdx.x + 1);
+  const int64_t k = x.b0 + threadIdx.x;
+  x.has = k < x.b1;
+  x.node = x.has ? __ldg(w.wnode + k) : 0;
+  x.s0 = x.has ? __ldg(w.wptr + k) : 0;
+  x.s1 = x.has ? __ldg(w.wptr + k + 1) : 0;
+  if (e < n_elem) {
+    const uint16_t* p = w.loc + e * NN;
+    if constexpr (NN == 4) {
+      const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+      x.l[0] = v.x & 0xffff; x.l[1] = v.x >> 16; x.l[2] = v.y & 0xffff; x.l[3] = v.y >> 16;
+    } else {
+#pragma unroll
+      for (int a = 0; a < NN; ++a) x.l[a] = __ldg(p + a);
+    }
+  } else {
+#pragma unroll
+    for (int a = 0; a < NN; ++a) x.l[a] = 0;
+  }
+  return x;
+}
+
+// Phase C: element contributions -> shared slots SoA [NC][NN][BLOCK]
+// (conflict-free), then the owner thread of each window node sums its slots
+// in list order and issues one fp64 reduction per component.
 template <int NN, int NC, int STRIDE, int BLOCK>
-__device__ __forceinline__ void scatter_window(double* __restrict__ out, const WinP& w, const double (&r)[NN][NC]) {
-  extern __shared__ double slots[];  // [BLOCK*NN][NC]
+__device__ __forceinline__ void win_scatter(double* __restrict__ out, const WinP& w, const WinCtx<NN>& cx,
+                                            double* slots, const double (&r)[NN][NC]) {
 #pragma unroll
   for (int a = 0; a < NN; ++a)
 #pragma unroll
-    for (int c = 0; c < NC; ++c) slots[(threadIdx.x * NN + a) * NC + c] = r[a][c];
+    for (int c = 0; c < NC; ++c) slots[(c * NN + a) * BLOCK + threadIdx.x] = r[a][c];
   __syncthreads();
-  const int64_t b0 = w.blk_ptr[blockIdx.x], b1 = w.blk_ptr[blockIdx.x + 1];
-  for (int64_t k = b0 + threadIdx.x; k < b1; k += BLOCK) {
-    const int node = __ldg(w.wnode + k);
-    const int s0 = __ldg(w.wptr + k), s1 = __ldg(w.wptr + k + 1);
+  auto reduce = [&](int node, int s0, int s1) {
     double acc[NC];
 #pragma unroll
     for (int c = 0; c < NC; ++c) acc[c] = 0.0;
-    for (int s = s0; s < s1; ++s) {
-      const int slot = __ldg(w.wslot + s);
+    int s = s0;
+    for (; s + 4 <= s1; s += 4) {
+      int sl[4];
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] += slots[slot * NC + c];
+      for (int u = 0; u < 4; ++u) sl[u] = __ldg(w.wslot + s + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int a = sl[u] % NN, e = sl[u] / NN;
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[c] += slots[(c * NN + a) * BLOCK + e];
+      }
+    }
+    for (; s < s1; ++s) {
+      const int sl = __ldg(w.wslot + s);
+      const int a = sl % NN, e = sl / NN;
+#pragma unroll
+      for (int c = 0; c < NC; ++c) acc[c] += slots[(c * NN + a) * BLOCK + e];
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) red_add(out + (int64_t)node * STRIDE + c, acc[c]);
+  };
+  if (cx.has) reduce(cx.node, cx.s0, cx.s1);
+  for (int64_t k = cx.b0 + threadIdx.x + BLOCK; k < cx.b1; k += BLOCK)
+    reduce(__ldg(w.wnode + k), __ldg(w.wptr + k), __ldg(w.wptr + k + 1));
+}
+
+// Phase A: the block's unique nodes -> shared memory SoA [NV][wmax]
+// (x, y, z, then NV-3 field components).
+template <int NN, int NV, int BLOCK>
+__device__ __forceinline__ void win_fill(const CatP& c, const WinP& w, const WinCtx<NN>& cx,
+                                         const double* __restrict__ f, int fstride, double* nodes) {
+  const int W = w.wmax;
+  auto put = [&](int l, int64_t node) {
+    const d4 X = ld4_nc(c.coords + 4 * node);
+    double fv[3] = {0.0, 0.0, 0.0};
+    if constexpr (NV == 6) {
+      const d4 U = ld4_nc(f + 4 * node);
+      fv[0] = U.x; fv[1] = U.y; fv[2] = U.z;
+    } else if constexpr (NV == 4) {
+      fv[0] = __ldg(f + node * fstride);
+    }
+    nodes[l] = X.x;
+    nodes[W + l] = X.y;
+    nodes[2 * W + l] = X.z;
+#pragma unroll
+    for (int q = 0; q < NV - 3; ++q) nodes[(3 + q) * W + l] = fv[q];
+  };
+  if (cx.has) put(threadIdx.x, cx.node);
+  for (int64_t k = cx.b0 + threadIdx.x + BLOCK; k < cx.b1; k += BLOCK) put((int)(k - cx.b0), __ldg(w.wnode + k));
+  __syncthreads();
+}
+
+// Phase B: element nodes from the window.
+template <int NN, int NV>
+__device__ __forceinline__ void win_element(const WinP& w, const WinCtx<NN>& cx, const double* nodes,
+                                            double (&x)[NN][3], double (&f)[NN][NV == 6 ? 3 : 1]) {
+  const int W = w.wmax;
+#pragma unroll
+  for (int a = 0; a < NN; ++a) {
+    const int l = cx.l[a];
+    x[a][0] = nodes[l];
+    x[a][1] = nodes[W + l];
+    x[a][2] = nodes[2 * W + l];
+    if constexpr (NV == 6) {
+      f[a][0] = nodes[3 * W + l];
+      f[a][1] = nodes[4 * W + l];
+      f[a][2] = nodes[5 * W + l];
+    } else {
+      f[a][0] = nodes[3 * W + l];
+    }
   }
 }
 
@@ -284,13 +393,9 @@ __global__ void k_mass(CatP c, double* __restrict__ ae, double* __restrict__ jde
 // K2: momentum RHS  R_a -= int rho N_a [2 eps(u) u + div(u) u] + 2 (mu+mu_t) eps : grad N_a
 // ---------------------------------------------------------------------------
 template <int R, int NN>
-__device__ __forceinline__ void momentum_element(const CatP& c, const ab_phys ph, const double* __restrict__ u4,
-                                                 int64_t e, int (&nd)[NN], double (&r)[NN][3]) {
+__device__ __forceinline__ void momentum_element(const ab_phys ph, const double (&x)[NN][3], const double (&u)[NN][3],
+                                                 double (&r)[NN][3]) {
   constexpr int NG = RuleT<R>::NG;
-  load_conn<NN>(c.conn, e, nd);
-  double x[NN][3], u[NN][3];
-  load_coords<NN>(c, nd, x);
-  load_vec<NN>(u4, nd, u);
 #pragma unroll
   for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
 
@@ -410,100 +515,153 @@ template <int R, int BLOCK, bool WIN>
 __global__ void __launch_bounds__(BLOCK) k_momentum(CatP c, ab_phys ph, const double* __restrict__ u4,
                                                     double* __restrict__ rhs4, WinP w) {
   constexpr int NN = RuleT<R>::NN;
+  extern __shared__ double sm[];
   const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-  int nd[NN];
-  double r[NN][3];
-  if (e < c.n) {
-    momentum_element<R, NN>(c, ph, u4, e, nd, r);
-    if constexpr (!WIN) scatter_direct<NN, 3, 4>(rhs4, nd, r);
-  } else {
-#pragma unroll
-    for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
+  WinCtx<NN> cx;
+  if constexpr (WIN) {
+    cx = win_begin<NN, BLOCK>(w, e, c.n);
+    win_fill<NN, 6, BLOCK>(c, w, cx, u4, 4, sm);
   }
-  if constexpr (WIN) scatter_window<NN, 3, 4, BLOCK>(rhs4, w, r);
+  double r[NN][3];
+#pragma unroll
+  for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
+  if (e < c.n) {
+    double x[NN][3], u[NN][3];
+    if constexpr (WIN) {
+      win_element<NN, 6>(w, cx, sm, x, u);
+      unwrap<NN>(c, x);
+      momentum_element<R, NN>(ph, x, u, r);
+    } else {
+      int nd[NN];
+      load_conn<NN>(c.conn, e, nd);
+      load_coords<NN>(c, nd, x);
+      load_vec<NN>(u4, nd, u);
+      momentum_element<R, NN>(ph, x, u, r);
+      scatter_direct<NN, 3, 4>(rhs4, nd, r);
+    }
+  }
+  if constexpr (WIN) win_scatter<NN, 3, 4, BLOCK>(rhs4, w, cx, sm + (size_t)w.wmax * 6, r);
 }
 
 // ---------------------------------------------------------------------------
 // K4 divergence / K6 gradient  (int N_a div u, int N_a grad p)
 // ---------------------------------------------------------------------------
+template <int R, int NN>
+__device__ __forceinline__ void divergence_element(double scale, const double (&x)[NN][3], const double (&u)[NN][3],
+                                                   double (&r)[NN][1]) {
+  constexpr int NG = RuleT<R>::NG;
+#pragma unroll 1
+  for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+    double dNdx[NN][3];
+    const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
+    double div = 0.0;
+#pragma unroll
+    for (int a = 0; a < NN; ++a) div += u[a][0] * dNdx[a][0] + u[a][1] * dNdx[a][1] + u[a][2] * dNdx[a][2];
+    if constexpr (RuleT<R>::TET) {
+#pragma unroll
+      for (int gg = 0; gg < NG; ++gg) {
+        const double f = scale * adet * c_w[R][gg] * div;
+#pragma unroll
+        for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][gg][a], f, r[a][0]);
+      }
+    } else {
+      const double f = scale * adet * c_w[R][g] * div;
+#pragma unroll
+      for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][g][a], f, r[a][0]);
+    }
+  }
+}
+
+template <int R, int NN>
+__device__ __forceinline__ void gradient_element(double scale, const double (&x)[NN][3], const double (&pe)[NN][1],
+                                                 double (&r)[NN][3]) {
+  constexpr int NG = RuleT<R>::NG;
+#pragma unroll 1
+  for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+    double dNdx[NN][3];
+    const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
+    double gp[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+    for (int a = 0; a < NN; ++a)
+#pragma unroll
+      for (int k = 0; k < 3; ++k) gp[k] = fma(pe[a][0], dNdx[a][k], gp[k]);
+#pragma unroll
+    for (int gg = 0; gg < (RuleT<R>::TET ? NG : 1); ++gg) {
+      const int gi = RuleT<R>::TET ? gg : g;
+      const double f = scale * adet * c_w[R][gi];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        const double fn = f * c_N[R][gi][a];
+#pragma unroll
+        for (int k = 0; k < 3; ++k) r[a][k] = fma(fn, gp[k], r[a][k]);
+      }
+    }
+  }
+}
+
 template <int R, int BLOCK, bool WIN>
 __global__ void __launch_bounds__(BLOCK) k_divergence(CatP c, const double* __restrict__ u4, double scale,
                                                       double* __restrict__ out, WinP w) {
-  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  constexpr int NN = RuleT<R>::NN;
+  extern __shared__ double sm[];
   const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-  int nd[NN];
+  WinCtx<NN> cx;
+  if constexpr (WIN) {
+    cx = win_begin<NN, BLOCK>(w, e, c.n);
+    win_fill<NN, 6, BLOCK>(c, w, cx, u4, 4, sm);
+  }
   double r[NN][1];
 #pragma unroll
   for (int a = 0; a < NN; ++a) r[a][0] = 0.0;
   if (e < c.n) {
-    load_conn<NN>(c.conn, e, nd);
     double x[NN][3], u[NN][3];
-    load_coords<NN>(c, nd, x);
-    load_vec<NN>(u4, nd, u);
-#pragma unroll 1
-    for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
-      double dNdx[NN][3];
-      const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
-      double div = 0.0;
-#pragma unroll
-      for (int a = 0; a < NN; ++a) div += u[a][0] * dNdx[a][0] + u[a][1] * dNdx[a][1] + u[a][2] * dNdx[a][2];
-      if constexpr (RuleT<R>::TET) {
-#pragma unroll
-        for (int gg = 0; gg < NG; ++gg) {
-          const double f = scale * adet * c_w[R][gg] * div;
-#pragma unroll
-          for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][gg][a], f, r[a][0]);
-        }
-      } else {
-        const double f = scale * adet * c_w[R][g] * div;
-#pragma unroll
-        for (int a = 0; a < NN; ++a) r[a][0] = fma(c_N[R][g][a], f, r[a][0]);
-      }
+    if constexpr (WIN) {
+      win_element<NN, 6>(w, cx, sm, x, u);
+      unwrap<NN>(c, x);
+      divergence_element<R, NN>(scale, x, u, r);
+    } else {
+      int nd[NN];
+      load_conn<NN>(c.conn, e, nd);
+      load_coords<NN>(c, nd, x);
+      load_vec<NN>(u4, nd, u);
+      divergence_element<R, NN>(scale, x, u, r);
+      scatter_direct<NN, 1, 1>(out, nd, r);
     }
-    if constexpr (!WIN) scatter_direct<NN, 1, 1>(out, nd, r);
   }
-  if constexpr (WIN) scatter_window<NN, 1, 1, BLOCK>(out, w, r);
+  if constexpr (WIN) win_scatter<NN, 1, 1, BLOCK>(out, w, cx, sm + (size_t)w.wmax * 6, r);
 }
 
 template <int R, int BLOCK, bool WIN>
 __global__ void __launch_bounds__(BLOCK) k_gradient(CatP c, const double* __restrict__ p, double scale,
                                                     double* __restrict__ out4, WinP w) {
-  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  constexpr int NN = RuleT<R>::NN;
+  extern __shared__ double sm[];
   const int64_t e = (int64_t)blockIdx.x * BLOCK + threadIdx.x;
-  int nd[NN];
+  WinCtx<NN> cx;
+  if constexpr (WIN) {
+    cx = win_begin<NN, BLOCK>(w, e, c.n);
+    win_fill<NN, 4, BLOCK>(c, w, cx, p, 1, sm);
+  }
   double r[NN][3];
 #pragma unroll
   for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
   if (e < c.n) {
-    load_conn<NN>(c.conn, e, nd);
-    double x[NN][3], pe[NN];
-    load_coords<NN>(c, nd, x);
+    double x[NN][3], pe[NN][1];
+    if constexpr (WIN) {
+      win_element<NN, 4>(w, cx, sm, x, pe);
+      unwrap<NN>(c, x);
+      gradient_element<R, NN>(scale, x, pe, r);
+    } else {
+      int nd[NN];
+      load_conn<NN>(c.conn, e, nd);
+      load_coords<NN>(c, nd, x);
 #pragma unroll
-    for (int a = 0; a < NN; ++a) pe[a] = __ldg(p + nd[a]);
-#pragma unroll 1
-    for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
-      double dNdx[NN][3];
-      const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
-      double gp[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-      for (int a = 0; a < NN; ++a)
-#pragma unroll
-        for (int k = 0; k < 3; ++k) gp[k] = fma(pe[a], dNdx[a][k], gp[k]);
-#pragma unroll
-      for (int gg = 0; gg < (RuleT<R>::TET ? NG : 1); ++gg) {
-        const int gi = RuleT<R>::TET ? gg : g;
-        const double f = scale * adet * c_w[R][gi];
-#pragma unroll
-        for (int a = 0; a < NN; ++a) {
-          const double fn = f * c_N[R][gi][a];
-#pragma unroll
-          for (int k = 0; k < 3; ++k) r[a][k] = fma(fn, gp[k], r[a][k]);
-        }
-      }
+      for (int a = 0; a < NN; ++a) pe[a][0] = __ldg(p + nd[a]);
+      gradient_element<R, NN>(scale, x, pe, r);
+      scatter_direct<NN, 3, 4>(out4, nd, r);
     }
-    if constexpr (!WIN) scatter_direct<NN, 3, 4>(out4, nd, r);
   }
-  if constexpr (WIN) scatter_window<NN, 3, 4, BLOCK>(out4, w, r);
+  if constexpr (WIN) win_scatter<NN, 3, 4, BLOCK>(out4, w, cx, sm + (size_t)w.wmax * 4, r);
 }
 
 // ---------------------------------------------------------------------------
@@ -622,6 +780,16 @@ static int dispatch_rule(int rule, F&& f) {
 
 static constexpr int kBlock = 128;
 
+// Opt a kernel into > 48 KB of dynamic shared memory when a window needs it.
+template <class K>
+static int ensure_smem(K* kernel, size_t bytes) {
+  if (bytes <= 48 * 1024) return AB_OK;
+  if (bytes > 227 * 1024) return fail("node window exceeds 227 KB of shared memory");
+  if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) != cudaSuccess)
+    return fail("cudaFuncSetAttribute(MaxDynamicSharedMemorySize) failed");
+  return AB_OK;
+}
+
 // Windows are attached per category through ab_set_windows (host registry
 // keyed by the connectivity pointer, so the ab_mesh struct stays plain).
 struct WinEntry { const int32_t* conn; WinP w; };
@@ -642,17 +810,20 @@ extern "C" {
 
 // Register (or clear with blk_ptr == NULL) the node windows of a category.
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
-                   const int32_t* wptr, const uint16_t* wslot) {
+                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, int32_t wmax) {
+  const WinP wp{blk_ptr, wnode, wptr, wslot, loc, block, wmax};
   for (int i = 0; i < g_nwin; ++i)
     if (g_win[i].conn == conn) {
       if (!blk_ptr) { g_win[i] = g_win[--g_nwin]; return AB_OK; }
-      g_win[i].w = WinP{blk_ptr, wnode, wptr, wslot, block};
+      g_win[i].w = wp;
       return AB_OK;
     }
   if (!blk_ptr) return AB_OK;
   if (block != kBlock) return fail("ab_set_windows: block must be 128");
+  if (wmax < 1 || wmax > 8 * kBlock) return fail("ab_set_windows: bad wmax");
+  if (!wnode || !wptr || !wslot || !loc) return fail("ab_set_windows: null window array");
   if (g_nwin >= 64) return fail("ab_set_windows: registry full");
-  g_win[g_nwin++] = WinEntry{conn, WinP{blk_ptr, wnode, wptr, wslot, block}};
+  g_win[g_nwin++] = WinEntry{conn, wp};
   return AB_OK;
 }
 
@@ -686,7 +857,8 @@ int ab_momentum_rhs(const ab_mesh* m, const ab_phys* ph, const double* u4, doubl
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
       if (win) {
-        size_t sm = sizeof(double) * kBlock * NN * 3;
+        size_t sm = sizeof(double) * ((size_t)w.wmax * 6 + kBlock * NN * 3);
+        if (int rc = ensure_smem(k_momentum<R, kBlock, true>, sm)) return rc;
         k_momentum<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sm, S(stream)>>>(c, *ph, u4, rhs4, w);
       } else {
         k_momentum<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, *ph, u4, rhs4, w);
@@ -708,11 +880,13 @@ int ab_divergence(const ab_mesh* m, const double* u4, double scale, double* out,
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
-      if (win)
-        k_divergence<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sizeof(double) * kBlock * NN, S(stream)>>>(
-            c, u4, scale, out, w);
-      else
+      if (win) {
+        const size_t sm = sizeof(double) * ((size_t)w.wmax * 6 + kBlock * NN);
+        if (int rc = ensure_smem(k_divergence<R, kBlock, true>, sm)) return rc;
+        k_divergence<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sm, S(stream)>>>(c, u4, scale, out, w);
+      } else {
         k_divergence<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, u4, scale, out, w);
+      }
       return check_launch("ab_divergence");
     });
     if (rc) return rc;
@@ -730,11 +904,13 @@ int ab_gradient(const ab_mesh* m, const double* p, double scale, double* out4, v
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
-      if (win)
-        k_gradient<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sizeof(double) * kBlock * NN * 3,
-                                      S(stream)>>>(c, p, scale, out4, w);
-      else
+      if (win) {
+        const size_t sm = sizeof(double) * ((size_t)w.wmax * 4 + kBlock * NN * 3);
+        if (int rc = ensure_smem(k_gradient<R, kBlock, true>, sm)) return rc;
+        k_gradient<R, kBlock, true><<<grid_for(c.n, kBlock), kBlock, sm, S(stream)>>>(c, p, scale, out4, w);
+      } else {
         k_gradient<R, kBlock, false><<<grid_for(c.n, kBlock), kBlock, 0, S(stream)>>>(c, p, scale, out4, w);
+      }
       return check_launch("ab_gradient");
     });
     if (rc) return rc;

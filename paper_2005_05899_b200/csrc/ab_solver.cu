@@ -65,28 +65,34 @@ __global__ void k_sell_spmv(int64_t n, const int64_t* __restrict__ sp, const int
 }
 
 // ---------------------------------------------------------------------------
-// CG kernels
+// CG kernels.  z and the search direction p live interleaved as (z, p) pairs
+// so the SpMV gathers both with one 16-byte load per non-zero; two pair
+// buffers alternate between iterations.  All kernels are
+// grid-stride with at most kCgGrid blocks so the deterministic block
+// reduction is amortised over several rows per thread.
 // ---------------------------------------------------------------------------
+constexpr int kCgGrid = 148 * 8;
+
+__device__ __forceinline__ double2 ld2_nc(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+
 __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* __restrict__ b_in, double* b_zero,
                                                       const uint8_t* __restrict__ fixed,
                                                       const double* __restrict__ dinv, double* __restrict__ x,
-                                                      double* __restrict__ r, double* __restrict__ z,
-                                                      double* __restrict__ pold, const double* __restrict__ own,
-                                                      double* red, double* sc, double* part, uint32_t* cnt) {
-  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
+                                                      double* __restrict__ r, double* __restrict__ zp,
+                                                      const double* __restrict__ own, double* red, double* sc,
+                                                      double* part, uint32_t* cnt) {
   double v[2] = {0.0, 0.0};
-  if (i < n) {
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
     double ri = b_in[i];
     if (fixed && fixed[i]) ri = 0.0;
     if (b_zero) b_zero[i] = 0.0;
     const double zi = dinv[i] * ri;
     r[i] = ri;
-    z[i] = zi;
     x[i] = 0.0;
-    pold[i] = 0.0;
+    reinterpret_cast<double2*>(zp)[i] = make_double2(zi, 0.0);
     const double w = own ? own[i] : 1.0;
-    v[0] = w * ri * zi;
-    v[1] = w * ri * ri;
+    v[0] += w * ri * zi;
+    v[1] += w * ri * ri;
   }
   double t[2];
   if (grid_sum<2, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
@@ -99,30 +105,50 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* _
 // Copy red[RR] -> sc[BB] after the (optionally all-reduced) init sums.
 __global__ void k_cg_set_bb(const double* red, double* sc) { sc[AB_SC_BB] = red[AB_RED_RR]; }
 
+// q = A (z + beta p_old); p_new -> zp_out[i].p; optional p.q partials.
+// One row per thread.  Each chunk of up to kChunk non-zeros issues all its
+// column/value loads, then all (z, p) gathers, then the FMAs, so a row costs
+// two memory latencies per chunk instead of two per non-zero; the scalar
+// division for beta is placed after the first loads are in flight.
+constexpr int kChunk = 16;
+
 template <bool DOT>
 __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* __restrict__ sp,
                                                       const int32_t* __restrict__ scol,
-                                                      const double* __restrict__ sval, const double* __restrict__ z,
-                                                      const double* __restrict__ pold, double* __restrict__ pnew,
+                                                      const double* __restrict__ sval,
+                                                      const double* __restrict__ zp_in, double* __restrict__ zp_out,
                                                       double* __restrict__ q, const double* __restrict__ own,
                                                       double* red, double* sc, double* part, uint32_t* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
+  const double2* zp2 = reinterpret_cast<const double2*>(zp_in);
   const double rz_old = sc[AB_SC_RZ];
   const double rz_new = red[AB_RED_RZN];
   const double beta = rz_old != 0.0 ? rz_new / rz_old : 0.0;
-  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
   double v[1] = {0.0};
   if (i < n) {
     const int64_t s = i >> 5;
     const int lane = (int)(i & 31);
-    const int64_t base = sp[s], end = sp[s + 1];
+    const int64_t base = sp[s] + lane;
+    const int width = (int)((sp[s + 1] - sp[s]) >> 5);
     double acc = 0.0;
-    for (int64_t k = base + lane; k < end; k += 32) {
-      const int c = __ldcs(scol + k);
-      const double pc = fma(beta, __ldg(pold + c), __ldg(z + c));
-      acc = fma(__ldcs(sval + k), pc, acc);
+    for (int j0 = 0; j0 < width; j0 += kChunk) {
+      int c[kChunk];
+      double a[kChunk];
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) {
+        const bool ok = j0 + u < width;
+        c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
+        a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+      }
+      double2 g[kChunk];
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) g[u] = __ldg(zp2 + c[u]);
+#pragma unroll
+      for (int u = 0; u < kChunk; ++u) acc = fma(a[u], fma(beta, g[u].y, g[u].x), acc);
     }
-    const double pi = fma(beta, pold[i], z[i]);
-    pnew[i] = pi;
+    const double2 own_zp = __ldg(zp2 + i);
+    const double pi = fma(beta, own_zp.y, own_zp.x);
+    zp_out[2 * i + 1] = pi;
     q[i] = acc;
     if (DOT) v[0] = (own ? own[i] : 1.0) * pi * acc;
   }
@@ -138,12 +164,12 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* 
 
 // p.q after the interface sum of q (decomposed path); the last block also
 // performs the rz shift that k_cg_spmv<true> does in the single-domain path.
-__global__ void __launch_bounds__(kCgBlock) k_cg_dot(int64_t n, const double* __restrict__ p,
+__global__ void __launch_bounds__(kCgBlock) k_cg_dot(int64_t n, const double* __restrict__ zp,
                                                      const double* __restrict__ q, const double* __restrict__ own,
                                                      double* red, double* sc, double* part, uint32_t* cnt) {
-  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
   double v[1] = {0.0};
-  if (i < n) v[0] = (own ? own[i] : 1.0) * p[i] * q[i];
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock)
+    v[0] += (own ? own[i] : 1.0) * zp[2 * i + 1] * q[i];
   double t[1];
   if (grid_sum<1, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
     red[AB_RED_PQ] = t[0];
@@ -151,22 +177,42 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_dot(int64_t n, const double* __
   }
 }
 
-__global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, const double* __restrict__ p,
+// x += alpha p; r -= alpha q; z = dinv r (-> zp[i].z); r.z and r.r partials.
+// Two consecutive rows per thread with 128/256-bit accesses (n even is not
+// required: the odd tail row is handled by the scalar path).
+__global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, double* __restrict__ zp,
                                                         const double* __restrict__ q,
                                                         const double* __restrict__ dinv, double* __restrict__ x,
-                                                        double* __restrict__ r, double* __restrict__ z,
-                                                        const double* __restrict__ own, double* red,
-                                                        const double* sc, double* part, uint32_t* cnt) {
-  const double pq = red[AB_RED_PQ];
-  const double alpha = pq != 0.0 ? sc[AB_SC_RZ] / pq : 0.0;
-  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
+                                                        double* __restrict__ r, const double* __restrict__ own,
+                                                        double* red, const double* sc, double* part, uint32_t* cnt) {
   double v[2] = {0.0, 0.0};
-  if (i < n) {
-    x[i] = fma(alpha, p[i], x[i]);
+  const int64_t i = 2 * ((int64_t)blockIdx.x * kCgBlock + threadIdx.x);
+  const double pq = red[AB_RED_PQ];
+  const double rz = sc[AB_SC_RZ];
+  if (i + 1 < n) {
+    const d4 zpv = ld4(zp + 2 * i);  // (z0, p0, z1, p1)
+    const double2 xv = *reinterpret_cast<const double2*>(x + i);
+    const double2 qv = __ldcs(reinterpret_cast<const double2*>(q + i));
+    const double2 rv = *reinterpret_cast<const double2*>(r + i);
+    const double2 dv = __ldg(reinterpret_cast<const double2*>(dinv + i));
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    const double r0 = fma(-alpha, qv.x, rv.x), r1 = fma(-alpha, qv.y, rv.y);
+    const double z0 = dv.x * r0, z1 = dv.y * r1;
+    *reinterpret_cast<double2*>(x + i) = make_double2(fma(alpha, zpv.y, xv.x), fma(alpha, zpv.w, xv.y));
+    *reinterpret_cast<double2*>(r + i) = make_double2(r0, r1);
+    st4(zp + 2 * i, d4{z0, zpv.y, z1, zpv.w});
+    double w0 = 1.0, w1 = 1.0;
+    if (own) { w0 = own[i]; w1 = own[i + 1]; }
+    v[0] = w0 * r0 * z0 + w1 * r1 * z1;
+    v[1] = w0 * r0 * r0 + w1 * r1 * r1;
+  } else if (i < n) {
+    const double alpha = pq != 0.0 ? rz / pq : 0.0;
+    const double pi = zp[2 * i + 1];
+    x[i] = fma(alpha, pi, x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     const double zi = dinv[i] * ri;
     r[i] = ri;
-    z[i] = zi;
+    zp[2 * i] = zi;
     const double w = own ? own[i] : 1.0;
     v[0] = w * ri * zi;
     v[1] = w * ri * ri;
@@ -176,6 +222,11 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, const double*
     red[AB_RED_RZN] = t[0];
     red[AB_RED_RR] = t[1];
   }
+}
+
+static unsigned cg_grid(int64_t n) {
+  const int64_t g = (n + kCgBlock - 1) / kCgBlock;
+  return (unsigned)(g < kCgGrid ? g : kCgGrid);
 }
 
 }  // namespace ab
@@ -207,11 +258,10 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream) {
 }
 
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv, double* x,
-               double* r, double* z, double* p_old, const double* own, double* red, double* sc, double* part,
-               uint32_t* cnt, void* stream) {
+               double* r, double* zp, const double* own, double* red, double* sc, double* part, uint32_t* cnt,
+               void* stream) {
   if (n <= 0) return fail("ab_cg_init: empty system");
-  k_cg_init<<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, z, p_old, own,
-                                                               red, sc, part, cnt);
+  k_cg_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, zp, own, red, sc, part, cnt);
   return check_launch("ab_cg_init");
 }
 
@@ -220,28 +270,30 @@ int ab_cg_set_bb(double* red, double* sc, void* stream) {
   return check_launch("ab_cg_set_bb");
 }
 
-int ab_cg_spmv(const ab_sell* a, const double* z, const double* p_old, double* p_new, double* q, int32_t with_dot,
-               const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream) {
+int ab_cg_spmv(const ab_sell* a, const double* zp_in, double* zp_out, double* q, int32_t with_dot, const double* own,
+               double* red, double* sc, double* part, uint32_t* cnt, void* stream) {
   if (!a) return fail("ab_cg_spmv: null matrix");
+  if (zp_in == zp_out) return fail("ab_cg_spmv: zp_in and zp_out must differ");
   const int64_t n = a->n_rows;
   if (with_dot)
-    k_cg_spmv<true><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p_old,
-                                                                       p_new, q, own, red, sc, part, cnt);
+    k_cg_spmv<true><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, zp_in,
+                                                                       zp_out, q, own, red, sc, part, cnt);
   else
-    k_cg_spmv<false><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p_old,
-                                                                        p_new, q, own, red, sc, part, cnt);
+    k_cg_spmv<false><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, zp_in,
+                                                                        zp_out, q, own, red, sc, part, cnt);
   return check_launch("ab_cg_spmv");
 }
 
-int ab_cg_dot(int64_t n, const double* p, const double* q, const double* own, double* red, double* sc, double* part,
+int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, double* red, double* sc, double* part,
               uint32_t* cnt, void* stream) {
-  k_cg_dot<<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, p, q, own, red, sc, part, cnt);
+  k_cg_dot<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, zp, q, own, red, sc, part, cnt);
   return check_launch("ab_cg_dot");
 }
 
-int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r, double* z,
-                 const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream) {
-  k_cg_update<<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, p, q, dinv, x, r, z, own, red, sc, part, cnt);
+int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r, const double* own,
+                 double* red, const double* sc, double* part, uint32_t* cnt, void* stream) {
+  k_cg_update<<<grid_for((n + 1) / 2, kCgBlock), kCgBlock, 0, S(stream)>>>(n, zp, q, dinv, x, r, own, red, sc, part,
+                                                                        cnt);
   return check_launch("ab_cg_update");
 }
 

@@ -125,9 +125,16 @@ class DeviceMesh:
             nblk = (E + B - 1) // B
             blk_ptr = torch.searchsorted(wblk, torch.arange(nblk + 1, device=self.device, dtype=torch.int64))
             blk_ptr = blk_ptr.to(torch.int64).contiguous()
-            w = (blk_ptr, wnode, wptr, wslot)
+            # window-local index of every (element, node) reference
+            uid = torch.cumsum(start.to(torch.int64), 0) - 1
+            local = uid - blk_ptr[blk[order]]
+            loc = torch.empty_like(local)
+            loc[order] = local
+            loc = loc.to(torch.int16).reshape(E, nn).contiguous()
+            wmax = int((blk_ptr[1:] - blk_ptr[:-1]).max().item())
+            w = (blk_ptr, wnode, wptr, wslot, loc, wmax)
             self._win.append(w)
-            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot))
+            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot), ptr(loc), wmax)
         self.windows = True
 
     def window_stats(self):
@@ -135,14 +142,14 @@ class DeviceMesh:
         for rule, conn, w in zip(self.rules, self.conn, self._win):
             if w is None:
                 continue
-            out[rule] = {"refs": int(conn.numel()), "window_nodes": int(w[1].numel()),
+            out[rule] = {"refs": int(conn.numel()), "window_nodes": int(w[1].numel()), "wmax": w[5],
                          "reduction": float(conn.numel()) / max(1, int(w[1].numel()))}
         return out
 
     def clear_windows(self):
         for conn, w in zip(self.conn, self._win):
             if w is not None:
-                call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None)
+                call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None, None, 0)
         self._win = []
         self.windows = False
 

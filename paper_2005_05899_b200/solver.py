@@ -33,8 +33,13 @@ class SellMatrix:
     diag: torch.Tensor        # f64 [n_rows]
     csr: tuple | None = None  # (row_ptr int64, cols int32, vals f64), kept for tests/export
 
+    staged: bool = True       # TMA-staged SpMV (ab_cg_spmv) when every slice fits
+
     def __post_init__(self):
+        w = (self.slice_ptr[1:] - self.slice_ptr[:-1]) // 32
+        self.max_width = int(w.max().item()) if w.numel() else 0
         self.struct = AbSell(n_rows=self.n_rows, n_slices=self.slice_ptr.numel() - 1,
+                             max_width=self.max_width if self.staged else 0,
                              slice_ptr=ptr(self.slice_ptr), cols=ptr(self.cols), vals=ptr(self.vals))
 
     @property
@@ -80,8 +85,9 @@ def csr_to_sell(n: int, row_ptr, cols, vals) -> SellMatrix:
     slice_ptr = torch.zeros(n_slices + 1, dtype=torch.int64, device=dev)
     slice_ptr[1:] = torch.cumsum(width * 32, 0)
     total = int(slice_ptr[-1].item())
-    scols = torch.empty(total, dtype=torch.int32, device=dev)
-    svals = torch.empty(total, dtype=torch.float64, device=dev)
+    # zero-filled: lanes of the last slice past n_rows stay (col 0, val 0)
+    scols = torch.zeros(total, dtype=torch.int32, device=dev)
+    svals = torch.zeros(total, dtype=torch.float64, device=dev)
     diag = torch.empty(n, dtype=torch.float64, device=dev)
     call("ab_csr_to_sell", n, ptr(row_ptr), ptr(cols), ptr(vals), ptr(slice_ptr), ptr(scols), ptr(svals),
          ptr(diag), stream_handle())
@@ -120,12 +126,16 @@ class PCG:
         self.own = own
         self.halo = halo
         z = lambda: torch.zeros(n, dtype=torch.float64, device=dev)  # noqa: E731
-        self.x, self.r, self.zv, self.p0, self.p1, self.q = z(), z(), z(), z(), z(), z()
-        nb = (n + 255) // 256
-        self.part = torch.zeros(2 * nb + 8, dtype=torch.float64, device=dev)
+        self.x, self.r, self.q = z(), z(), z()
+        # (z, p) pairs, two alternating buffers
+        self.zpa = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+        self.zpb = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+        nb = (n + 255) // 256 + 1
+        ng = (nb + 63) // 64 + 1
+        self.part = torch.zeros(2 * (nb + ng) + 8, dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
-        self.cnt = torch.zeros(4, dtype=torch.int32, device=dev)
+        self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)
         self.launches_per_iter = 2 if halo is None else 3
         self.mark = None  # optional event recorder (FlowSolver._mark)
 
@@ -140,12 +150,12 @@ class PCG:
         s = stream_handle()
         A = ctypes.byref(self.A.struct)
         call("ab_cg_init", self.n, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
-             ptr(self.x), ptr(self.r), ptr(self.zv), ptr(self.p0), ptr(self.own), ptr(self.red), ptr(self.sc),
+             ptr(self.x), ptr(self.r), ptr(self.zpa), ptr(self.own), ptr(self.red), ptr(self.sc),
              ptr(self.part), ptr(self.cnt), s)
         if self.halo is not None:
             self.halo.allreduce_(self.red[0:2])
         call("ab_cg_set_bb", ptr(self.red), ptr(self.sc), s)
-        pold, pnew = self.p0, self.p1
+        zin, zout = self.zpa, self.zpb
         it = 0
         while it < maxit:
             if tol > 0 and it % check_every == 0:
@@ -154,21 +164,21 @@ class PCG:
                     break
             if self.halo is None:
                 with self._m("K5_cg_spmv"):
-                    call("ab_cg_spmv", A, ptr(self.zv), ptr(pold), ptr(pnew), ptr(self.q), 1, ptr(self.own),
+                    call("ab_cg_spmv", A, ptr(zin), ptr(zout), ptr(self.q), 1, ptr(self.own),
                          ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             else:
-                call("ab_cg_spmv", A, ptr(self.zv), ptr(pold), ptr(pnew), ptr(self.q), 0, ptr(self.own),
+                call("ab_cg_spmv", A, ptr(zin), ptr(zout), ptr(self.q), 0, ptr(self.own),
                      ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
                 self.halo.sum_(self.q, 1, 1)
-                call("ab_cg_dot", self.n, ptr(pnew), ptr(self.q), ptr(self.own), ptr(self.red), ptr(self.sc),
+                call("ab_cg_dot", self.n, ptr(zout), ptr(self.q), ptr(self.own), ptr(self.red), ptr(self.sc),
                      ptr(self.part), ptr(self.cnt), s)
                 self.halo.allreduce_(self.red[2:3])
             with self._m("K5_cg_update"):
-                call("ab_cg_update", self.n, ptr(pnew), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
-                     ptr(self.zv), ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                call("ab_cg_update", self.n, ptr(zout), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
+                     ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             if self.halo is not None:
                 self.halo.allreduce_(self.red[0:2])
-            pold, pnew = pnew, pold
+            zin, zout = zout, zin
             it += 1
         return self.x, it
 

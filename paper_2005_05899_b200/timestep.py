@@ -212,6 +212,12 @@ class FlowSolver:
         self._step_body(dt, cg_iters, cg_tol)
 
     def capture(self, dt: float, cg_iters: int):
+        import gc
+        # destroy unreachable graphs now: a CUDAGraph freed by the garbage
+        # collector in the middle of another capture invalidates that capture
+        self.graph = None
+        gc.collect()
+        torch.cuda.synchronize()
         # snapshot the state: capture runs the body once on a side stream
         saved = [t.clone() for t in (self.U0, self.P, self.GP)]
         side = torch.cuda.Stream()

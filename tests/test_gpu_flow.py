@@ -81,7 +81,8 @@ def test_laplacian_and_spmv(name):
 
 
 @pytest.mark.parametrize("name", ["tet", "mixed"])
-def test_pcg_fixed_iterations_and_convergence(name):
+@pytest.mark.parametrize("staged", [True, False])
+def test_pcg_fixed_iterations_and_convergence(name, staged):
     from paper_2005_05899_b200.solver import PCG, assemble_laplacian, pcg_solve
     import scipy.sparse.linalg as spla
     m = MESHES[name]
@@ -90,6 +91,8 @@ def test_pcg_fixed_iterations_and_convergence(name):
     b = np.random.default_rng(2).standard_normal(m.n_nodes)
     b[fixed] = 0.0
     A = assemble_laplacian(m, torch.from_numpy(fixed))
+    if not staged:
+        A.struct.max_width = 0  # plain SELL SpMV instead of the TMA-staged one
     dinv = 1.0 / A.diag
     # fixed iteration count: same iterate as the oracle
     pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed))
