@@ -125,12 +125,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int):
-    """Compulsory bytes (and flops for K2) per launch, layout-independent
-    (SURVEY §8(d)): int32 indices, fp64 values."""
+def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters: int = CG_ITERS):
+    """Algorithmic bytes (and flops for K2) per launch, layout-independent
+    (SURVEY §8(d) per-unit figures): int32 indices, fp64 values."""
     from paper_2005_05899_b200.meshgen import NODE_COUNT, RULE_KIND
     conn_bytes = sum(4 * NODE_COUNT[RULE_KIND[r]] * e for r, e in counts.items())
     N = n_nodes
+    if kernel == "K5_cg_resident":  # SURVEY §8(d) K5 per iteration: 12Z + 4(N+1) + 104N
+        return cg_iters * (12 * nnz + 4 * (N + 1) + 104 * N), cg_iters * (2 * nnz + 12 * N)
     if kernel == "K5_cg_spmv":      # vals+cols, z & p_old (gathered once), p_new & q writes
         return 12 * nnz + 32 * N, 2 * nnz + 3 * N
     if kernel == "K5_cg_update":    # x p r q dinv in, x r z out
@@ -149,7 +151,7 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int):
 
 
 # flops per element of K2 as written in the kernel (DESIGN.md §4.1 counts)
-FLOPS_K2 = {"tet4": 640, "tet1": 520}
+FLOPS_K2 = {"tet4": 664}  # ncu: 255 DFMA + 90 DMUL + 64 DADD thread-instructions per tet4 element
 
 
 def load_peaks():
@@ -296,7 +298,7 @@ def run_native(args):
     nnz = solver.L.nnz
     kern = {}
     for name, ts in per.items():
-        B, F = algorithmic_cost(name, counts, solver.n, nnz)
+        B, F = algorithmic_cost(name, counts, solver.n, nnz, args.cg_iters)
         avg = float(np.mean(ts))
         kern[name] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
                       "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,
@@ -306,7 +308,13 @@ def run_native(args):
     traffic = load_traffic().get(dom)
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(kern[dom]["gbs"], 1), "peak": peak, "unit": "GB/s",
             "frac": round(kern[dom]["gbs"] / peak, 4), "peak_source": peak_kind,
-            "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"]}
+            "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"],
+            "alg_bytes_definition": "SURVEY.md §8(d) per-unit figure x units per launch"}
+    if dom == "K5_cg_resident":
+        # what this design must move at minimum: matrix + (z, p) pair writes + D^-1 re-read per iteration
+        comp = args.cg_iters * (12 * nnz + 24 * solver.n)
+        roof["compulsory_bytes_per_launch"] = comp
+        roof["compulsory_frac"] = round(comp / (kern[dom]["avg_us"] * 1e-6) / 1e9 / peak, 4)
 
     result = {
         "metric": "M element-steps/s per time step (assembly + CG)", "value": round(value, 3),

@@ -153,6 +153,7 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 #define AB_RED_RZN 0
 #define AB_RED_RR 1
 #define AB_RED_PQ 2
+#define AB_RED_ITERS 3
 #define AB_SC_RZ 0
 #define AB_SC_BB 1
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
@@ -165,6 +166,18 @@ int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, d
               double* part, uint32_t* cnt, void* stream);
 int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r,
                  const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
+
+/* Resident CG: init + up to `maxit` iterations (stop when ||r||/||b|| <=
+ * tol, tested on the device; tol = 0 runs exactly maxit) in one cooperative
+ * kernel with one CTA per SM; each CTA keeps x, r, z, p, D^-1 of its rows in
+ * shared memory.  Same iterates as the kernels above.
+ * Outputs: x; red[RZN], red[RR], red[ITERS]; sc[BB].  `part` >= 5 * n_cta
+ * doubles.  ab_cg_resident_fits() returns 1 when n rows fit (and reports the
+ * launch shape); ab_cg_resident fails with AB_EINVAL otherwise. */
+int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta);
+int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
+                   double* x, double* zpa, double* zpb, int32_t maxit, double tol, double* red, double* sc,
+                   double* part, void* stream);
 
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */

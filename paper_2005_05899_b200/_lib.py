@@ -57,6 +57,8 @@ _SIGS = {
     "ab_cg_spmv": ([P(AbSell), vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_resident_fits": ([i64, vp, vp], C.c_int),
+    "ab_cg_resident": ([P(AbSell), vp, vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp], C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),

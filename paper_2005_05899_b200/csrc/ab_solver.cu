@@ -7,6 +7,8 @@
 //   update: x += alpha p, r -= alpha q, z = D^-1 r, r.z and r.r partials.
 // Scalars (alpha, beta) are formed on the device from the reduction slots,
 // so the loop never synchronises with the host.
+#include <cooperative_groups.h>
+
 #include "ab_common.cuh"
 
 namespace ab {
@@ -224,6 +226,182 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, double* __res
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Resident CG: the whole solve in ONE cooperative kernel (one CTA per SM).
+// Every CTA owns a contiguous, slice-aligned range of rows and keeps their
+// x, r, z, p and q in shared memory for all iterations (D^-1 is re-read
+// from L2 in phase B).  Per iteration only the
+// matrix is streamed from HBM, the (z, p) pairs of the owned rows are written
+// once for the neighbours' gathers, and the two grid-wide reductions are
+// deterministic (per-CTA partials, every CTA sums them in index order after a
+// grid barrier).  Convergence (tol > 0) is tested on the device, uniformly
+// in all CTAs, so even a tolerance-driven solve never returns to the host.
+// Used when the owned rows fit in shared memory (C2: 4768 rows x 40 B per SM);
+// otherwise the two-kernel path above runs.
+// ---------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+constexpr int kResBlock = 1024;
+constexpr int kResQ = 8;  // max slices per warp
+
+__device__ __forceinline__ double2 block_sum2(double a, double b, double* sm) {
+  double v[2] = {a, b};
+  block_sum<2, kResBlock>(v, sm);
+  return make_double2(v[0], v[1]);  // valid in warp 0
+}
+
+// Ordered sum of nb per-CTA partials (NV values each, layout part[k*nb+b]);
+// identical in every CTA.  Result broadcast through shared memory.
+template <int NV>
+__device__ __forceinline__ void all_sum(const double* part, int nb, double* bcast, double (&out)[NV]) {
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double acc = 0.0;
+      for (int b = threadIdx.x; b < nb; b += 32) acc += __ldcg(part + (size_t)k * nb + b);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (threadIdx.x == 0) bcast[k] = acc;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
+    int64_t n, int64_t rows_per_cta, const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
+    const double* __restrict__ sval, const double* __restrict__ b_in, double* b_zero, const uint8_t* __restrict__ fixed,
+    const double* __restrict__ dinv, double* __restrict__ x_out, double* zpa, double* zpb, int maxit, double tol,
+    double* red, double* sc, double* part) {
+  cg::grid_group grid = cg::this_grid();
+  extern __shared__ double smem[];
+  __shared__ double sred[2 * (kResBlock / 32)];
+  __shared__ double bcast[4];
+  const int nb = gridDim.x;
+  const int64_t RB = rows_per_cta;
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int64_t r1 = r0 + RB < n ? r0 + RB : n;
+  const int nloc = r1 > r0 ? (int)(r1 - r0) : 0;
+  double* sx = smem;
+  double* sr = sx + RB;
+  double* sz = sr + RB;
+  double* spp = sz + RB;
+  double* sq = spp + RB;
+  double* partA = part;                 // [nb]     p.q
+  double* partB = part + nb;            // [2][nb]  r.z, r.r
+  double* partI = part + 3 * (size_t)nb;  // [2][nb]  init r.z, r.r
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (nloc + 31) >> 5;     // slices of this CTA
+  const int64_t s_first = r0 >> 5;      // r0 is slice aligned
+
+  // ---- init: r = b (masked), z = D^-1 r, p = 0, x = 0
+  double a0 = 0.0, a1 = 0.0;
+  for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+    const int64_t i = r0 + l;
+    double ri = b_in[i];
+    if (fixed && fixed[i]) ri = 0.0;
+    if (b_zero) b_zero[i] = 0.0;
+    const double d = dinv[i];
+    const double zi = d * ri;
+    sx[l] = 0.0; sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
+    reinterpret_cast<double2*>(zpa)[i] = make_double2(zi, 0.0);
+    a0 += ri * zi;
+    a1 += ri * ri;
+  }
+  double2 bs = block_sum2(a0, a1, sred);
+  if (threadIdx.x == 0) { partI[blockIdx.x] = bs.x; partI[nb + blockIdx.x] = bs.y; }
+  grid.sync();
+  double t2[2];
+  all_sum<2>(partI, nb, bcast, t2);
+  double rz = t2[0], rr = t2[1];
+  const double bb = rr;
+  double rz_old = 0.0;
+  const double* zin = zpa;
+  double* zout = zpb;
+  int it = 0;
+  for (; it < maxit; ++it) {
+    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;  // same test as the host path
+    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    const double2* zin2 = reinterpret_cast<const double2*>(zin);
+    // ---- phase A: q = A (z + beta p_old), p = z + beta p_old
+    double pq = 0.0;
+#pragma unroll 1
+    for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
+      {
+        const int64_t s = s_first + sl;
+        const int64_t base = sp[s] + lane;
+        const int width = (int)((sp[s + 1] - sp[s]) >> 5);
+        double acc = 0.0;
+        for (int j0 = 0; j0 < width; j0 += kChunk) {
+          int c[kChunk];
+          double a[kChunk];
+#pragma unroll
+          for (int u = 0; u < kChunk; ++u) {
+            const bool ok = j0 + u < width;
+            c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
+            a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+          }
+          double2 g[kChunk];
+#pragma unroll
+          for (int u = 0; u < kChunk; ++u) g[u] = __ldcg(zin2 + c[u]);
+#pragma unroll
+          for (int u = 0; u < kChunk; ++u) acc = fma(a[u], fma(beta, g[u].y, g[u].x), acc);
+        }
+        const int l = sl * 32 + lane;
+        if (l < nloc) {
+          const double p = fma(beta, spp[l], sz[l]);
+          spp[l] = p;
+          zout[2 * (r0 + l) + 1] = p;
+          sq[l] = acc;
+          pq += p * acc;
+        }
+      }
+    }
+    {
+      double v[1] = {pq};
+      block_sum<1, kResBlock>(v, sred);
+      if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+    }
+    grid.sync();
+    double t1[1];
+    all_sum<1>(partA, nb, bcast, t1);
+    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+    // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
+    double b0 = 0.0, b1 = 0.0;
+    for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+      {
+        sx[l] = fma(alpha, spp[l], sx[l]);
+        const double ri = fma(-alpha, sq[l], sr[l]);
+        const double zi = __ldg(dinv + r0 + l) * ri;
+        sr[l] = ri;
+        sz[l] = zi;
+        zout[2 * (r0 + l)] = zi;
+        b0 += ri * zi;
+        b1 += ri * ri;
+      }
+    }
+    bs = block_sum2(b0, b1, sred);
+    if (threadIdx.x == 0) { partB[blockIdx.x] = bs.x; partB[nb + blockIdx.x] = bs.y; }
+    grid.sync();
+    all_sum<2>(partB, nb, bcast, t2);
+    rz_old = rz;
+    rz = t2[0];
+    rr = t2[1];
+    const double* tmp = zin;
+    zin = zout;
+    zout = const_cast<double*>(tmp);
+  }
+  for (int l = threadIdx.x; l < nloc; l += kResBlock) x_out[r0 + l] = sx[l];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    red[AB_RED_RZN] = rz;
+    red[AB_RED_RR] = rr;
+    red[AB_RED_ITERS] = (double)it;
+    sc[AB_SC_BB] = bb;
+  }
+}
+
 static unsigned cg_grid(int64_t n) {
   const int64_t g = (n + kCgBlock - 1) / kCgBlock;
   return (unsigned)(g < kCgGrid ? g : kCgGrid);
@@ -288,6 +466,44 @@ int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, d
               uint32_t* cnt, void* stream) {
   k_cg_dot<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, zp, q, own, red, sc, part, cnt);
   return check_launch("ab_cg_dot");
+}
+
+int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta) {
+  int dev = 0, sms = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  int64_t rb = ((n + sms - 1) / sms + 31) / 32 * 32;
+  const size_t smem = (size_t)rb * 5 * sizeof(double);
+  const bool ok = coop && smem <= 200 * 1024;
+  if (rows_per_cta) *rows_per_cta = rb;
+  if (n_cta) *n_cta = (int32_t)((n + rb - 1) / rb);
+  return ok ? 1 : 0;
+}
+
+int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
+                   double* x, double* zpa, double* zpb, int32_t maxit, double tol, double* red, double* sc,
+                   double* part, void* stream) {
+  if (!a) return fail("ab_cg_resident: null matrix");
+  int64_t n = a->n_rows, rb = 0;
+  int32_t ncta = 0;
+  if (!ab_cg_resident_fits(n, &rb, &ncta)) return fail("ab_cg_resident: system does not fit in shared memory");
+  const size_t smem = (size_t)rb * 5 * sizeof(double);
+  if (cudaFuncSetAttribute(k_cg_resident, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail("ab_cg_resident: cannot reserve shared memory");
+  const int64_t* sp = a->slice_ptr;
+  const int32_t* cols = a->cols;
+  const double* vals = a->vals;
+  int mi = maxit;
+  void* args[] = {&n, &rb, (void*)&sp, (void*)&cols, (void*)&vals, (void*)&b_in, &b_zero, (void*)&fixed,
+                  (void*)&dinv, &x, &zpa, &zpb, &mi, &tol, &red, &sc, &part};
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cg_resident, dim3(ncta), dim3(kResBlock), args, smem,
+                                              S(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_cg_resident: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  return check_launch("ab_cg_resident");
 }
 
 int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r, const double* own,

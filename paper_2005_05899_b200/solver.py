@@ -15,12 +15,13 @@ is interface-summed and the dots all-reduced between them (DESIGN.md §4.3/§5).
 from __future__ import annotations
 
 import ctypes
+import ctypes as C
 import math
 from dataclasses import dataclass
 
 import torch
 
-from ._lib import AbSell, call, ptr, stream_handle
+from ._lib import AbSell, call, lib, ptr, stream_handle
 from .device import DeviceMesh
 
 
@@ -116,7 +117,7 @@ class PCG:
     """
 
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
-                 own: torch.Tensor | None = None, halo=None):
+                 own: torch.Tensor | None = None, halo=None, resident: bool = True):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -132,12 +133,17 @@ class PCG:
         self.zpb = torch.zeros((n, 2), dtype=torch.float64, device=dev)
         nb = (n + 255) // 256 + 1
         ng = (nb + 63) // 64 + 1
-        self.part = torch.zeros(2 * (nb + ng) + 8, dtype=torch.float64, device=dev)
+        n_cta = C.c_int32(0)
+        fits = lib().ab_cg_resident_fits(n, None, C.byref(n_cta))
+        self.part = torch.zeros(max(2 * (nb + ng), 5 * n_cta.value) + 8, dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)
         self.launches_per_iter = 2 if halo is None else 3
         self.mark = None  # optional event recorder (FlowSolver._mark)
+        # single-domain solves run as one cooperative kernel when the rows fit
+        # in shared memory (ab_cg_resident); otherwise two kernels/iteration
+        self.resident = bool(resident and halo is None and fits)
 
     def _m(self, name):
         import contextlib
@@ -149,6 +155,13 @@ class PCG:
         ``zero_b`` re-zeroes b (it is an accumulation buffer of K4)."""
         s = stream_handle()
         A = ctypes.byref(self.A.struct)
+        if self.resident:
+            with self._m("K5_cg_resident"):
+                call("ab_cg_resident", A, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
+                     ptr(self.x), ptr(self.zpa), ptr(self.zpb), int(maxit), float(tol), ptr(self.red), ptr(self.sc),
+                     ptr(self.part), s)
+            it = int(self.red[3].item()) if tol > 0 else maxit
+            return self.x, it
         call("ab_cg_init", self.n, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
              ptr(self.x), ptr(self.r), ptr(self.zpa), ptr(self.own), ptr(self.red), ptr(self.sc),
              ptr(self.part), ptr(self.cnt), s)

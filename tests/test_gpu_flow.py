@@ -81,8 +81,8 @@ def test_laplacian_and_spmv(name):
 
 
 @pytest.mark.parametrize("name", ["tet", "mixed"])
-@pytest.mark.parametrize("staged", [True, False])
-def test_pcg_fixed_iterations_and_convergence(name, staged):
+@pytest.mark.parametrize("resident", [True, False])
+def test_pcg_fixed_iterations_and_convergence(name, resident):
     from paper_2005_05899_b200.solver import PCG, assemble_laplacian, pcg_solve
     import scipy.sparse.linalg as spla
     m = MESHES[name]
@@ -91,18 +91,21 @@ def test_pcg_fixed_iterations_and_convergence(name, staged):
     b = np.random.default_rng(2).standard_normal(m.n_nodes)
     b[fixed] = 0.0
     A = assemble_laplacian(m, torch.from_numpy(fixed))
-    if not staged:
-        A.struct.max_width = 0  # plain SELL SpMV instead of the TMA-staged one
     dinv = 1.0 / A.diag
     # fixed iteration count: same iterate as the oracle
-    pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed))
+    pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed), resident=resident)
+    assert pcg.resident == resident
     bt = torch.from_numpy(b).cuda()
     x, it = pcg.solve(bt.clone(), 7)
     xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 7)
     assert it == itr == 7
     assert rel_l2(x.cpu().numpy(), xr) <= 1e-10
-    # to convergence: matches a direct solve
-    x, it, res = pcg_solve(A, bt, tol=1e-12, max_it=2000, fixed=torch.from_numpy(fixed))
+    # to convergence (tested on the device for the resident kernel): matches a direct solve
+    pcg2 = PCG(A, dinv, fixed=torch.from_numpy(fixed), resident=resident)
+    x, it = pcg2.solve(bt.clone(), 2000, tol=1e-12, zero_b=False)
+    res = pcg2.residual()
+    xr2, itr2, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 2000, tol=1e-12)
+    assert it == itr2
     assert res <= 1e-12
     assert rel_l2(x.cpu().numpy(), spla.spsolve(L.tocsc(), b)) <= 1e-9
 
