@@ -99,11 +99,16 @@ int ab_mass(const ab_mesh* mesh, int32_t cat, double* ae, double* jdet, double* 
  * unique nodes are wnode[blk_ptr[b] .. blk_ptr[b+1]); window node k
  * collects the element slots wslot[wptr[k] .. wptr[k+1]) (slot = local
  * element * nnode + a); loc[e][a] is the window index of element e's node
- * a; wmax = largest window.  Every K2/K4/K6 launch on that connectivity
- * then gathers node data through the shared-memory window and issues one
- * fp64 reduction per (block, node) instead of per (element, node). */
+ * a; desc[b] = {blk_ptr[b], blk_ptr[b+1], wptr[blk_ptr[b]],
+ * wptr[blk_ptr[b+1]]} (int32 x 4, nullable); wmax = largest window.  Every
+ * K2/K4/K6 launch on that connectivity then gathers node data through the
+ * shared-memory window and issues one fp64 reduction per (block, node)
+ * instead of per (element, node); with `desc` it runs the persistent
+ * two-stage pipelined kernel (bulk-async metadata, cp.async node gathers).
+ * Every window array must be readable 16 bytes past its end. */
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
-                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, int32_t wmax);
+                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, const int32_t* desc,
+                   int32_t wmax);
 
 /* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
  * New entry point; rhs4 accumulated. */

@@ -38,6 +38,7 @@ struct WinP {
   const int32_t* __restrict__ wptr;      // [n_win+1] offsets into wslot
   const uint16_t* __restrict__ wslot;    // slot = local_elem*NN + a
   const uint16_t* __restrict__ loc;      // [E][NN] window-local node index of each element node
+  const int4* __restrict__ desc;         // per block {b0, b1, wptr[b0], wptr[b1]} (pipelined kernels)
   int block;                             // elements per block (== blockDim.x)
   int wmax;                              // largest window (nodes) of any block
 };
@@ -343,6 +344,8 @@ __device__ __forceinline__ void win_element(const WinP& w, const WinCtx<NN>& cx,
   }
 }
 
+// (the pipelined engine needs the element bodies below; see after K6)
+
 // ---------------------------------------------------------------------------
 // K1: mass matrix / Jacobians / lumped mass
 // ---------------------------------------------------------------------------
@@ -392,14 +395,15 @@ __global__ void k_mass(CatP c, double* __restrict__ ae, double* __restrict__ jde
 // ---------------------------------------------------------------------------
 // K2: momentum RHS  R_a -= int rho N_a [2 eps(u) u + div(u) u] + 2 (mu+mu_t) eps : grad N_a
 // ---------------------------------------------------------------------------
-template <int R, int NN>
+template <int R, int NN, class Emit>
 __device__ __forceinline__ void momentum_element(const ab_phys ph, const double (&x)[NN][3], const double (&u)[NN][3],
-                                                 double (&r)[NN][3]) {
+                                                 Emit emit) {
   constexpr int NG = RuleT<R>::NG;
-#pragma unroll
-  for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
-
   if constexpr (RuleT<R>::TET) {
+    // Affine element: geometry, grad u and mu_t are constant, and the
+    // convective Gauss sum is  sum_g w_g N_a(g) A u_g = A sum_b M_ab u_b with
+    // the reference-element mass table M (c_M); each node's contribution is
+    // emitted as soon as it is formed (no per-node accumulator registers).
     double dNdx[NN][3];
     const double det = shape_grads<R, NN>(x, 0, dNdx);
     const double adet = fabs(det);
@@ -433,34 +437,27 @@ __device__ __forceinline__ void momentum_element(const ab_phys ph, const double 
         A[i][j] = s + (i == j ? div : 0.0);
         sg[i][j] = mu_eff * s * vol;  // 2 mu eps_ij vol
       }
-    // m_a = sum_g w_g N_a(g) u_g   (convective term is linear in u_g here)
-    double mv[NN][3];
+    const double rdet = ph.rho * adet;
 #pragma unroll
-    for (int a = 0; a < NN; ++a) mv[a][0] = mv[a][1] = mv[a][2] = 0.0;
-#pragma unroll
-    for (int g = 0; g < NG; ++g) {
-      double ug[3] = {0.0, 0.0, 0.0};
+    for (int a = 0; a < NN; ++a) {
+      double m[3] = {0.0, 0.0, 0.0};
 #pragma unroll
       for (int b = 0; b < NN; ++b)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) ug[i] = fma(c_N[R][g][b], u[b][i], ug[i]);
-#pragma unroll
-      for (int a = 0; a < NN; ++a) {
-        const double wn = c_w[R][g] * c_N[R][g][a];
-#pragma unroll
-        for (int i = 0; i < 3; ++i) mv[a][i] = fma(wn, ug[i], mv[a][i]);
-      }
-    }
-    const double rdet = ph.rho * adet;
-#pragma unroll
-    for (int a = 0; a < NN; ++a)
+        for (int i = 0; i < 3; ++i) m[i] = fma(c_M[R][a][b], u[b][i], m[i]);
+      double r[3];
 #pragma unroll
       for (int i = 0; i < 3; ++i) {
-        double cv = A[i][0] * mv[a][0] + A[i][1] * mv[a][1] + A[i][2] * mv[a][2];
-        double vs = sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
-        r[a][i] = -(rdet * cv + vs);
+        const double cv = A[i][0] * m[0] + A[i][1] * m[1] + A[i][2] * m[2];
+        const double vs = sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
+        r[i] = -(rdet * cv + vs);
       }
+      emit(a, r);
+    }
   } else {
+    double r[NN][3];
+#pragma unroll
+    for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
     double delta2 = 0.0;
     if (ph.c_vreman > 0.0) {
       double vol = 0.0;
@@ -508,6 +505,8 @@ __device__ __forceinline__ void momentum_element(const ab_phys ph, const double 
         for (int i = 0; i < 3; ++i)
           r[a][i] -= c_N[R][g][a] * cv[i] + sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
     }
+#pragma unroll
+    for (int a = 0; a < NN; ++a) emit(a, r[a]);
   }
 }
 
@@ -530,14 +529,18 @@ __global__ void __launch_bounds__(BLOCK) k_momentum(CatP c, ab_phys ph, const do
     if constexpr (WIN) {
       win_element<NN, 6>(w, cx, sm, x, u);
       unwrap<NN>(c, x);
-      momentum_element<R, NN>(ph, x, u, r);
+      momentum_element<R, NN>(ph, x, u, [&](int a, const double (&v)[3]) {
+        r[a][0] = v[0]; r[a][1] = v[1]; r[a][2] = v[2];
+      });
     } else {
       int nd[NN];
       load_conn<NN>(c.conn, e, nd);
       load_coords<NN>(c, nd, x);
       load_vec<NN>(u4, nd, u);
-      momentum_element<R, NN>(ph, x, u, r);
-      scatter_direct<NN, 3, 4>(rhs4, nd, r);
+      momentum_element<R, NN>(ph, x, u, [&](int a, const double (&v)[3]) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) red_add(rhs4 + 4 * (int64_t)nd[a] + i, v[i]);
+      });
     }
   }
   if constexpr (WIN) win_scatter<NN, 3, 4, BLOCK>(rhs4, w, cx, sm + (size_t)w.wmax * 6, r);
@@ -664,6 +667,318 @@ __global__ void __launch_bounds__(BLOCK) k_gradient(CatP c, const double* __rest
   if constexpr (WIN) win_scatter<NN, 3, 4, BLOCK>(out4, w, cx, sm + (size_t)w.wmax * 4, r);
 }
 
+
+// ---------------------------------------------------------------------------
+// Pipelined windowed element kernels.  Persistent CTAs walk the element
+// blocks b = blockIdx.x, +gridDim.x, ... with a two-stage shared-memory
+// pipeline:
+//   * the block's window metadata (node ids, slot ranges, slot lists, the
+//     elements' window-local indices) is contiguous in HBM and arrives by
+//     bulk async copies (cp.async.bulk -> UBLKCP, mbarrier completion), two
+//     blocks ahead;
+//   * the window's node data (coordinates + field) is gathered with
+//     cp.async (LDGSTS) one block ahead, straight into SoA shared memory;
+//   * the current block is computed from shared memory and reduced per
+//     window node into global memory (one fp64 RED per node and component).
+// Latency of both loads is therefore hidden behind the FP64 work of the
+// previous block instead of serialising the phases of every block.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init1(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "PW_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra PW_%=;\n}\n" ::"r"(su32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   su32(dst)),
+               "l"(src), "r"(bytes), "r"(su32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// Byte range [lo, hi) of a global array, widened to 16-byte alignment for a
+// bulk copy; returns the element offset of `lo` inside the copied chunk.
+struct Chunk { const char* src; uint32_t bytes; uint32_t skip; };
+__device__ __forceinline__ Chunk chunk16(const void* base, int64_t lo_elem, int64_t hi_elem, int es) {
+  const uint64_t lo = (uint64_t)base + (uint64_t)lo_elem * es;
+  const uint64_t hi = (uint64_t)base + (uint64_t)hi_elem * es;
+  const uint64_t a = lo & ~(uint64_t)15;
+  const uint64_t b = (hi + 15) & ~(uint64_t)15;
+  return Chunk{reinterpret_cast<const char*>(a), (uint32_t)(b - a), (uint32_t)((lo - a) / es)};
+}
+
+// Shared-memory layout: 3 metadata stages, 2 node-data stages, 1 slot buffer.
+template <int NN, int NV, int BLOCK>
+struct PipeSmem {
+  static __host__ __device__ size_t wcap(int wmax) { return ((size_t)wmax + 8 + 3) & ~(size_t)3; }
+  static __host__ __device__ size_t meta_bytes(int wmax) {
+    return wcap(wmax) * 4 + (wcap(wmax) + 4) * 4 + (size_t)BLOCK * NN * 2 + ((size_t)BLOCK * NN + 16) * 2;
+  }
+  static __host__ __device__ size_t node_bytes(int wmax) { return (size_t)NV * wmax * 8; }
+  static __host__ __device__ size_t slot_bytes() { return sizeof(double) * 3 * NN * BLOCK; }
+  static __host__ __device__ size_t total(int wmax) {
+    return 3 * meta_bytes(wmax) + 2 * node_bytes(wmax) + slot_bytes();
+  }
+};
+
+struct MetaPtr {
+  int32_t* wnode;
+  int32_t* wptr;
+  uint16_t* loc;
+  uint16_t* wslot;
+};
+
+template <int NN, int NV, int BLOCK>
+__device__ __forceinline__ MetaPtr meta_ptr(unsigned char* smem, int wmax, int q) {
+  using L = PipeSmem<NN, NV, BLOCK>;
+  unsigned char* base = smem + (size_t)q * L::meta_bytes(wmax);
+  const size_t wn = L::wcap(wmax) * 4, wp = (L::wcap(wmax) + 4) * 4, lc = (size_t)BLOCK * NN * 2;
+  MetaPtr m;
+  m.wnode = reinterpret_cast<int32_t*>(base);
+  m.wptr = reinterpret_cast<int32_t*>(base + wn);
+  m.loc = reinterpret_cast<uint16_t*>(base + wn + wp);
+  m.wslot = reinterpret_cast<uint16_t*>(base + wn + wp + lc);
+  return m;
+}
+
+// Offsets of a block's data inside its (16-byte widened) metadata chunks.
+struct BlockView {
+  int nw, s_lo, skip_wnode, skip_wptr, skip_wslot;
+};
+__device__ __forceinline__ BlockView block_view(const WinP& w, int4 d) {
+  BlockView v;
+  v.nw = d.y - d.x;
+  v.s_lo = d.z;
+  v.skip_wnode = (int)((((uint64_t)w.wnode + (uint64_t)d.x * 4) & 15) / 4);
+  v.skip_wptr = (int)((((uint64_t)w.wptr + (uint64_t)d.x * 4) & 15) / 4);
+  v.skip_wslot = (int)((((uint64_t)w.wslot + (uint64_t)d.z * 2) & 15) / 2);
+  return v;
+}
+
+// Elected thread: bulk-copy the metadata of element block b.
+template <int NN>
+__device__ __forceinline__ void issue_meta(const WinP& w, int64_t n_elem, int64_t b, int4 d, const MetaPtr& m,
+                                           uint64_t* bar) {
+  const int64_t e0 = b * w.block;
+  const int64_t e1 = e0 + w.block < n_elem ? e0 + w.block : n_elem;
+  const Chunk cw = chunk16(w.wnode, d.x, d.y, 4);
+  const Chunk cp = chunk16(w.wptr, d.x, (int64_t)d.y + 1, 4);
+  const Chunk cs = chunk16(w.wslot, d.z, d.w, 2);
+  const Chunk cl = chunk16(w.loc, e0 * NN, e1 * NN, 2);
+  mbar_arrive_tx(bar, cw.bytes + cp.bytes + cs.bytes + cl.bytes);
+  bulk_copy(m.wnode, cw.src, cw.bytes, bar);
+  bulk_copy(m.wptr, cp.src, cp.bytes, bar);
+  bulk_copy(m.wslot, cs.src, cs.bytes, bar);
+  bulk_copy(m.loc, cl.src, cl.bytes, bar);
+}
+
+// All threads: cp.async gather of a block's window node data (SoA).
+template <int NV, int BLOCK>
+__device__ __forceinline__ void issue_nodes(const CatP& c, const double* __restrict__ f, int wmax, const MetaPtr& m,
+                                            const BlockView& v, double* nodes) {
+  for (int k = threadIdx.x; k < v.nw; k += BLOCK) {
+    const int64_t node = m.wnode[v.skip_wnode + k];
+    const double* xp = c.coords + 4 * node;
+    cp_async8(nodes + k, xp);
+    cp_async8(nodes + wmax + k, xp + 1);
+    cp_async8(nodes + 2 * wmax + k, xp + 2);
+    if constexpr (NV == 6) {
+      const double* up = f + 4 * node;
+      cp_async8(nodes + 3 * wmax + k, up);
+      cp_async8(nodes + 4 * wmax + k, up + 1);
+      cp_async8(nodes + 5 * wmax + k, up + 2);
+    } else {
+      cp_async8(nodes + 3 * wmax + k, f + node);
+    }
+  }
+  cp_async_commit();
+}
+
+enum { OP_MOMENTUM = 0, OP_DIVERGENCE = 1, OP_GRADIENT = 2 };
+
+template <int R, int OP>
+struct OpT;
+template <int R> struct OpT<R, OP_MOMENTUM> { static constexpr int NV = 6, NC = 3, STRIDE = 4; };
+template <int R> struct OpT<R, OP_DIVERGENCE> { static constexpr int NV = 6, NC = 1, STRIDE = 1; };
+template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 3, STRIDE = 4; };
+
+// minimum resident CTAs per SM requested from the register allocator
+template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
+
+// Persistent pipelined element kernel.  Iteration i (element block b_i):
+//   A  wait metadata(b_{i+1}) [mbarrier], cp.async node data(b_{i+1})
+//   B  wait node data(b_i) [cp.async group], __syncthreads; thread 0 then
+//      bulk-copies metadata(b_{i+2}) into the stage of b_{i-1} (free: every
+//      thread finished b_{i-1} before reaching this barrier)
+//   C  elements of b_i -> shared slots, __syncthreads
+//   D  window-node reductions of b_i -> global fp64 REDs
+// Three metadata stages and two node stages make every buffer reuse safe
+// with two CTA barriers per block.
+template <int R, int OP, int BLOCK>
+__global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, WinP w, ab_phys ph, double scale,
+                                                                       const double* __restrict__ f,
+                                                                       double* __restrict__ out, int64_t n_blocks) {
+  constexpr int NN = RuleT<R>::NN;
+  constexpr int NV = OpT<R, OP>::NV, NC = OpT<R, OP>::NC, STRIDE = OpT<R, OP>::STRIDE;
+  using L = PipeSmem<NN, NV, BLOCK>;
+  extern __shared__ __align__(128) unsigned char smem[];
+  __shared__ __align__(8) uint64_t bars[3];
+  const int wmax = w.wmax;
+  double* nodes0 = reinterpret_cast<double*>(smem + 3 * L::meta_bytes(wmax));
+  double* slots = reinterpret_cast<double*>(smem + 3 * L::meta_bytes(wmax) + 2 * L::node_bytes(wmax));
+  const int64_t stride = gridDim.x;
+  const int64_t b_first = blockIdx.x;
+  if (b_first >= n_blocks) return;
+  if (threadIdx.x == 0) {
+    mbar_init1(&bars[0]);
+    mbar_init1(&bars[1]);
+    mbar_init1(&bars[2]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // block descriptors (16 B each) of the current and the next two blocks
+  int4 d0 = __ldg(w.desc + b_first);
+  int4 d1 = b_first + stride < n_blocks ? __ldg(w.desc + b_first + stride) : d0;
+  int4 d2 = b_first + 2 * stride < n_blocks ? __ldg(w.desc + b_first + 2 * stride) : d0;
+  if (threadIdx.x == 0) {
+    issue_meta<NN>(w, c.n, b_first, d0, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), &bars[0]);
+    if (b_first + stride < n_blocks)
+      issue_meta<NN>(w, c.n, b_first + stride, d1, meta_ptr<NN, NV, BLOCK>(smem, wmax, 1), &bars[1]);
+  }
+  mbar_wait_parity(&bars[0], 0);
+  issue_nodes<NV, BLOCK>(c, f, wmax, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), block_view(w, d0), nodes0);
+
+  int it = 0;
+  for (int64_t b = b_first; b < n_blocks; b += stride, ++it) {
+    const int mq = it % 3, mq1 = (it + 1) % 3, mq2 = (it + 2) % 3;
+    double* nodes_cur = nodes0 + (size_t)(it & 1) * NV * wmax;
+    double* nodes_nxt = nodes0 + (size_t)((it + 1) & 1) * NV * wmax;
+    const int64_t b2 = b + 2 * stride, b3 = b + 3 * stride;
+    const int4 d3 = b3 < n_blocks ? __ldg(w.desc + b3) : d0;  // lands during this block
+    // A: node data of the next block
+    if (b + stride < n_blocks) {
+      mbar_wait_parity(&bars[mq1], (uint32_t)(((it + 1) / 3) & 1));
+      issue_nodes<NV, BLOCK>(c, f, wmax, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq1), block_view(w, d1), nodes_nxt);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    __syncthreads();  // B
+    if (threadIdx.x == 0 && b2 < n_blocks) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_meta<NN>(w, c.n, b2, d2, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq2), &bars[mq2]);
+    }
+    // C: elements of this block
+    const MetaPtr mc = meta_ptr<NN, NV, BLOCK>(smem, wmax, mq);
+    const BlockView vc = block_view(w, d0);
+    const int64_t e = b * BLOCK + threadIdx.x;
+    if (e < c.n) {
+      double x[NN][3], fv[NN][NV == 6 ? 3 : 1];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        const int l = mc.loc[threadIdx.x * NN + a];
+        x[a][0] = nodes_cur[l];
+        x[a][1] = nodes_cur[wmax + l];
+        x[a][2] = nodes_cur[2 * wmax + l];
+        if constexpr (NV == 6) {
+          fv[a][0] = nodes_cur[3 * wmax + l];
+          fv[a][1] = nodes_cur[4 * wmax + l];
+          fv[a][2] = nodes_cur[5 * wmax + l];
+        } else {
+          fv[a][0] = nodes_cur[3 * wmax + l];
+        }
+      }
+      unwrap<NN>(c, x);
+      if constexpr (OP == OP_MOMENTUM) {
+        momentum_element<R, NN>(ph, x, fv, [&](int a, const double (&v)[3]) {
+#pragma unroll
+          for (int k = 0; k < 3; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = v[k];
+        });
+      } else {
+        double r[NN][NC];
+#pragma unroll
+        for (int a = 0; a < NN; ++a)
+#pragma unroll
+          for (int k = 0; k < NC; ++k) r[a][k] = 0.0;
+        if constexpr (OP == OP_DIVERGENCE) divergence_element<R, NN>(scale, x, fv, r);
+        if constexpr (OP == OP_GRADIENT) gradient_element<R, NN>(scale, x, fv, r);
+#pragma unroll
+        for (int a = 0; a < NN; ++a)
+#pragma unroll
+          for (int k = 0; k < NC; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = r[a][k];
+      }
+    } else {
+#pragma unroll
+      for (int a = 0; a < NN; ++a)
+#pragma unroll
+        for (int k = 0; k < NC; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = 0.0;
+    }
+    __syncthreads();
+    // D: ordered per-window-node sums, one fp64 reduction per component
+    for (int k = threadIdx.x; k < vc.nw; k += BLOCK) {
+      const int node = mc.wnode[vc.skip_wnode + k];
+      const int s0 = mc.wptr[vc.skip_wptr + k] - vc.s_lo, s1 = mc.wptr[vc.skip_wptr + k + 1] - vc.s_lo;
+      double acc[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc[q] = 0.0;
+      for (int t = s0; t < s1; ++t) {
+        const int slot = mc.wslot[vc.skip_wslot + t];
+        const int a = slot % NN, el = slot / NN;
+#pragma unroll
+        for (int q = 0; q < NC; ++q) acc[q] += slots[(q * NN + a) * BLOCK + el];
+      }
+#pragma unroll
+      for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+    }
+    d0 = d1;
+    d1 = d2;
+    d2 = d3;
+  }
+}
+
+template <int R, int OP, int BLOCK>
+static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double scale, const double* f, double* out,
+                       cudaStream_t stream) {
+  constexpr int NN = RuleT<R>::NN;
+  constexpr int NV = OpT<R, OP>::NV;
+  using L = PipeSmem<NN, NV, BLOCK>;
+  const size_t smem = L::total(w.wmax);
+  auto kern = k_pipe<R, OP, BLOCK>;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail("pipelined element kernel: shared memory request rejected");
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, BLOCK, smem);
+  if (per_sm < 1) return fail("pipelined element kernel does not fit on an SM");
+  const int64_t n_blocks = (c.n + BLOCK - 1) / BLOCK;
+  int64_t grid = (int64_t)sms * per_sm;
+  if (grid > n_blocks) grid = n_blocks;
+  kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w, ph, scale, f, out, n_blocks);
+  return check_launch("k_pipe");
+}
 // ---------------------------------------------------------------------------
 // Laplacian values into a CSR pattern (setup)
 // ---------------------------------------------------------------------------
@@ -810,8 +1125,9 @@ extern "C" {
 
 // Register (or clear with blk_ptr == NULL) the node windows of a category.
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
-                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, int32_t wmax) {
-  const WinP wp{blk_ptr, wnode, wptr, wslot, loc, block, wmax};
+                   const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, const int32_t* desc,
+                   int32_t wmax) {
+  const WinP wp{blk_ptr, wnode, wptr, wslot, loc, reinterpret_cast<const int4*>(desc), block, wmax};
   for (int i = 0; i < g_nwin; ++i)
     if (g_win[i].conn == conn) {
       if (!blk_ptr) { g_win[i] = g_win[--g_nwin]; return AB_OK; }
@@ -856,6 +1172,10 @@ int ab_momentum_rhs(const ab_mesh* m, const ab_phys* ph, const double* u4, doubl
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
+      if (win && w.desc) {
+        if (int rc = launch_pipe<R, OP_MOMENTUM, kBlock>(c, w, *ph, 1.0, u4, rhs4, S(stream))) return rc;
+        return AB_OK;
+      }
       if (win) {
         size_t sm = sizeof(double) * ((size_t)w.wmax * 6 + kBlock * NN * 3);
         if (int rc = ensure_smem(k_momentum<R, kBlock, true>, sm)) return rc;
@@ -880,6 +1200,11 @@ int ab_divergence(const ab_mesh* m, const double* u4, double scale, double* out,
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
+      if (win && w.desc) {
+        ab_phys ph{};
+        if (int rc = launch_pipe<R, OP_DIVERGENCE, kBlock>(c, w, ph, scale, u4, out, S(stream))) return rc;
+        return AB_OK;
+      }
       if (win) {
         const size_t sm = sizeof(double) * ((size_t)w.wmax * 6 + kBlock * NN);
         if (int rc = ensure_smem(k_divergence<R, kBlock, true>, sm)) return rc;
@@ -904,6 +1229,11 @@ int ab_gradient(const ab_mesh* m, const double* p, double scale, double* out4, v
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       constexpr int R = decltype(r)::value;
       constexpr int NN = RuleT<R>::NN;
+      if (win && w.desc) {
+        ab_phys ph{};
+        if (int rc = launch_pipe<R, OP_GRADIENT, kBlock>(c, w, ph, scale, p, out4, S(stream))) return rc;
+        return AB_OK;
+      }
       if (win) {
         const size_t sm = sizeof(double) * ((size_t)w.wmax * 4 + kBlock * NN * 3);
         if (int rc = ensure_smem(k_gradient<R, kBlock, true>, sm)) return rc;

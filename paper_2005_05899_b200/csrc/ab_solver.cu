@@ -244,6 +244,16 @@ namespace cg = cooperative_groups;
 constexpr int kResBlock = 1024;
 constexpr int kResQ = 8;  // max slices per warp
 
+// Bulk prefetch of one SELL slice (column indices + values) into L2.
+__device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, const int32_t* scol,
+                                               const double* sval, int64_t s) {
+  const int64_t b = sp[s];
+  const uint32_t cnt = (uint32_t)(sp[s + 1] - b);
+  if (cnt == 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + b), "r"(cnt * 4u) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
+}
+
 __device__ __forceinline__ double2 block_sum2(double a, double b, double* sm) {
   double v[2] = {a, b};
   block_sum<2, kResBlock>(v, sm);
@@ -327,10 +337,14 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
     const double2* zin2 = reinterpret_cast<const double2*>(zin);
     // ---- phase A: q = A (z + beta p_old), p = z + beta p_old
     double pq = 0.0;
+    if (it == 0 && lane == 0 && warp < nsl) prefetch_slice(sp, scol, sval, s_first + warp);
 #pragma unroll 1
     for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
       {
         const int64_t s = s_first + sl;
+        // the TMA engine pulls the warp's next slice into L2 while this one
+        // is gathered, so the next iteration's matrix loads hit L2
+        if (lane == 0 && sl + kResBlock / 32 < nsl) prefetch_slice(sp, scol, sval, s + kResBlock / 32);
         const int64_t base = sp[s] + lane;
         const int width = (int)((sp[s + 1] - sp[s]) >> 5);
         double acc = 0.0;
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
           }
           double2 g[kChunk];
 #pragma unroll
-          for (int u = 0; u < kChunk; ++u) g[u] = __ldcg(zin2 + c[u]);
+          for (int u = 0; u < kChunk; ++u) g[u] = zin2[c[u]];  // written last phase: coherent after grid.sync
 #pragma unroll
           for (int u = 0; u < kChunk; ++u) acc = fma(a[u], fma(beta, g[u].y, g[u].x), acc);
         }
@@ -369,6 +383,8 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
     all_sum<1>(partA, nb, bcast, t1);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
+    // (first two slices of the next iteration go to L2 meanwhile)
+    if (lane == 0 && it + 1 < maxit && warp < nsl) prefetch_slice(sp, scol, sval, s_first + warp);
     double b0 = 0.0, b1 = 0.0;
     for (int l = threadIdx.x; l < nloc; l += kResBlock) {
       {

@@ -23,7 +23,8 @@ WINDOW_BLOCK = 128
 
 
 class DeviceMesh:
-    def __init__(self, mesh: MeshArrays, device="cuda", reorder: str | None = None, windows: bool = False):
+    def __init__(self, mesh: MeshArrays, device="cuda", reorder: str | None = None, windows: bool = False,
+                 pipelined: bool = True):
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceMesh needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device(device)
@@ -39,6 +40,7 @@ class DeviceMesh:
             self.conn.append(torch.from_numpy(np.ascontiguousarray(conn, dtype=np.int32)).to(self.device))
             self.ids.append(torch.from_numpy(np.asarray(ids, dtype=np.int64)).to(self.device))
         self._win = []
+        self.pipelined = pipelined
         self._build_struct()
         if reorder == "sfc":
             self.reorder_sfc()
@@ -132,9 +134,16 @@ class DeviceMesh:
             loc[order] = local
             loc = loc.to(torch.int16).reshape(E, nn).contiguous()
             wmax = int((blk_ptr[1:] - blk_ptr[:-1]).max().item())
-            w = (blk_ptr, wnode, wptr, wslot, loc, wmax)
+            # per-block descriptors for the pipelined kernels
+            b0, b1 = blk_ptr[:-1], blk_ptr[1:]
+            desc = torch.stack([b0, b1, wptr[b0].to(torch.int64), wptr[b1].to(torch.int64)], dim=1)
+            desc = desc.to(torch.int32).contiguous()
+            # bulk copies read whole 16-byte granules: pad every array
+            wnode, wptr, wslot, loc = (_padded(t) for t in (wnode, wptr, wslot, loc))
+            w = (blk_ptr, wnode, wptr, wslot, loc, wmax, desc)
             self._win.append(w)
-            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot), ptr(loc), wmax)
+            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot), ptr(loc),
+                 ptr(desc) if self.pipelined else None, wmax)
         self.windows = True
 
     def window_stats(self):
@@ -149,7 +158,7 @@ class DeviceMesh:
     def clear_windows(self):
         for conn, w in zip(self.conn, self._win):
             if w is not None:
-                call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None, None, 0)
+                call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None, None, None, 0)
         self._win = []
         self.windows = False
 
@@ -158,6 +167,16 @@ class DeviceMesh:
             self.clear_windows()
         except Exception:
             pass
+
+
+def _padded(t: torch.Tensor) -> torch.Tensor:
+    """Copy of a 1D/2D tensor with 64 spare bytes behind its data (views keep
+    the original shape)."""
+    flat = t.reshape(-1)
+    extra = max(1, 64 // flat.element_size())
+    buf = torch.zeros(flat.numel() + extra, dtype=flat.dtype, device=flat.device)
+    buf[: flat.numel()] = flat
+    return buf[: flat.numel()].view(t.shape)
 
 
 def C_ref(struct):

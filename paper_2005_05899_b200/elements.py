@@ -168,6 +168,18 @@ def emit_tables(path: Path | None = None) -> str:
             gs.append("{" + ", ".join(aa) + "}")
         lines.append("  {" + ", ".join(gs) + "},")
     lines.append("};")
+    # M[rule][a][b] = sum_g w_g N_a(g) N_b(g): reference-element mass table,
+    # used by the affine (tet) momentum kernel (sum_g w N_a u_g = sum_b M_ab u_b)
+    lines.append("__constant__ double c_M[5][8][8] = {")
+    for name in RULE_NAMES:
+        N, w = Ns[name], RULES[name].weights
+        M = (N * w[None, :]) @ N.T
+        rows = []
+        for a in range(8):
+            vals = [float(M[a, b]) if (a < M.shape[0] and b < M.shape[1]) else 0.0 for b in range(8)]
+            rows.append("{" + ", ".join(repr(v) for v in vals) + "}")
+        lines.append("  {" + ", ".join(rows) + "},")
+    lines.append("};")
     text = "\n".join(lines) + "\n"
     if path is not None:
         Path(path).write_text(text)

@@ -37,29 +37,36 @@ def _field(m, seed=0):
     return u + 0.1 * rng.standard_normal(u.shape), np.cos(2 * x[:, 0] + x[:, 1]) + rng.standard_normal(len(x)) * 0.1
 
 
-@pytest.mark.parametrize("name", list(MESHES))
-@pytest.mark.parametrize("windows", [False, True])
-@pytest.mark.parametrize("c_vreman", [0.0, 0.07])
-def test_momentum_rhs(name, windows, c_vreman):
+SCATTER = ["direct", "window", "pipelined"]
+
+
+def _dm(m, mode):
     from paper_2005_05899_b200.device import DeviceMesh
+    return DeviceMesh(m, reorder=None if mode == "direct" else "sfc", windows=mode != "direct",
+                      pipelined=mode == "pipelined")
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+@pytest.mark.parametrize("mode", SCATTER)
+@pytest.mark.parametrize("c_vreman", [0.0, 0.07])
+def test_momentum_rhs(name, mode, c_vreman):
     from paper_2005_05899_b200.ops import assemble_momentum
     from paper_2005_05899_b200.timestep import FlowParams
     m = MESHES[name]
     u, _ = _field(m)
     ref = fem.momentum_rhs(m, u, rho=1.3, mu=0.01, c_vreman=c_vreman)
-    dm = DeviceMesh(m, reorder="sfc" if windows else None, windows=windows)
+    dm = _dm(m, mode)
     got = assemble_momentum(dm, u, FlowParams(rho=1.3, mu=0.01, c_vreman=c_vreman)).cpu().numpy()
     assert rel_l2(got, ref) <= TOL_RHS
 
 
 @pytest.mark.parametrize("name", list(MESHES))
-@pytest.mark.parametrize("windows", [False, True])
-def test_divergence_gradient(name, windows):
-    from paper_2005_05899_b200.device import DeviceMesh
+@pytest.mark.parametrize("mode", SCATTER)
+def test_divergence_gradient(name, mode):
     from paper_2005_05899_b200.ops import assemble_divergence, assemble_gradient
     m = MESHES[name]
     u, p = _field(m, 1)
-    dm = DeviceMesh(m, reorder="sfc" if windows else None, windows=windows)
+    dm = _dm(m, mode)
     assert rel_l2(assemble_divergence(dm, u, 2.0).cpu().numpy(), 2.0 * fem.divergence(m, u)) <= TOL_RHS
     assert rel_l2(assemble_gradient(dm, p).cpu().numpy(), fem.gradient(m, p)) <= TOL_RHS
 
