@@ -137,24 +137,24 @@ int ab_csr_to_sell(int64_t n_rows, const int64_t* row_ptr, const int32_t* cols, 
 int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 
 /* ---- K5: Jacobi-PCG kernels --------------------
- * z and the search direction p are stored interleaved as (z, p) pairs
- * [n][2] in two alternating buffers; x, r, q, dinv are [n].  `red` = 8
- * doubles of reduction results, `sc` = 8 doubles of solver scalars, `part`
- * = partial-sum scratch (>= 2*(nb + ng) doubles, nb = ceil(n/256),
+ * Vectors x, r, z, p, q (and t for decomposed domains), dinv are [n].  The
+ * SpMV is applied to z and A p is formed recursively: p = z + beta p_old,
+ * q = A z + beta q_old (one 8-byte gather per non-zero).  `red` = 8 doubles
+ * of reduction results, `sc` = 8 doubles of solver scalars, `part` =
+ * partial-sum scratch (>= 2*(nb + ng) doubles, nb = ceil(n/256),
  * ng = ceil(nb/64)), `cnt` = 1 + ng zero-initialised uint32 counters
- * (two-level deterministic grid reduction, re-armed by the kernels).
- * for the dot products of a decomposed domain.
- *   init:   r = fixed ? 0 : b; b = 0 (if b_zero); x = 0; zp = (dinv r, 0);
+ * (two-level deterministic grid reduction, re-armed by the kernels).  `own`
+ * (nullable) = per-row ownership weights for the dots of a decomposed domain.
+ *   init:   r = fixed ? 0 : b; b = 0 (if b_zero); x = p = q = 0; z = dinv r;
  *           red[RZN] = r.z, red[RR] = r.r, sc[RZ] = 0
  *   set_bb: sc[BB] = red[RR]
- *   spmv:   beta = sc[RZ] ? red[RZN]/sc[RZ] : 0; p = z + beta p_old (from
- *           zp_in); zp_out.p = p; q = A p; if with_dot: red[PQ] = p.q and
- *           sc[RZ] = red[RZN]
- *   dot:    red[PQ] = p.q; sc[RZ] = red[RZN]  (decomposed domains: spmv runs
- *           with with_dot = 0, then the q interface sum, then dot)
+ *   spmv:   with_dot: beta = sc[RZ] ? red[RZN]/sc[RZ] : 0; p = z + beta p;
+ *           q = A z + beta q; red[PQ] = p.q; sc[RZ] = red[RZN]
+ *           !with_dot (decomposed): t = (A z)_local only
+ *   dot:    (after the interface sum of t) p = z + beta p; q = t + beta q;
+ *           red[PQ] = p.q; sc[RZ] = red[RZN]
  *   update: alpha = red[PQ] ? sc[RZ]/red[PQ] : 0; x += alpha p; r -= alpha q;
- *           zp.z = dinv r; red[RZN] = r.z; red[RR] = r.r
- * All sums are deterministic (fixed-order block partials).                */
+ *           z = dinv r; red[RZN] = r.z; red[RR] = r.r                      */
 #define AB_RED_RZN 0
 #define AB_RED_RR 1
 #define AB_RED_PQ 2
@@ -162,27 +162,28 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 #define AB_SC_RZ 0
 #define AB_SC_BB 1
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
-               double* x, double* r, double* zp, const double* own, double* red, double* sc, double* part,
-               uint32_t* cnt, void* stream);
+               double* x, double* r, double* z, double* p, double* q, const double* own, double* red, double* sc,
+               double* part, uint32_t* cnt, void* stream);
 int ab_cg_set_bb(double* red, double* sc, void* stream);
-int ab_cg_spmv(const ab_sell* a, const double* zp_in, double* zp_out, double* q, int32_t with_dot,
+int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
                const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);
-int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, double* red, double* sc,
-              double* part, uint32_t* cnt, void* stream);
-int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r,
+int ab_cg_dot(int64_t n, const double* z, const double* t, double* p, double* q, const double* own, double* red,
+              double* sc, double* part, uint32_t* cnt, void* stream);
+int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r, double* z,
                  const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
 
 /* Resident CG: init + up to `maxit` iterations (stop when ||r||/||b|| <=
  * tol, tested on the device; tol = 0 runs exactly maxit) in one cooperative
- * kernel with one CTA per SM; each CTA keeps x, r, z, p, D^-1 of its rows in
+ * kernel with one CTA per SM; each CTA keeps x, r, z, p, q of its rows in
  * shared memory.  Same iterates as the kernels above.
- * Outputs: x; red[RZN], red[RR], red[ITERS]; sc[BB].  `part` >= 5 * n_cta
- * doubles.  ab_cg_resident_fits() returns 1 when n rows fit (and reports the
- * launch shape); ab_cg_resident fails with AB_EINVAL otherwise. */
+ * Outputs: x, z (scratch); red[RZN], red[RR], red[ITERS]; sc[BB].  `part`
+ * >= 5 * n_cta doubles.  ab_cg_resident_fits() returns 1 when n rows fit
+ * (and reports the launch shape); ab_cg_resident fails with AB_EINVAL
+ * otherwise. */
 int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta);
 int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
-                   double* x, double* zpa, double* zpb, int32_t maxit, double tol, double* red, double* sc,
-                   double* part, void* stream);
+                   double* x, double* z, int32_t maxit, double tol, double* red, double* sc, double* part,
+                   void* stream);
 
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */

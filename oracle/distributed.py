@@ -74,10 +74,11 @@ class DistFlowOracle:
         x = np.zeros_like(b)
         rz, rr = self._allsum([float(own @ (r * z)), float(own @ (r * r))])
         p = np.zeros_like(b)
+        q = np.zeros_like(b)
         beta = 0.0
         for _ in range(maxit):
             p = z + beta * p
-            q = self._sum1(self.L @ p)
+            q = self._sum1(self.L @ z) + beta * q
             pq = self._allsum([float(own @ (p * q))])[0]
             alpha = rz / pq if pq != 0.0 else 0.0
             x += alpha * p

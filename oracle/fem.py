@@ -354,7 +354,9 @@ def apply_dirichlet(A, fixed):
 def pcg(A, b, dinv, maxit, tol=0.0, x0=None):
     """Jacobi-preconditioned CG in the exact operation
     order of the fused GPU kernels: the direction update
-    p = z + beta p is evaluated at the start of the next SpMV.
+    p = z + beta p is evaluated at the start of the next SpMV, and the SpMV
+    is applied to the preconditioned residual, q = A p = A z + beta q_old
+    (the recursive form of A p, so only z is gathered by the SpMV).
 
     Stops after ``maxit`` iterations or when ||r||/||b|| <= tol (tol > 0).
     Returns (x, iterations, ||r||/||b||).
@@ -366,13 +368,14 @@ def pcg(A, b, dinv, maxit, tol=0.0, x0=None):
     bb = float(b @ b)
     rr = float(r @ r)
     p = np.zeros_like(b)
+    q = np.zeros_like(b)
     beta = 0.0
     it = 0
     while it < maxit:
         if tol > 0 and bb > 0 and math.sqrt(rr / bb) <= tol:
             break
         p = z + beta * p
-        q = A @ p
+        q = A @ z + beta * q
         pq = float(p @ q)
         alpha = rz / pq if pq != 0.0 else 0.0
         x += alpha * p

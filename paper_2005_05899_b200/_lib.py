@@ -52,13 +52,13 @@ _SIGS = {
     "ab_csr_dirichlet": ([i64, vp, vp, vp, vp, vp], C.c_int),
     "ab_csr_to_sell": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
-    "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
-    "ab_cg_spmv": ([P(AbSell), vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
-    "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
-    "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_resident_fits": ([i64, vp, vp], C.c_int),
-    "ab_cg_resident": ([P(AbSell), vp, vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp], C.c_int),
+    "ab_cg_resident": ([P(AbSell), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp], C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),

@@ -67,20 +67,22 @@ __global__ void k_sell_spmv(int64_t n, const int64_t* __restrict__ sp, const int
 }
 
 // ---------------------------------------------------------------------------
-// CG kernels.  z and the search direction p live interleaved as (z, p) pairs
-// so the SpMV gathers both with one 16-byte load per non-zero; two pair
-// buffers alternate between iterations.  All kernels are
-// grid-stride with at most kCgGrid blocks so the deterministic block
-// reduction is amortised over several rows per thread.
+// CG kernels.  The SpMV is applied to the preconditioned
+// residual z and the product A p is formed recursively,
+//     p = z + beta p_old,   q = A p = A z + beta q_old,
+// so each non-zero costs one 8-byte gather.  All kernels are row-per-thread
+// with deterministic two-level grid reductions; alpha and beta are formed on
+// the device from the reduction slots, so the loop never synchronises with
+// the host.
 // ---------------------------------------------------------------------------
 constexpr int kCgGrid = 148 * 8;
-
-__device__ __forceinline__ double2 ld2_nc(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+constexpr int kChunk = 16;
 
 __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* __restrict__ b_in, double* b_zero,
                                                       const uint8_t* __restrict__ fixed,
                                                       const double* __restrict__ dinv, double* __restrict__ x,
-                                                      double* __restrict__ r, double* __restrict__ zp,
+                                                      double* __restrict__ r, double* __restrict__ z,
+                                                      double* __restrict__ p, double* __restrict__ q,
                                                       const double* __restrict__ own, double* red, double* sc,
                                                       double* part, uint32_t* cnt) {
   double v[2] = {0.0, 0.0};
@@ -90,8 +92,10 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* _
     if (b_zero) b_zero[i] = 0.0;
     const double zi = dinv[i] * ri;
     r[i] = ri;
+    z[i] = zi;
     x[i] = 0.0;
-    reinterpret_cast<double2*>(zp)[i] = make_double2(zi, 0.0);
+    p[i] = 0.0;
+    q[i] = 0.0;
     const double w = own ? own[i] : 1.0;
     v[0] += w * ri * zi;
     v[1] += w * ri * ri;
@@ -107,142 +111,154 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* _
 // Copy red[RR] -> sc[BB] after the (optionally all-reduced) init sums.
 __global__ void k_cg_set_bb(const double* red, double* sc) { sc[AB_SC_BB] = red[AB_RED_RR]; }
 
-// q = A (z + beta p_old); p_new -> zp_out[i].p; optional p.q partials.
-// One row per thread.  Each chunk of up to kChunk non-zeros issues all its
-// column/value loads, then all (z, p) gathers, then the FMAs, so a row costs
-// two memory latencies per chunk instead of two per non-zero; the scalar
-// division for beta is placed after the first loads are in flight.
-constexpr int kChunk = 16;
+// (A z)_i for one SELL row: all column/value loads of a 16-wide chunk first,
+// then the gathers, then the FMAs.
+__device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
+                                               const double* __restrict__ sval, const double* zv, int64_t i) {
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t base = sp[s] + lane;
+  const int width = (int)((sp[s + 1] - sp[s]) >> 5);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < width; j0 += kChunk) {
+    int c[kChunk];
+    double a[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      const bool ok = j0 + u < width;
+      c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
+      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+    }
+    double g[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) g[u] = zv[c[u]];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) acc = fma(a[u], g[u], acc);
+  }
+  return acc;
+}
 
+// Single domain (DOT): p = z + beta p, q = A z + beta q, p.q partials, then
+// sc[RZ] := red[RZN].  Decomposed (!DOT): t = (A z)_local only; the
+// interface sum of t and k_cg_dot follow.
 template <bool DOT>
 __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* __restrict__ sp,
                                                       const int32_t* __restrict__ scol,
-                                                      const double* __restrict__ sval,
-                                                      const double* __restrict__ zp_in, double* __restrict__ zp_out,
-                                                      double* __restrict__ q, const double* __restrict__ own,
+                                                      const double* __restrict__ sval, const double* __restrict__ z,
+                                                      double* __restrict__ p, double* __restrict__ q,
+                                                      double* __restrict__ t, const double* __restrict__ own,
                                                       double* red, double* sc, double* part, uint32_t* cnt) {
   const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
-  const double2* zp2 = reinterpret_cast<const double2*>(zp_in);
   const double rz_old = sc[AB_SC_RZ];
   const double rz_new = red[AB_RED_RZN];
   const double beta = rz_old != 0.0 ? rz_new / rz_old : 0.0;
   double v[1] = {0.0};
   if (i < n) {
-    const int64_t s = i >> 5;
-    const int lane = (int)(i & 31);
-    const int64_t base = sp[s] + lane;
-    const int width = (int)((sp[s + 1] - sp[s]) >> 5);
-    double acc = 0.0;
-    for (int j0 = 0; j0 < width; j0 += kChunk) {
-      int c[kChunk];
-      double a[kChunk];
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u) {
-        const bool ok = j0 + u < width;
-        c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
-        a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
-      }
-      double2 g[kChunk];
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u) g[u] = __ldg(zp2 + c[u]);
-#pragma unroll
-      for (int u = 0; u < kChunk; ++u) acc = fma(a[u], fma(beta, g[u].y, g[u].x), acc);
+    const double az = sell_row_dot(sp, scol, sval, z, i);
+    if (DOT) {
+      const double pi = fma(beta, p[i], z[i]);
+      const double qi = fma(beta, q[i], az);
+      p[i] = pi;
+      q[i] = qi;
+      v[0] = (own ? own[i] : 1.0) * pi * qi;
+    } else {
+      t[i] = az;
     }
-    const double2 own_zp = __ldg(zp2 + i);
-    const double pi = fma(beta, own_zp.y, own_zp.x);
-    zp_out[2 * i + 1] = pi;
-    q[i] = acc;
-    if (DOT) v[0] = (own ? own[i] : 1.0) * pi * acc;
   }
   if (DOT) {
-    double t[1];
-    if (grid_sum<1, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
-      red[AB_RED_PQ] = t[0];
+    double tot[1];
+    if (grid_sum<1, kCgBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+      red[AB_RED_PQ] = tot[0];
       sc[AB_SC_RZ] = rz_new;
     }
   }
-  // decomposed path (DOT=false): the rz shift is done by k_cg_dot's last block
 }
 
-// p.q after the interface sum of q (decomposed path); the last block also
-// performs the rz shift that k_cg_spmv<true> does in the single-domain path.
-__global__ void __launch_bounds__(kCgBlock) k_cg_dot(int64_t n, const double* __restrict__ zp,
-                                                     const double* __restrict__ q, const double* __restrict__ own,
+// Decomposed path, after the interface sum of t = A z: p = z + beta p,
+// q = t + beta q, p.q partials; the last block shifts sc[RZ] := red[RZN].
+__global__ void __launch_bounds__(kCgBlock) k_cg_dot(int64_t n, const double* __restrict__ z,
+                                                     const double* __restrict__ t, double* __restrict__ p,
+                                                     double* __restrict__ q, const double* __restrict__ own,
                                                      double* red, double* sc, double* part, uint32_t* cnt) {
+  const double rz_old = sc[AB_SC_RZ];
+  const double rz_new = red[AB_RED_RZN];
+  const double beta = rz_old != 0.0 ? rz_new / rz_old : 0.0;
   double v[1] = {0.0};
-  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock)
-    v[0] += (own ? own[i] : 1.0) * zp[2 * i + 1] * q[i];
-  double t[1];
-  if (grid_sum<1, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
-    red[AB_RED_PQ] = t[0];
-    sc[AB_SC_RZ] = red[AB_RED_RZN];
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
+    const double pi = fma(beta, p[i], z[i]);
+    const double qi = fma(beta, q[i], t[i]);
+    p[i] = pi;
+    q[i] = qi;
+    v[0] += (own ? own[i] : 1.0) * pi * qi;
+  }
+  double tot[1];
+  if (grid_sum<1, kCgBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_PQ] = tot[0];
+    sc[AB_SC_RZ] = rz_new;
   }
 }
 
-// x += alpha p; r -= alpha q; z = dinv r (-> zp[i].z); r.z and r.r partials.
-// Two consecutive rows per thread with 128/256-bit accesses (n even is not
-// required: the odd tail row is handled by the scalar path).
-__global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, double* __restrict__ zp,
+// x += alpha p; r -= alpha q; z = dinv r; r.z and r.r partials.  Two
+// consecutive rows per thread with 128-bit accesses.
+__global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, const double* __restrict__ p,
                                                         const double* __restrict__ q,
                                                         const double* __restrict__ dinv, double* __restrict__ x,
-                                                        double* __restrict__ r, const double* __restrict__ own,
-                                                        double* red, const double* sc, double* part, uint32_t* cnt) {
+                                                        double* __restrict__ r, double* __restrict__ z,
+                                                        const double* __restrict__ own, double* red,
+                                                        const double* sc, double* part, uint32_t* cnt) {
   double v[2] = {0.0, 0.0};
   const int64_t i = 2 * ((int64_t)blockIdx.x * kCgBlock + threadIdx.x);
   const double pq = red[AB_RED_PQ];
   const double rz = sc[AB_SC_RZ];
   if (i + 1 < n) {
-    const d4 zpv = ld4(zp + 2 * i);  // (z0, p0, z1, p1)
+    const double2 pv = *reinterpret_cast<const double2*>(p + i);
     const double2 xv = *reinterpret_cast<const double2*>(x + i);
-    const double2 qv = __ldcs(reinterpret_cast<const double2*>(q + i));
+    const double2 qv = *reinterpret_cast<const double2*>(q + i);
     const double2 rv = *reinterpret_cast<const double2*>(r + i);
     const double2 dv = __ldg(reinterpret_cast<const double2*>(dinv + i));
     const double alpha = pq != 0.0 ? rz / pq : 0.0;
     const double r0 = fma(-alpha, qv.x, rv.x), r1 = fma(-alpha, qv.y, rv.y);
     const double z0 = dv.x * r0, z1 = dv.y * r1;
-    *reinterpret_cast<double2*>(x + i) = make_double2(fma(alpha, zpv.y, xv.x), fma(alpha, zpv.w, xv.y));
+    *reinterpret_cast<double2*>(x + i) = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
     *reinterpret_cast<double2*>(r + i) = make_double2(r0, r1);
-    st4(zp + 2 * i, d4{z0, zpv.y, z1, zpv.w});
+    *reinterpret_cast<double2*>(z + i) = make_double2(z0, z1);
     double w0 = 1.0, w1 = 1.0;
     if (own) { w0 = own[i]; w1 = own[i + 1]; }
     v[0] = w0 * r0 * z0 + w1 * r1 * z1;
     v[1] = w0 * r0 * r0 + w1 * r1 * r1;
   } else if (i < n) {
     const double alpha = pq != 0.0 ? rz / pq : 0.0;
-    const double pi = zp[2 * i + 1];
-    x[i] = fma(alpha, pi, x[i]);
+    x[i] = fma(alpha, p[i], x[i]);
     const double ri = fma(-alpha, q[i], r[i]);
     const double zi = dinv[i] * ri;
     r[i] = ri;
-    zp[2 * i] = zi;
+    z[i] = zi;
     const double w = own ? own[i] : 1.0;
     v[0] = w * ri * zi;
     v[1] = w * ri * ri;
   }
-  double t[2];
-  if (grid_sum<2, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
-    red[AB_RED_RZN] = t[0];
-    red[AB_RED_RR] = t[1];
+  double tot[2];
+  if (grid_sum<2, kCgBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = tot[0];
+    red[AB_RED_RR] = tot[1];
   }
 }
-
 
 // ---------------------------------------------------------------------------
 // Resident CG: the whole solve in ONE cooperative kernel (one CTA per SM).
 // Every CTA owns a contiguous, slice-aligned range of rows and keeps their
-// x, r, z, p and q in shared memory for all iterations (D^-1 is re-read
-// from L2 in phase B).  Per iteration only the
-// matrix is streamed from HBM, the (z, p) pairs of the owned rows are written
-// once for the neighbours' gathers, and the two grid-wide reductions are
-// deterministic (per-CTA partials, every CTA sums them in index order after a
-// grid barrier).  Convergence (tol > 0) is tested on the device, uniformly
-// in all CTAs, so even a tolerance-driven solve never returns to the host.
-// Used when the owned rows fit in shared memory (C2: 4768 rows x 40 B per SM);
-// otherwise the two-kernel path above runs.
+// x, r, z, p and q in shared memory for all iterations (D^-1 is re-read from
+// L2 in phase B); only z goes to global memory, for the neighbours' gathers.
+// Per iteration the matrix is streamed (the next slice of every warp is
+// bulk-prefetched into L2 by the TMA engine while the current one is
+// gathered) and the two grid-wide reductions are deterministic (per-CTA
+// partials, summed in index order by every CTA after a grid barrier).
+// Convergence (tol > 0) is tested on the device, identically in all CTAs.
+// Used when the owned rows fit in shared memory (C2: 4768 rows x 40 B per
+// SM); otherwise the kernels above run.
 // ---------------------------------------------------------------------------
 namespace cg = cooperative_groups;
 constexpr int kResBlock = 1024;
-constexpr int kResQ = 8;  // max slices per warp
 
 // Bulk prefetch of one SELL slice (column indices + values) into L2.
 __device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, const int32_t* scol,
@@ -254,14 +270,8 @@ __device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, c
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
 }
 
-__device__ __forceinline__ double2 block_sum2(double a, double b, double* sm) {
-  double v[2] = {a, b};
-  block_sum<2, kResBlock>(v, sm);
-  return make_double2(v[0], v[1]);  // valid in warp 0
-}
-
-// Ordered sum of nb per-CTA partials (NV values each, layout part[k*nb+b]);
-// identical in every CTA.  Result broadcast through shared memory.
+// Ordered sum of nb per-CTA partials (layout part[k*nb+b]); identical in
+// every CTA, broadcast through shared memory.
 template <int NV>
 __device__ __forceinline__ void all_sum(const double* part, int nb, double* bcast, double (&out)[NV]) {
   if (threadIdx.x < 32) {
@@ -283,8 +293,8 @@ __device__ __forceinline__ void all_sum(const double* part, int nb, double* bcas
 __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
     int64_t n, int64_t rows_per_cta, const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
     const double* __restrict__ sval, const double* __restrict__ b_in, double* b_zero, const uint8_t* __restrict__ fixed,
-    const double* __restrict__ dinv, double* __restrict__ x_out, double* zpa, double* zpb, int maxit, double tol,
-    double* red, double* sc, double* part) {
+    const double* __restrict__ dinv, double* __restrict__ x_out, double* zg, int maxit, double tol, double* red,
+    double* sc, double* part) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
@@ -299,78 +309,56 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
   double* sz = sr + RB;
   double* spp = sz + RB;
   double* sq = spp + RB;
-  double* partA = part;                 // [nb]     p.q
-  double* partB = part + nb;            // [2][nb]  r.z, r.r
+  double* partA = part;                   // [nb]     p.q
+  double* partB = part + nb;              // [2][nb]  r.z, r.r
   double* partI = part + 3 * (size_t)nb;  // [2][nb]  init r.z, r.r
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nsl = (nloc + 31) >> 5;     // slices of this CTA
-  const int64_t s_first = r0 >> 5;      // r0 is slice aligned
+  const int nsl = (nloc + 31) >> 5;
+  const int64_t s_first = r0 >> 5;  // r0 is slice aligned
 
-  // ---- init: r = b (masked), z = D^-1 r, p = 0, x = 0
   double a0 = 0.0, a1 = 0.0;
   for (int l = threadIdx.x; l < nloc; l += kResBlock) {
     const int64_t i = r0 + l;
     double ri = b_in[i];
     if (fixed && fixed[i]) ri = 0.0;
     if (b_zero) b_zero[i] = 0.0;
-    const double d = dinv[i];
-    const double zi = d * ri;
+    const double zi = dinv[i] * ri;
     sx[l] = 0.0; sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
-    reinterpret_cast<double2*>(zpa)[i] = make_double2(zi, 0.0);
+    zg[i] = zi;
     a0 += ri * zi;
     a1 += ri * ri;
   }
-  double2 bs = block_sum2(a0, a1, sred);
-  if (threadIdx.x == 0) { partI[blockIdx.x] = bs.x; partI[nb + blockIdx.x] = bs.y; }
+  {
+    double v[2] = {a0, a1};
+    block_sum<2, kResBlock>(v, sred);
+    if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
+  }
   grid.sync();
   double t2[2];
   all_sum<2>(partI, nb, bcast, t2);
   double rz = t2[0], rr = t2[1];
   const double bb = rr;
   double rz_old = 0.0;
-  const double* zin = zpa;
-  double* zout = zpb;
   int it = 0;
   for (; it < maxit; ++it) {
     if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;  // same test as the host path
     const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
-    const double2* zin2 = reinterpret_cast<const double2*>(zin);
-    // ---- phase A: q = A (z + beta p_old), p = z + beta p_old
+    // ---- phase A: p = z + beta p; q = A z + beta q
     double pq = 0.0;
     if (it == 0 && lane == 0 && warp < nsl) prefetch_slice(sp, scol, sval, s_first + warp);
 #pragma unroll 1
     for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
-      {
-        const int64_t s = s_first + sl;
-        // the TMA engine pulls the warp's next slice into L2 while this one
-        // is gathered, so the next iteration's matrix loads hit L2
-        if (lane == 0 && sl + kResBlock / 32 < nsl) prefetch_slice(sp, scol, sval, s + kResBlock / 32);
-        const int64_t base = sp[s] + lane;
-        const int width = (int)((sp[s + 1] - sp[s]) >> 5);
-        double acc = 0.0;
-        for (int j0 = 0; j0 < width; j0 += kChunk) {
-          int c[kChunk];
-          double a[kChunk];
-#pragma unroll
-          for (int u = 0; u < kChunk; ++u) {
-            const bool ok = j0 + u < width;
-            c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
-            a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
-          }
-          double2 g[kChunk];
-#pragma unroll
-          for (int u = 0; u < kChunk; ++u) g[u] = zin2[c[u]];  // written last phase: coherent after grid.sync
-#pragma unroll
-          for (int u = 0; u < kChunk; ++u) acc = fma(a[u], fma(beta, g[u].y, g[u].x), acc);
-        }
-        const int l = sl * 32 + lane;
-        if (l < nloc) {
-          const double p = fma(beta, spp[l], sz[l]);
-          spp[l] = p;
-          zout[2 * (r0 + l) + 1] = p;
-          sq[l] = acc;
-          pq += p * acc;
-        }
+      const int64_t s = s_first + sl;
+      // the TMA engine pulls the warp's next slice into L2 meanwhile
+      if (lane == 0 && sl + kResBlock / 32 < nsl) prefetch_slice(sp, scol, sval, s + kResBlock / 32);
+      const double az = sell_row_dot(sp, scol, sval, zg, s * 32 + lane);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        const double p = fma(beta, spp[l], sz[l]);
+        const double q = fma(beta, sq[l], az);
+        spp[l] = p;
+        sq[l] = q;
+        pq += p * q;
       }
     }
     {
@@ -378,36 +366,33 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
       block_sum<1, kResBlock>(v, sred);
       if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
     }
-    grid.sync();
+    grid.sync();  // all gathers of z done, p.q partials visible
     double t1[1];
     all_sum<1>(partA, nb, bcast, t1);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
-    // (first two slices of the next iteration go to L2 meanwhile)
     if (lane == 0 && it + 1 < maxit && warp < nsl) prefetch_slice(sp, scol, sval, s_first + warp);
     double b0 = 0.0, b1 = 0.0;
     for (int l = threadIdx.x; l < nloc; l += kResBlock) {
-      {
-        sx[l] = fma(alpha, spp[l], sx[l]);
-        const double ri = fma(-alpha, sq[l], sr[l]);
-        const double zi = __ldg(dinv + r0 + l) * ri;
-        sr[l] = ri;
-        sz[l] = zi;
-        zout[2 * (r0 + l)] = zi;
-        b0 += ri * zi;
-        b1 += ri * ri;
-      }
+      sx[l] = fma(alpha, spp[l], sx[l]);
+      const double ri = fma(-alpha, sq[l], sr[l]);
+      const double zi = __ldg(dinv + r0 + l) * ri;
+      sr[l] = ri;
+      sz[l] = zi;
+      zg[r0 + l] = zi;
+      b0 += ri * zi;
+      b1 += ri * ri;
     }
-    bs = block_sum2(b0, b1, sred);
-    if (threadIdx.x == 0) { partB[blockIdx.x] = bs.x; partB[nb + blockIdx.x] = bs.y; }
-    grid.sync();
+    {
+      double v[2] = {b0, b1};
+      block_sum<2, kResBlock>(v, sred);
+      if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
+    }
+    grid.sync();  // new z visible to every CTA's gathers
     all_sum<2>(partB, nb, bcast, t2);
     rz_old = rz;
     rz = t2[0];
     rr = t2[1];
-    const double* tmp = zin;
-    zin = zout;
-    zout = const_cast<double*>(tmp);
   }
   for (int l = threadIdx.x; l < nloc; l += kResBlock) x_out[r0 + l] = sx[l];
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -452,10 +437,11 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream) {
 }
 
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv, double* x,
-               double* r, double* zp, const double* own, double* red, double* sc, double* part, uint32_t* cnt,
-               void* stream) {
+               double* r, double* z, double* p, double* q, const double* own, double* red, double* sc, double* part,
+               uint32_t* cnt, void* stream) {
   if (n <= 0) return fail("ab_cg_init: empty system");
-  k_cg_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, zp, own, red, sc, part, cnt);
+  k_cg_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, z, p, q, own, red, sc, part,
+                                                    cnt);
   return check_launch("ab_cg_init");
 }
 
@@ -464,24 +450,31 @@ int ab_cg_set_bb(double* red, double* sc, void* stream) {
   return check_launch("ab_cg_set_bb");
 }
 
-int ab_cg_spmv(const ab_sell* a, const double* zp_in, double* zp_out, double* q, int32_t with_dot, const double* own,
-               double* red, double* sc, double* part, uint32_t* cnt, void* stream) {
+int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
+               const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream) {
   if (!a) return fail("ab_cg_spmv: null matrix");
-  if (zp_in == zp_out) return fail("ab_cg_spmv: zp_in and zp_out must differ");
+  if (!with_dot && !t) return fail("ab_cg_spmv: the decomposed form needs t");
   const int64_t n = a->n_rows;
   if (with_dot)
-    k_cg_spmv<true><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, zp_in,
-                                                                       zp_out, q, own, red, sc, part, cnt);
+    k_cg_spmv<true><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p, q, t,
+                                                                       own, red, sc, part, cnt);
   else
-    k_cg_spmv<false><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, zp_in,
-                                                                        zp_out, q, own, red, sc, part, cnt);
+    k_cg_spmv<false><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p, q,
+                                                                        t, own, red, sc, part, cnt);
   return check_launch("ab_cg_spmv");
 }
 
-int ab_cg_dot(int64_t n, const double* zp, const double* q, const double* own, double* red, double* sc, double* part,
-              uint32_t* cnt, void* stream) {
-  k_cg_dot<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, zp, q, own, red, sc, part, cnt);
+int ab_cg_dot(int64_t n, const double* z, const double* t, double* p, double* q, const double* own, double* red,
+              double* sc, double* part, uint32_t* cnt, void* stream) {
+  k_cg_dot<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, z, t, p, q, own, red, sc, part, cnt);
   return check_launch("ab_cg_dot");
+}
+
+int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r, double* z,
+                 const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream) {
+  k_cg_update<<<grid_for((n + 1) / 2, kCgBlock), kCgBlock, 0, S(stream)>>>(n, p, q, dinv, x, r, z, own, red, sc, part,
+                                                                        cnt);
+  return check_launch("ab_cg_update");
 }
 
 int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta) {
@@ -498,8 +491,8 @@ int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta) {
 }
 
 int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
-                   double* x, double* zpa, double* zpb, int32_t maxit, double tol, double* red, double* sc,
-                   double* part, void* stream) {
+                   double* x, double* z, int32_t maxit, double tol, double* red, double* sc, double* part,
+                   void* stream) {
   if (!a) return fail("ab_cg_resident: null matrix");
   int64_t n = a->n_rows, rb = 0;
   int32_t ncta = 0;
@@ -512,7 +505,7 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
   const double* vals = a->vals;
   int mi = maxit;
   void* args[] = {&n, &rb, (void*)&sp, (void*)&cols, (void*)&vals, (void*)&b_in, &b_zero, (void*)&fixed,
-                  (void*)&dinv, &x, &zpa, &zpb, &mi, &tol, &red, &sc, &part};
+                  (void*)&dinv, &x, &z, &mi, &tol, &red, &sc, &part};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cg_resident, dim3(ncta), dim3(kResBlock), args, smem,
                                               S(stream));
   if (e != cudaSuccess) {
@@ -520,13 +513,6 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
     return AB_ECUDA;
   }
   return check_launch("ab_cg_resident");
-}
-
-int ab_cg_update(int64_t n, double* zp, const double* q, const double* dinv, double* x, double* r, const double* own,
-                 double* red, const double* sc, double* part, uint32_t* cnt, void* stream) {
-  k_cg_update<<<grid_for((n + 1) / 2, kCgBlock), kCgBlock, 0, S(stream)>>>(n, zp, q, dinv, x, r, own, red, sc, part,
-                                                                        cnt);
-  return check_launch("ab_cg_update");
 }
 
 }  // extern "C"

@@ -127,10 +127,8 @@ class PCG:
         self.own = own
         self.halo = halo
         z = lambda: torch.zeros(n, dtype=torch.float64, device=dev)  # noqa: E731
-        self.x, self.r, self.q = z(), z(), z()
-        # (z, p) pairs, two alternating buffers
-        self.zpa = torch.zeros((n, 2), dtype=torch.float64, device=dev)
-        self.zpb = torch.zeros((n, 2), dtype=torch.float64, device=dev)
+        self.x, self.r, self.z, self.p, self.q = z(), z(), z(), z(), z()
+        self.t = z() if halo is not None else None  # local A z before the interface sum
         nb = (n + 255) // 256 + 1
         ng = (nb + 63) // 64 + 1
         n_cta = C.c_int32(0)
@@ -158,17 +156,16 @@ class PCG:
         if self.resident:
             with self._m("K5_cg_resident"):
                 call("ab_cg_resident", A, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
-                     ptr(self.x), ptr(self.zpa), ptr(self.zpb), int(maxit), float(tol), ptr(self.red), ptr(self.sc),
+                     ptr(self.x), ptr(self.z), int(maxit), float(tol), ptr(self.red), ptr(self.sc),
                      ptr(self.part), s)
             it = int(self.red[3].item()) if tol > 0 else maxit
             return self.x, it
         call("ab_cg_init", self.n, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
-             ptr(self.x), ptr(self.r), ptr(self.zpa), ptr(self.own), ptr(self.red), ptr(self.sc),
-             ptr(self.part), ptr(self.cnt), s)
+             ptr(self.x), ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.own), ptr(self.red),
+             ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
         if self.halo is not None:
             self.halo.allreduce_(self.red[0:2])
         call("ab_cg_set_bb", ptr(self.red), ptr(self.sc), s)
-        zin, zout = self.zpa, self.zpb
         it = 0
         while it < maxit:
             if tol > 0 and it % check_every == 0:
@@ -177,21 +174,20 @@ class PCG:
                     break
             if self.halo is None:
                 with self._m("K5_cg_spmv"):
-                    call("ab_cg_spmv", A, ptr(zin), ptr(zout), ptr(self.q), 1, ptr(self.own),
+                    call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, ptr(self.own),
                          ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             else:
-                call("ab_cg_spmv", A, ptr(zin), ptr(zout), ptr(self.q), 0, ptr(self.own),
+                call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.t), 0, ptr(self.own),
                      ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
-                self.halo.sum_(self.q, 1, 1)
-                call("ab_cg_dot", self.n, ptr(zout), ptr(self.q), ptr(self.own), ptr(self.red), ptr(self.sc),
-                     ptr(self.part), ptr(self.cnt), s)
+                self.halo.sum_(self.t, 1, 1)
+                call("ab_cg_dot", self.n, ptr(self.z), ptr(self.t), ptr(self.p), ptr(self.q), ptr(self.own),
+                     ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
                 self.halo.allreduce_(self.red[2:3])
             with self._m("K5_cg_update"):
-                call("ab_cg_update", self.n, ptr(zout), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
-                     ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
+                     ptr(self.z), ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             if self.halo is not None:
                 self.halo.allreduce_(self.red[0:2])
-            zin, zout = zout, zin
             it += 1
         return self.x, it
 

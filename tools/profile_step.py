@@ -19,11 +19,16 @@ ap.add_argument("--n", type=int, default=88)
 ap.add_argument("--no-windows", action="store_true")
 ap.add_argument("--no-reorder", action="store_true")
 ap.add_argument("--cg-iters", type=int, default=50)
+ap.add_argument("--no-resident", action="store_true")
+ap.add_argument("--no-pipeline", action="store_true")
 a = ap.parse_args()
 m = meshgen.box_tets(a.n, a.n, a.n, jitter=0.2, seed=20200131)
 u, p = meshgen.c2_initial(m.coords)
-fs = FlowSolver(m, FlowParams(1.0, 1e-3, 0.07), p_fixed=meshgen.boundary_nodes(m), windows=not a.no_windows,
-                reorder=None if a.no_reorder else "sfc")
+from paper_2005_05899_b200.device import DeviceMesh  # noqa: E402
+dm = DeviceMesh(m, reorder=None if a.no_reorder else "sfc", windows=not a.no_windows, pipelined=not a.no_pipeline)
+fs = FlowSolver(dm, FlowParams(1.0, 1e-3, 0.07), p_fixed=meshgen.boundary_nodes(m))
+if a.no_resident:
+    fs.pcg.resident = False
 fs.set_state(u, p)
 if not a.no_windows:
     print(fs.dm.window_stats())
