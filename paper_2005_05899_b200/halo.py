@@ -49,6 +49,12 @@ class HaloExchanger:
     def _global(self, q: int) -> int:
         return q if self.group is None else dist.get_global_rank(self.group, q)
 
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        # gloo cannot move CUDA tensors point to point: stage through the host
+        # (used to run several ranks on one GPU in tests; NCCL moves device
+        # buffers directly)
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def sum_(self, field: torch.Tensor, ncomp: int, stride: int):
         """field[shared] += neighbours' values at the shared nodes."""
         if not self.neighbors:
@@ -61,14 +67,27 @@ class HaloExchanger:
             self.pack(self.idx[q], field, stride, ncomp, s)
             views.append((q, s, self.recv[off:off + m]))
             off += m
+        staged = self._host_staged(self.send)
+        if staged:
+            torch.cuda.current_stream().synchronize()
+            views = [(q, s.cpu(), r.cpu(), r) for q, s, r in views]
+        else:
+            views = [(q, s, r, r) for q, s, r in views]
         ops = []
-        for q, s, r in views:
+        for q, s, r, _dev in views:
             ops.append(dist.P2POp(dist.isend, s, self._global(q), group=self.group))
             ops.append(dist.P2POp(dist.irecv, r, self._global(q), group=self.group))
         for req in dist.batch_isend_irecv(ops):
             req.wait()
-        for q, _s, r in views:
-            self.unpack(self.idx[q], r, stride, ncomp, field)
+        for q, _s, r, dev in views:
+            if staged:
+                dev.copy_(r)
+            self.unpack(self.idx[q], dev, stride, ncomp, field)
 
     def allreduce_(self, t: torch.Tensor):
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        if self._host_staged(t):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
