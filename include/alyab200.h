@@ -177,7 +177,7 @@ int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv
  * kernel with one CTA per SM; each CTA keeps x, r, z, p, q of its rows in
  * shared memory.  Same iterates as the kernels above.
  * Outputs: x, z (scratch); red[RZN], red[RR], red[ITERS]; sc[BB].  `part`
- * >= 5 * n_cta doubles.  ab_cg_resident_fits() returns 1 when n rows fit
+ * >= 5 * n_cta + 1 doubles (partials + the grid-barrier counter).  ab_cg_resident_fits() returns 1 when n rows fit
  * (and reports the launch shape); ab_cg_resident fails with AB_EINVAL
  * otherwise. */
 int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta);

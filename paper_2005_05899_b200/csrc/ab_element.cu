@@ -789,23 +789,32 @@ __device__ __forceinline__ void issue_meta(const WinP& w, int64_t n_elem, int64_
   bulk_copy(m.loc, cl.src, cl.bytes, bar);
 }
 
-// All threads: cp.async gather of a block's window node data (SoA).
+// All threads: cp.async gather of a block's window node data into shared
+// memory as arrays of double2 pairs [NV/2][wmax] — (x,y),(z,u),(v,w) for
+// NV = 6, (x,y),(z,p) for NV = 4 — so an element reads a node with NV/2
+// 128-bit shared loads.
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(su32(dst)), "l"(src) : "memory");
+}
+
 template <int NV, int BLOCK>
 __device__ __forceinline__ void issue_nodes(const CatP& c, const double* __restrict__ f, int wmax, const MetaPtr& m,
                                             const BlockView& v, double* nodes) {
+  double2* pr = reinterpret_cast<double2*>(nodes);
   for (int k = threadIdx.x; k < v.nw; k += BLOCK) {
     const int64_t node = m.wnode[v.skip_wnode + k];
     const double* xp = c.coords + 4 * node;
-    cp_async8(nodes + k, xp);
-    cp_async8(nodes + wmax + k, xp + 1);
-    cp_async8(nodes + 2 * wmax + k, xp + 2);
+    cp_async16(pr + k, xp);                                  // (x, y)
+    double* zu = reinterpret_cast<double*>(pr + wmax + k);   // (z, f0)
+    cp_async8(zu, xp + 2);
     if constexpr (NV == 6) {
       const double* up = f + 4 * node;
-      cp_async8(nodes + 3 * wmax + k, up);
-      cp_async8(nodes + 4 * wmax + k, up + 1);
-      cp_async8(nodes + 5 * wmax + k, up + 2);
+      cp_async8(zu + 1, up);
+      double* vw = reinterpret_cast<double*>(pr + 2 * wmax + k);  // (v, w)
+      cp_async8(vw, up + 1);
+      cp_async8(vw + 1, up + 2);
     } else {
-      cp_async8(nodes + 3 * wmax + k, f + node);
+      cp_async8(zu + 1, f + node);
     }
   }
   cp_async_commit();
@@ -891,18 +900,27 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     const int64_t e = b * BLOCK + threadIdx.x;
     if (e < c.n) {
       double x[NN][3], fv[NN][NV == 6 ? 3 : 1];
+      int li[NN];
+      if constexpr (NN == 4) {
+        const uint2 lv = *reinterpret_cast<const uint2*>(mc.loc + threadIdx.x * NN);
+        li[0] = lv.x & 0xffff; li[1] = lv.x >> 16; li[2] = lv.y & 0xffff; li[3] = lv.y >> 16;
+      } else {
+#pragma unroll
+        for (int a = 0; a < NN; ++a) li[a] = mc.loc[threadIdx.x * NN + a];
+      }
+      const double2* pr = reinterpret_cast<const double2*>(nodes_cur);
 #pragma unroll
       for (int a = 0; a < NN; ++a) {
-        const int l = mc.loc[threadIdx.x * NN + a];
-        x[a][0] = nodes_cur[l];
-        x[a][1] = nodes_cur[wmax + l];
-        x[a][2] = nodes_cur[2 * wmax + l];
+        const int l = li[a];
+        const double2 xy = pr[l], zf = pr[wmax + l];
+        x[a][0] = xy.x;
+        x[a][1] = xy.y;
+        x[a][2] = zf.x;
+        fv[a][0] = zf.y;
         if constexpr (NV == 6) {
-          fv[a][0] = nodes_cur[3 * wmax + l];
-          fv[a][1] = nodes_cur[4 * wmax + l];
-          fv[a][2] = nodes_cur[5 * wmax + l];
-        } else {
-          fv[a][0] = nodes_cur[3 * wmax + l];
+          const double2 vw = pr[2 * wmax + l];
+          fv[a][1] = vw.x;
+          fv[a][2] = vw.y;
         }
       }
       unwrap<NN>(c, x);

@@ -7,8 +7,6 @@
 //   update: x += alpha p, r -= alpha q, z = D^-1 r, r.z and r.r partials.
 // Scalars (alpha, beta) are formed on the device from the reduction slots,
 // so the loop never synchronises with the host.
-#include <cooperative_groups.h>
-
 #include "ab_common.cuh"
 
 namespace ab {
@@ -112,7 +110,9 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* _
 __global__ void k_cg_set_bb(const double* red, double* sc) { sc[AB_SC_BB] = red[AB_RED_RR]; }
 
 // (A z)_i for one SELL row: all column/value loads of a 16-wide chunk first,
-// then the gathers, then the FMAs.
+// then the gathers, then the FMAs.  CG = true gathers through L2 only (z is
+// rewritten inside the resident kernel).
+template <bool CG = false>
 __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
                                                const double* __restrict__ sval, const double* zv, int64_t i) {
   const int64_t s = i >> 5;
@@ -131,7 +131,7 @@ __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, c
     }
     double g[kChunk];
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) g[u] = zv[c[u]];
+    for (int u = 0; u < kChunk; ++u) g[u] = CG ? __ldcg(zv + c[u]) : zv[c[u]];
 #pragma unroll
     for (int u = 0; u < kChunk; ++u) acc = fma(a[u], g[u], acc);
   }
@@ -255,9 +255,9 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, const double*
 // partials, summed in index order by every CTA after a grid barrier).
 // Convergence (tol > 0) is tested on the device, identically in all CTAs.
 // Used when the owned rows fit in shared memory (C2: 4768 rows x 40 B per
-// SM); otherwise the kernels above run.
+// SM); otherwise the kernels above run.  Launched cooperatively so that all
+// CTAs are co-resident for the grid barriers.
 // ---------------------------------------------------------------------------
-namespace cg = cooperative_groups;
 constexpr int kResBlock = 1024;
 
 // Bulk prefetch of one SELL slice (column indices + values) into L2.
@@ -268,6 +268,24 @@ __device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, c
   if (cnt == 0) return;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + b), "r"(cnt * 4u) : "memory");
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
+}
+
+// Grid barrier on a monotone arrival counter (zeroed before launch): the
+// k-th barrier completes when the counter reaches k * gridDim.x.  One
+// release-reduction per CTA and one acquire-polling thread per CTA; the
+// CTA barriers on both sides extend the ordering to all threads.  Data
+// exchanged across it is read with L2-only loads (ld.cg), so no stale L1
+// lines are possible.
+__device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
 }
 
 // Ordered sum of nb per-CTA partials (layout part[k*nb+b]); identical in
@@ -294,8 +312,8 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
     int64_t n, int64_t rows_per_cta, const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
     const double* __restrict__ sval, const double* __restrict__ b_in, double* b_zero, const uint8_t* __restrict__ fixed,
     const double* __restrict__ dinv, double* __restrict__ x_out, double* zg, int maxit, double tol, double* red,
-    double* sc, double* part) {
-  cg::grid_group grid = cg::this_grid();
+    double* sc, double* part, unsigned* bar) {
+  unsigned nbar = 0;
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
   __shared__ double bcast[4];
@@ -333,7 +351,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
     block_sum<2, kResBlock>(v, sred);
     if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
   }
-  grid.sync();
+  grid_barrier(bar, ++nbar * nb);
   double t2[2];
   all_sum<2>(partI, nb, bcast, t2);
   double rz = t2[0], rr = t2[1];
@@ -351,7 +369,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
       const int64_t s = s_first + sl;
       // the TMA engine pulls the warp's next slice into L2 meanwhile
       if (lane == 0 && sl + kResBlock / 32 < nsl) prefetch_slice(sp, scol, sval, s + kResBlock / 32);
-      const double az = sell_row_dot(sp, scol, sval, zg, s * 32 + lane);
+      const double az = sell_row_dot<true>(sp, scol, sval, zg, s * 32 + lane);
       const int l = sl * 32 + lane;
       if (l < nloc) {
         const double p = fma(beta, spp[l], sz[l]);
@@ -366,7 +384,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
       block_sum<1, kResBlock>(v, sred);
       if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
     }
-    grid.sync();  // all gathers of z done, p.q partials visible
+    grid_barrier(bar, ++nbar * nb);  // all gathers of z done, p.q partials visible
     double t1[1];
     all_sum<1>(partA, nb, bcast, t1);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
@@ -388,7 +406,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
       block_sum<2, kResBlock>(v, sred);
       if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
     }
-    grid.sync();  // new z visible to every CTA's gathers
+    grid_barrier(bar, ++nbar * nb);  // new z visible to every CTA's gathers
     all_sum<2>(partB, nb, bcast, t2);
     rz_old = rz;
     rz = t2[0];
@@ -504,8 +522,12 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
   const int32_t* cols = a->cols;
   const double* vals = a->vals;
   int mi = maxit;
-  void* args[] = {&n, &rb, (void*)&sp, (void*)&cols, (void*)&vals, (void*)&b_in, &b_zero, (void*)&fixed,
-                  (void*)&dinv, &x, &z, &mi, &tol, &red, &sc, &part};
+  // the barrier counter lives behind the 5 * n_cta partials, zeroed per solve
+  unsigned* bar = reinterpret_cast<unsigned*>(part + 5 * (size_t)ncta);
+  if (cudaMemsetAsync(bar, 0, sizeof(unsigned), S(stream)) != cudaSuccess)
+    return fail("ab_cg_resident: cannot reset the barrier counter");
+  void* args[] = {&n,  &rb, (void*)&sp, (void*)&cols, (void*)&vals, (void*)&b_in, &b_zero, (void*)&fixed,
+                  (void*)&dinv, &x, &z, &mi, &tol, &red, &sc, &part, &bar};
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)k_cg_resident, dim3(ncta), dim3(kResBlock), args, smem,
                                               S(stream));
   if (e != cudaSuccess) {

@@ -133,7 +133,7 @@ class PCG:
         ng = (nb + 63) // 64 + 1
         n_cta = C.c_int32(0)
         fits = lib().ab_cg_resident_fits(n, None, C.byref(n_cta))
-        self.part = torch.zeros(max(2 * (nb + ng), 5 * n_cta.value) + 8, dtype=torch.float64, device=dev)
+        self.part = torch.zeros(max(2 * (nb + ng), 5 * n_cta.value + 1) + 8, dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)
