@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-windows", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-rebalance", action="store_true",
+                    help="N>1: skip the throughput-weighted repartitioning (DLB analog)")
     return ap.parse_args()
 
 
@@ -133,8 +135,10 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
     N = n_nodes
     if kernel == "K5_cg_resident":  # SURVEY §8(d) K5 per iteration: 12Z + 4(N+1) + 104N
         return cg_iters * (12 * nnz + 4 * (N + 1) + 104 * N), cg_iters * (2 * nnz + 12 * N)
-    if kernel == "K5_cg_spmv":      # vals+cols, z & p_old (gathered once), p_new & q writes
-        return 12 * nnz + 32 * N, 2 * nnz + 3 * N
+    if kernel == "K5_cg_spmv":      # vals+cols, z gathered once, p & q read + written
+        return 12 * nnz + 8 * N + 32 * N, 2 * nnz + 4 * N
+    if kernel == "K5_cg_dot":       # z t p q in, p q out
+        return 48 * N, 6 * N
     if kernel == "K5_cg_update":    # x p r q dinv in, x r z out
         return 64 * N, 10 * N
     if kernel == "K2_momentum":     # conn, coords, u in; rhs out
@@ -201,29 +205,54 @@ def run_native(args):
     ws, rank, local = dist_env()
     if args.gpus != ws and ws > 1:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE {ws}")
+    # AB_DIST_BACKEND=gloo runs several ranks on one GPU (exchange staged
+    # through the host): a functional check of this multi-rank path only
+    backend = os.environ.get("AB_DIST_BACKEND", "nccl")
+    if backend != "nccl":
+        local = 0
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    mesh, u, p, bc, params, desc = build_workload(args.workload, ws)
-    halo = own = None
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    mesh, u_g, p_g, bc_g, params, desc = build_workload(args.workload, ws)
     n_elem_total = mesh.n_elements
-    if ws > 1:
+    rebalance = None
+
+    def make_solver(parts=None):
+        if ws == 1:
+            s_ = FlowSolver(mesh, FlowParams(**params), **bc_g, windows=not args.no_windows, reorder="sfc")
+            s_.set_state(u_g, p_g)
+            return s_, mesh.n_elements
         from paper_2005_05899_b200.decompose import decompose
         from paper_2005_05899_b200.halo import HaloExchanger
-        from paper_2005_05899_b200.partition import sfc_partition
-        parts, _cuts, subw = sfc_partition(mesh, ws, level=8)
         sub, plan = decompose(mesh, parts, ws, rank)
         l2g = plan.l2g
-        bc = {k: np.asarray(v)[l2g] for k, v in bc.items()}
-        u, p = u[l2g], p[l2g]
         halo = HaloExchanger(plan, "cuda")
-        own = halo.own
-        local_mesh = sub
+        s_ = FlowSolver(sub, FlowParams(**params), **{k: np.asarray(v)[l2g] for k, v in bc_g.items()},
+                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own)
+        s_.set_state(u_g[l2g], p_g[l2g])
+        return s_, sub.n_elements
+
+    if ws == 1:
+        solver, n_local = make_solver()
     else:
-        local_mesh = mesh
-    solver = FlowSolver(local_mesh, FlowParams(**params), **bc, windows=not args.no_windows, reorder="sfc",
-                        halo=halo, own=own)
-    solver.set_state(u, p)
+        from paper_2005_05899_b200.balance import distributed_timer, throughput_coefficients
+        from paper_2005_05899_b200.partition import sfc_partition
+        parts, _cuts, subw = sfc_partition(mesh, ws, level=8)
+        solver, n_local = make_solver(parts)
+        if not args.no_rebalance:
+            # DLB analog: lambda_i = P theta_i / sum(theta) from
+            # each rank's measured K2 throughput, one re-split, rebuild
+            sample = distributed_timer(solver)
+            lam = throughput_coefficients(sample.times, subw)
+            parts, _cuts, subw2 = sfc_partition(mesh, ws, coeffs=lam, level=8)
+            del solver
+            torch.cuda.synchronize()
+            solver, n_local = make_solver(parts)
+            rebalance = {"k2_seconds_before": [float(t) for t in sample.times], "lambda": [float(x) for x in lam],
+                         "weights_before": [float(x) for x in subw], "weights_after": [float(x) for x in subw2]}
     graph = (not args.no_graph) and ws == 1
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
@@ -303,7 +332,7 @@ def run_native(args):
         kern[name] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
                       "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,
                       "gflops": F / avg / 1e9 if F and avg > 0 else None}
-    dom = max(kern, key=lambda k: kern[k]["total_ms"])
+    dom = max((k for k in kern if k.startswith("K")), key=lambda k: kern[k]["total_ms"])
     peak, peak_kind = load_peaks()
     traffic = load_traffic().get(dom)
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(kern[dom]["gbs"], 1), "peak": peak, "unit": "GB/s",
@@ -334,6 +363,10 @@ def run_native(args):
         "gpu_launches": int(launches_per_step * args.steps),
         "clocks": clk,
     }
+    if rebalance is not None:
+        result["rebalance"] = rebalance
+    if backend != "nccl":
+        result["note"] = f"{ws} ranks on one GPU over {backend}: functional check, not a performance number"
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             result["cpu_baseline"] = cpu_baseline_sample()

@@ -135,7 +135,8 @@ def distributed_timer(solver, group=None, reps: int = 5):
     import torch
     import torch.distributed as dist
     t = _time_momentum(solver.dm, reps)
-    buf = torch.tensor([t], dtype=torch.float64, device=solver.dm.device)
+    dev = solver.dm.device if dist.get_backend(group) == "nccl" else torch.device("cpu")
+    buf = torch.tensor([t], dtype=torch.float64, device=dev)
     out = [torch.zeros_like(buf) for _ in range(dist.get_world_size(group))]
     dist.all_gather(out, buf, group=group)
     return TimingSample(iteration=1, times=np.array([float(x.item()) for x in out]))

@@ -177,17 +177,22 @@ class PCG:
                     call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, ptr(self.own),
                          ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             else:
-                call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.t), 0, ptr(self.own),
-                     ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
-                self.halo.sum_(self.t, 1, 1)
-                call("ab_cg_dot", self.n, ptr(self.z), ptr(self.t), ptr(self.p), ptr(self.q), ptr(self.own),
-                     ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
-                self.halo.allreduce_(self.red[2:3])
+                with self._m("K5_cg_spmv"):
+                    call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.t), 0, ptr(self.own),
+                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                with self._m("X_halo_sum"):
+                    self.halo.sum_(self.t, 1, 1)
+                with self._m("K5_cg_dot"):
+                    call("ab_cg_dot", self.n, ptr(self.z), ptr(self.t), ptr(self.p), ptr(self.q), ptr(self.own),
+                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                with self._m("X_allreduce"):
+                    self.halo.allreduce_(self.red[2:3])
             with self._m("K5_cg_update"):
                 call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(self.dinv), ptr(self.x), ptr(self.r),
                      ptr(self.z), ptr(self.own), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             if self.halo is not None:
-                self.halo.allreduce_(self.red[0:2])
+                with self._m("X_allreduce"):
+                    self.halo.allreduce_(self.red[0:2])
             it += 1
         return self.x, it
 

@@ -164,7 +164,8 @@ class FlowSolver:
             with self._mark("K2_momentum"):
                 call("ab_momentum_rhs", ctypes.byref(dm.struct), ctypes.byref(self.phys), ptr(uin), ptr(self.R), s)
             if self.halo is not None:
-                self.halo.sum_(self.R, 3, 4)
+                with self._mark("X_halo_sum"):
+                    self.halo.sum_(self.R, 3, 4)
             with self._mark("K3_rk_stage"):
                 call("ab_rk_stage", self.n, RK3_A[st], RK3_B[st], k, ptr(self.U0), ptr(uin), ptr(self.R),
                      ptr(self.GP), ptr(self.minv), ptr(self.U), s)
@@ -172,14 +173,16 @@ class FlowSolver:
         with self._mark("K4_divergence"):
             call("ab_divergence", ctypes.byref(dm.struct), ptr(self.U), -rho / dt, ptr(self.B), s)
         if self.halo is not None:
-            self.halo.sum_(self.B, 1, 1)
+            with self._mark("X_halo_sum"):
+                self.halo.sum_(self.B, 1, 1)
         self.pcg.mark = self._mark
         x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
         self.last_cg_iters = it
         with self._mark("K6_gradient"):
             call("ab_gradient", ctypes.byref(dm.struct), ptr(x), 1.0, ptr(self.GD), s)
         if self.halo is not None:
-            self.halo.sum_(self.GD, 3, 4)
+            with self._mark("X_halo_sum"):
+                self.halo.sum_(self.GD, 3, 4)
         with self._mark("K7_correct"):
             call("ab_correct", self.n, k, ptr(self.U), ptr(self.U0), ptr(self.GD), ptr(self.minv), ptr(self.P),
                  ptr(x), ptr(self.GP), s)
