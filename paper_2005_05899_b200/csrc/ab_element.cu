@@ -186,21 +186,21 @@ __device__ __forceinline__ double abs_det(const double (&x)[NN][3], int g) {
 // Vreman eddy viscosity: mu_t = rho c sqrt(B_beta / a:a),
 // alpha_ij = du_j/dx_i = G_ji, beta = Delta^2 alpha^T alpha.
 __device__ __forceinline__ double vreman(const double (&G)[3][3], double delta2, double rho, double c) {
-  double b[3][3], aa = 0.0;
+  // S = alpha^T alpha (symmetric, S_ij = sum_m G_im G_jm); beta = Delta^2 S, so
+  // B_beta = Delta^4 * (sum of the principal 2x2 minors of S) and a:a = tr S.
+  double S[6];  // 00 11 22 01 02 12
+  const int I[6] = {0, 1, 2, 0, 0, 1}, J[6] = {0, 1, 2, 1, 2, 2};
 #pragma unroll
-  for (int i = 0; i < 3; ++i)
+  for (int k = 0; k < 6; ++k) {
+    double t = 0.0;
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < 3; ++m) s = fma(G[i][m], G[j][m], s);  // sum_m alpha_mi alpha_mj
-      b[i][j] = delta2 * s;
-      aa = fma(G[i][j], G[i][j], aa);
-    }
-  double B = b[0][0] * b[1][1] - b[0][1] * b[0][1] + b[0][0] * b[2][2] - b[0][2] * b[0][2] + b[1][1] * b[2][2] -
-             b[1][2] * b[1][2];
-  B = fmax(B, 0.0);
-  return aa > 1e-30 ? rho * c * sqrt(B / aa) : 0.0;
+    for (int m = 0; m < 3; ++m) t = fma(G[I[k]][m], G[J[k]][m], t);
+    S[k] = t;
+  }
+  const double aa = S[0] + S[1] + S[2];
+  double Bm = S[0] * S[1] - S[3] * S[3] + S[0] * S[2] - S[4] * S[4] + S[1] * S[2] - S[5] * S[5];
+  Bm = fmax(Bm, 0.0);
+  return aa > 1e-30 ? rho * c * delta2 * sqrt(Bm / aa) : 0.0;
 }
 
 // ---------------------------------------------------------------------------
@@ -427,31 +427,47 @@ __device__ __forceinline__ void momentum_element(const ab_phys ph, const double 
       const double d = cbrt(vol);
       mu_eff += vreman(G, d * d, ph.rho, ph.c_vreman);
     }
-    // A = G + G^T + div I  (c = A u_g);  sigma = 2 mu_eff eps V
-    double A[3][3], sg[3][3];
-#pragma unroll
-    for (int i = 0; i < 3; ++i)
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const double s = G[i][j] + G[j][i];
-        A[i][j] = s + (i == j ? div : 0.0);
-        sg[i][j] = mu_eff * s * vol;  // 2 mu eps_ij vol
-      }
-    const double rdet = ph.rho * adet;
-#pragma unroll
-    for (int a = 0; a < NN; ++a) {
-      double m[3] = {0.0, 0.0, 0.0};
+    // Symmetric A' = rho |J| (G + G^T + div I) and sigma = 2 mu_eff eps V,
+    // 6 unique entries each (index k: 00 11 22 01 02 12).
+    const double rdet = ph.rho * adet, mv = mu_eff * vol;
+    double Ap[6], sg[6];
+    {
+      const double s00 = G[0][0] + G[0][0], s11 = G[1][1] + G[1][1], s22 = G[2][2] + G[2][2];
+      const double s01 = G[0][1] + G[1][0], s02 = G[0][2] + G[2][0], s12 = G[1][2] + G[2][1];
+      Ap[0] = rdet * (s00 + div); Ap[1] = rdet * (s11 + div); Ap[2] = rdet * (s22 + div);
+      Ap[3] = rdet * s01; Ap[4] = rdet * s02; Ap[5] = rdet * s12;
+      sg[0] = mv * s00; sg[1] = mv * s11; sg[2] = mv * s22;
+      sg[3] = mv * s01; sg[4] = mv * s02; sg[5] = mv * s12;
+    }
+    // m_a = sum_b M_ab u_b; for the exactly integrated P1 mass (tet4),
+    // M_ab = (1 + delta_ab) / 120, i.e. m_a = (u_a + sum_b u_b) / 120.
+    double U[3] = {0.0, 0.0, 0.0};
+    if constexpr (R == AB_RULE_TET4) {
 #pragma unroll
       for (int b = 0; b < NN; ++b)
 #pragma unroll
-        for (int i = 0; i < 3; ++i) m[i] = fma(c_M[R][a][b], u[b][i], m[i]);
-      double r[3];
+        for (int i = 0; i < 3; ++i) U[i] += u[b][i];
+    }
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double cv = A[i][0] * m[0] + A[i][1] * m[1] + A[i][2] * m[2];
-        const double vs = sg[i][0] * dNdx[a][0] + sg[i][1] * dNdx[a][1] + sg[i][2] * dNdx[a][2];
-        r[i] = -(rdet * cv + vs);
+    for (int a = 0; a < NN; ++a) {
+      double m[3];
+      if constexpr (R == AB_RULE_TET4) {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) m[i] = (u[a][i] + U[i]) * (1.0 / 120.0);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          double t = 0.0;
+#pragma unroll
+          for (int b = 0; b < NN; ++b) t = fma(c_M[R][a][b], u[b][i], t);
+          m[i] = t;
+        }
       }
+      const double* d = dNdx[a];
+      double r[3];
+      r[0] = -(Ap[0] * m[0] + Ap[3] * m[1] + Ap[4] * m[2] + sg[0] * d[0] + sg[3] * d[1] + sg[4] * d[2]);
+      r[1] = -(Ap[3] * m[0] + Ap[1] * m[1] + Ap[5] * m[2] + sg[3] * d[0] + sg[1] * d[1] + sg[5] * d[2]);
+      r[2] = -(Ap[4] * m[0] + Ap[5] * m[1] + Ap[2] * m[2] + sg[4] * d[0] + sg[5] * d[1] + sg[2] * d[2]);
       emit(a, r);
     }
   } else {
@@ -828,8 +844,12 @@ template <int R> struct OpT<R, OP_MOMENTUM> { static constexpr int NV = 6, NC = 
 template <int R> struct OpT<R, OP_DIVERGENCE> { static constexpr int NV = 6, NC = 1, STRIDE = 1; };
 template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 3, STRIDE = 4; };
 
+#ifndef PIPE_OCC_K2
+#define PIPE_OCC_K2 5  // 90 registers, measured 192 us vs 197 us at 106 (C2 K2)
+#endif
 // minimum resident CTAs per SM requested from the register allocator
 template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
+template <> struct PipeOcc<AB_RULE_TET4, OP_MOMENTUM> { static constexpr int value = PIPE_OCC_K2; };
 
 // Persistent pipelined element kernel.  Iteration i (element block b_i):
 //   A  wait metadata(b_{i+1}) [mbarrier], cp.async node data(b_{i+1})
