@@ -83,6 +83,7 @@ const char* ab_last_error(void);
 /* Number of kernels this library launched since load (evidence counter). */
 int64_t ab_launch_count(void);
 
+
 /* ---- K1: packed mass matrix + lumped mass -------------------------------
  * Replaces build_packs' Jacobians + assemble_packs (reference
  * assembly.py:129-141, :178-244) and scatter_global(...).row_sums()
@@ -184,6 +185,38 @@ int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta);
 int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
                    double* x, double* z, int32_t maxit, double tol, double* red, double* sc, double* part,
                    void* stream);
+
+/* CTA-local column map of a SELL matrix for the resident CG (DESIGN.md
+ * §4.3): CTA b owns rows [b*rows_per_cta, (b+1)*rows_per_cta) (the launch
+ * shape of ab_cg_resident_fits); its remote columns ("ghost rows") are
+ * ghost[ghost_ptr[b] .. ghost_ptr[b+1]) ascending, and cols[k] (same layout
+ * as ab_sell.cols) is the local index of entry k: c - row0 for an own row,
+ * rows_per_cta + g for ghost g.  rows_per_cta + max_ghost <= 65536.
+ * perm (nullable): the matrix is P L P^T, row i of the system is node
+ * perm[i] (a compact, SFC-ordered numbering keeps the ghost sets small);
+ * b_in, b_zero and x are then in node order, fixed and dinv in row order.
+ * prefetch_depth: SELL slices per warp bulk-prefetched into L2 ahead of
+ * use (also across the grid barriers, so the matrix stream of the next
+ * iteration starts while the reductions complete). */
+typedef struct ab_cg_local {
+  int64_t rows_per_cta;
+  int32_t n_cta;
+  int32_t max_ghost;
+  const uint16_t* cols;
+  const int32_t* ghost_ptr;  /* [n_cta+1] */
+  const int32_t* ghost;
+  const int32_t* perm;       /* [n_rows] or NULL */
+  int32_t prefetch_depth;
+  int32_t pad_;
+} ab_cg_local;
+/* 2: fits with x in shared memory, 1: fits with x in global memory, 0: no */
+int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost);
+/* ab_cg_resident with the z gathers served from shared memory: each CTA
+ * fetches its ghost z values once per iteration, the SpMV reads z through
+ * the 16-bit local columns.  Same iterates as ab_cg_resident. */
+int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b_in, double* b_zero,
+                         const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
+                         double* red, double* sc, double* part, void* stream);
 
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */

@@ -14,4 +14,5 @@ extern "C" {
 int ab_version(void) { return 100; }  // 0.1.0
 const char* ab_last_error(void) { return ab::t_err.c_str(); }
 int64_t ab_launch_count(void) { return ab::g_launches.load(); }
+
 }

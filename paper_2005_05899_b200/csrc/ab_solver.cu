@@ -421,6 +421,206 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Resident CG over a CTA-local column map (ab_cg_local).  Every CTA gathers
+// the z values of its ghost rows (columns it references outside its own
+// row range) ONCE per iteration into shared memory behind its own z, and
+// the SpMV then reads z exclusively from shared memory through 16-bit local
+// column indices: the per-non-zero L2 gathers of k_cg_resident (10.4M per
+// iteration on C2) become ~0.3M per-ghost gathers, and the column stream
+// shrinks from 4 to 2 bytes per non-zero.  Same iterates, same order of
+// floating-point operations per row as k_cg_resident.
+// Shared memory: r, p, q [RB] | x [RB] (XS only; else x lives in x_out) |
+// z [RB] followed by the ghost values [max_ghost].
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void prefetch_slice16(const int64_t* __restrict__ sp, const uint16_t* lcol,
+                                                 const double* sval, int64_t s) {
+  const int64_t b = sp[s];
+  const uint32_t cnt = (uint32_t)(sp[s + 1] - b);
+  if (cnt == 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lcol + b), "r"(cnt * 2u) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
+}
+
+template <int CH>
+__device__ __forceinline__ double sell_row_dot_smem(const int64_t* __restrict__ sp, const uint16_t* __restrict__ lcol,
+                                                    const double* __restrict__ sval, const double* zs, int64_t i) {
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t base = sp[s] + lane;
+  const int width = (int)((sp[s + 1] - sp[s]) >> 5);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < width; j0 += CH) {
+    unsigned c[CH];
+    double a[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const bool ok = j0 + u < width;
+      c[u] = ok ? (unsigned)__ldcs(lcol + base + (int64_t)(j0 + u) * 32) : 0u;
+      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) acc = fma(a[u], zs[c[u]], acc);
+  }
+  return acc;
+}
+
+// Ordered sum of nb (<= blockDim) per-CTA partials, all loads in flight at
+// once (one L2 round trip), fixed reduction tree: identical in every CTA.
+template <int NV>
+__device__ __forceinline__ void all_sum_par(const double* part, int nb, double* sred, double* bcast,
+                                            double (&out)[NV]) {
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = (int)threadIdx.x < nb ? __ldcg(part + (size_t)k * nb + threadIdx.x) : 0.0;
+  block_sum<NV, kResBlock>(v, sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bcast[k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
+}
+
+constexpr int kLocChunk = 8;
+
+template <bool XS>
+__global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
+    int64_t n, int64_t rows_per_cta, int max_ghost, const int64_t* __restrict__ sp,
+    const uint16_t* __restrict__ lcol, const double* __restrict__ sval, const int32_t* __restrict__ gptr,
+    const int32_t* __restrict__ gidx, const int32_t* __restrict__ perm, const double* __restrict__ b_in,
+    double* b_zero,
+    const uint8_t* __restrict__ fixed, const double* __restrict__ dinv, double* __restrict__ x_out, double* zg,
+    int maxit, double tol, double* red, double* sc, double* part, unsigned* bar, int pf_depth) {
+  unsigned nbar = 0;
+  extern __shared__ double smem[];
+  __shared__ double sred[2 * (kResBlock / 32)];
+  __shared__ double bcast[4];
+  const int nb = gridDim.x;
+  const int64_t RB = rows_per_cta;
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int64_t r1 = r0 + RB < n ? r0 + RB : n;
+  const int nloc = r1 > r0 ? (int)(r1 - r0) : 0;
+  double* sr = smem;
+  double* spp = sr + RB;
+  double* sq = spp + RB;
+  double* sx = sq + RB;               // XS only
+  double* sz = XS ? sx + RB : sx;     // [RB] own rows, then [max_ghost] ghosts
+  double* partA = part;
+  double* partB = part + nb;
+  double* partI = part + 3 * (size_t)nb;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (nloc + 31) >> 5;
+  const int64_t s_first = r0 >> 5;
+  const int g0 = gptr[blockIdx.x];
+  const int ng = gptr[blockIdx.x + 1] - g0;
+  (void)max_ghost;
+
+  double a0 = 0.0, a1 = 0.0;
+  for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+    const int64_t i = r0 + l;
+    const int64_t ni = perm ? (int64_t)perm[i] : i;
+    double ri = b_in[ni];
+    if (fixed && fixed[i]) ri = 0.0;
+    if (b_zero) b_zero[ni] = 0.0;
+    const double zi = dinv[i] * ri;
+    sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
+    if (XS) sx[l] = 0.0; else x_out[ni] = 0.0;
+    zg[i] = zi;
+    a0 += ri * zi;
+    a1 += ri * ri;
+  }
+  {
+    double v[2] = {a0, a1};
+    block_sum<2, kResBlock>(v, sred);
+    if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
+  }
+  // the first pf_depth slices of every warp go to L2 ahead of phase A
+  if (lane == 0)
+    for (int d = 0; d < pf_depth; ++d)
+      if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
+  grid_barrier(bar, ++nbar * nb);
+  double t2[2];
+  all_sum_par<2>(partI, nb, sred, bcast, t2);
+  double rz = t2[0], rr = t2[1];
+  const double bb = rr;
+  double rz_old = 0.0;
+  int it = 0;
+  for (; it < maxit; ++it) {
+    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
+    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    // ---- ghost z values of this CTA's columns -> shared memory
+    for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + __ldg(gidx + g0 + k));
+    __syncthreads();
+    // ---- phase A: p = z + beta p; q = A z + beta q (z from shared memory)
+    double pq = 0.0;
+#pragma unroll 1
+    for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
+      const int64_t s = s_first + sl;
+      if (lane == 0 && sl + pf_depth * (kResBlock / 32) < nsl)
+        prefetch_slice16(sp, lcol, sval, s + pf_depth * (kResBlock / 32));
+      const double az = sell_row_dot_smem<kLocChunk>(sp, lcol, sval, sz, s * 32 + lane);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        const double p = fma(beta, spp[l], sz[l]);
+        const double q = fma(beta, sq[l], az);
+        spp[l] = p;
+        sq[l] = q;
+        pq += p * q;
+      }
+    }
+    {
+      double v[1] = {pq};
+      block_sum<1, kResBlock>(v, sred);
+      if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+    }
+    grid_barrier(bar, ++nbar * nb);
+    double t1[1];
+    all_sum_par<1>(partA, nb, sred, bcast, t1);
+    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+    // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
+    if (lane == 0 && it + 1 < maxit)
+      for (int d = 0; d < pf_depth; ++d)
+        if (warp + d * (kResBlock / 32) < nsl)
+          prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
+    double b0 = 0.0, b1 = 0.0;
+    for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+      if (XS) {
+        sx[l] = fma(alpha, spp[l], sx[l]);
+      } else {
+        const int64_t ni = perm ? (int64_t)perm[r0 + l] : r0 + l;
+        x_out[ni] = fma(alpha, spp[l], x_out[ni]);
+      }
+      const double ri = fma(-alpha, sq[l], sr[l]);
+      const double zi = __ldg(dinv + r0 + l) * ri;
+      sr[l] = ri;
+      sz[l] = zi;
+      zg[r0 + l] = zi;
+      b0 += ri * zi;
+      b1 += ri * ri;
+    }
+    {
+      double v[2] = {b0, b1};
+      block_sum<2, kResBlock>(v, sred);
+      if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
+    }
+    grid_barrier(bar, ++nbar * nb);
+    all_sum_par<2>(partB, nb, sred, bcast, t2);
+    rz_old = rz;
+    rz = t2[0];
+    rr = t2[1];
+  }
+  if (XS)
+    for (int l = threadIdx.x; l < nloc; l += kResBlock) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = sx[l];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    red[AB_RED_RZN] = rz;
+    red[AB_RED_RR] = rr;
+    red[AB_RED_ITERS] = (double)it;
+    sc[AB_SC_BB] = bb;
+  }
+}
+
 static unsigned cg_grid(int64_t n) {
   const int64_t g = (n + kCgBlock - 1) / kCgBlock;
   return (unsigned)(g < kCgGrid ? g : kCgGrid);
@@ -535,6 +735,72 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
     return AB_ECUDA;
   }
   return check_launch("ab_cg_resident");
+}
+
+}  // extern "C"
+
+namespace {
+// dynamic shared memory of k_cg_resident_local: 2 = x in shared memory too,
+// 1 = x in global memory, 0 = does not fit
+int local_mode(int64_t rb, int32_t max_ghost, size_t* bytes) {
+  int dev = 0, optin = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  const size_t static_smem = 1024;  // sred + bcast + slack
+  const size_t cap = optin > (int)static_smem ? (size_t)optin - static_smem : 0;
+  if (!coop || max_ghost < 0 || rb + max_ghost > 65536) return 0;
+  const size_t xs = (size_t)(5 * rb + max_ghost) * sizeof(double);
+  const size_t xg = (size_t)(4 * rb + max_ghost) * sizeof(double);
+  if (xs <= cap) { if (bytes) *bytes = xs; return 2; }
+  if (xg <= cap) { if (bytes) *bytes = xg; return 1; }
+  return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost) {
+  return local_mode(rows_per_cta, max_ghost, nullptr);
+}
+
+int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b_in, double* b_zero,
+                         const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
+                         double* red, double* sc, double* part, void* stream) {
+  if (!a || !m) return fail("ab_cg_resident_local: null matrix or map");
+  if (!m->cols || !m->ghost_ptr || !m->ghost) return fail("ab_cg_resident_local: incomplete column map");
+  int64_t n = a->n_rows, rb = 0;
+  int32_t ncta = 0;
+  ab_cg_resident_fits(n, &rb, &ncta);
+  if (rb != m->rows_per_cta || ncta != m->n_cta)
+    return fail("ab_cg_resident_local: column map built for another launch shape");
+  size_t smem = 0;
+  const int mode = local_mode(rb, m->max_ghost, &smem);
+  if (mode == 0) return fail("ab_cg_resident_local: system does not fit in shared memory");
+  const void* fn = mode == 2 ? (const void*)k_cg_resident_local<true> : (const void*)k_cg_resident_local<false>;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return fail("ab_cg_resident_local: cannot reserve shared memory");
+  const int64_t* sp = a->slice_ptr;
+  const uint16_t* lcol = m->cols;
+  const double* vals = a->vals;
+  const int32_t* gp = m->ghost_ptr;
+  const int32_t* gi = m->ghost;
+  const int32_t* pm = m->perm;
+  int mg = m->max_ghost;
+  int depth = m->prefetch_depth;
+  int mi = maxit;
+  unsigned* bar = reinterpret_cast<unsigned*>(part + 5 * (size_t)ncta);
+  if (cudaMemsetAsync(bar, 0, sizeof(unsigned), S(stream)) != cudaSuccess)
+    return fail("ab_cg_resident_local: cannot reset the barrier counter");
+  void* args[] = {&n,           &rb,          &mg,  (void*)&sp, (void*)&lcol, (void*)&vals, (void*)&gp,
+                  (void*)&gi,   (void*)&pm,   (void*)&b_in, &b_zero, (void*)&fixed, (void*)&dinv, &x, &z,
+                  &mi,          &tol,         &red, &sc, &part, &bar, &depth};
+  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(ncta), dim3(kResBlock), args, smem, S(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_cg_resident_local: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  return check_launch("ab_cg_resident_local");
 }
 
 }  // extern "C"

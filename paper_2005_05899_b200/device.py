@@ -100,6 +100,18 @@ class DeviceMesh:
             self.ids[k] = self.ids[k][order].contiguous()
         self._build_struct()
 
+    def node_order(self, level: int = 10) -> torch.Tensor:
+        """Node ids sorted by the Hilbert key of their coordinates (stable):
+        the solver-row numbering of the resident CG (compact per-CTA row
+        ranges)."""
+        c = self.coords4[:, :3].contiguous()
+        lo = c.min(dim=0).values
+        hi = c.max(dim=0).values
+        span = torch.clamp(hi - lo, min=1e-300) * (1 + 1e-12)
+        keys = torch.empty(c.shape[0], dtype=torch.int64, device=self.device)
+        call("ab_hilbert_keys", c.shape[0], ptr(c), ptr(lo), ptr(span), level, ptr(keys), stream_handle())
+        return torch.sort(keys, stable=True).indices.to(torch.int32)
+
     # -- node windows ---------------------------------------------------------
     def build_windows(self):
         self.clear_windows()

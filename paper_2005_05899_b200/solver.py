@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import AbSell, call, lib, ptr, stream_handle
+from ._lib import AbCgLocal, AbSell, call, lib, ptr, stream_handle
 from .device import DeviceMesh
 
 
@@ -96,6 +96,62 @@ def csr_to_sell(n: int, row_ptr, cols, vals) -> SellMatrix:
                       csr=(row_ptr, cols, vals))
 
 
+def permute_matrix(A: SellMatrix, perm: torch.Tensor) -> SellMatrix:
+    """P A P^T as SELL-32: row i of the result is row perm[i] of A (columns
+    renumbered the same way, ascending within each row)."""
+    row_ptr, cols, vals = A.csr
+    n = A.n_rows
+    dev = vals.device
+    perm = perm.to(device=dev, dtype=torch.int64)
+    iperm = torch.empty_like(perm)
+    iperm[perm] = torch.arange(n, device=dev)
+    rows = torch.repeat_interleave(torch.arange(n, device=dev), row_ptr[1:] - row_ptr[:-1])
+    key = iperm[rows] * n + iperm[cols.to(torch.int64)]
+    key, order = torch.sort(key)
+    new_rows = key // n
+    new_cols = (key % n).to(torch.int32).contiguous()
+    new_vals = vals[order].contiguous()
+    rp = torch.zeros(n + 1, dtype=torch.int64, device=dev)
+    rp[1:] = torch.cumsum(torch.bincount(new_rows, minlength=n), 0)
+    return csr_to_sell(n, rp, new_cols, new_vals)
+
+
+def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
+    """CTA-local column map for ``ab_cg_resident_local`` (include/alyab200.h):
+    per CTA the ascending list of remote columns (ghost rows) and, per SELL
+    entry, the 16-bit local column (own row: c - row0; ghost g: rows_per_cta
+    + g).  Returns None when a CTA's rows + ghosts exceed 16 bits."""
+    n = A.n_rows
+    dev = A.cols.device
+    sp = A.slice_ptr
+    counts = sp[1:] - sp[:-1]
+    n_sl = counts.numel()
+    slice_of = torch.repeat_interleave(torch.arange(n_sl, device=dev), counts)
+    cta = slice_of // (rows_per_cta // 32)
+    del slice_of
+    r0 = cta * rows_per_cta
+    c = A.cols.to(torch.int64)
+    local = (c >= r0) & (c < r0 + rows_per_cta)
+    remote = ~local
+    key = cta[remote] * n + c[remote]
+    uk, inv = torch.unique(key, return_inverse=True)
+    g_cta = uk // n
+    ghost = (uk % n).to(torch.int32).contiguous()
+    gcount = torch.bincount(g_cta, minlength=n_cta)
+    ghost_ptr = torch.zeros(n_cta + 1, dtype=torch.int64, device=dev)
+    ghost_ptr[1:] = torch.cumsum(gcount, 0)
+    lc = c - r0
+    lc[remote] = rows_per_cta + inv - ghost_ptr[cta[remote]]
+    max_ghost = int(gcount.max().item()) if gcount.numel() else 0
+    if rows_per_cta + max_ghost > 65536:
+        return None
+    lcols = torch.where(lc >= 32768, lc - 65536, lc).to(torch.int16).contiguous()
+    ghost_ptr = ghost_ptr.to(torch.int32).contiguous()
+    struct = AbCgLocal(rows_per_cta=rows_per_cta, n_cta=n_cta, max_ghost=max_ghost, cols=ptr(lcols),
+                       ghost_ptr=ptr(ghost_ptr), ghost=ptr(ghost))
+    return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct)
+
+
 def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
     """Assemble L (SPD after Dirichlet rows/cols of ``fixed`` -> identity)."""
     dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
@@ -117,7 +173,8 @@ class PCG:
     """
 
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
-                 own: torch.Tensor | None = None, halo=None, resident: bool = True):
+                 own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
+                 order: torch.Tensor | None = None, prefetch_depth: int = 1):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -132,7 +189,8 @@ class PCG:
         nb = (n + 255) // 256 + 1
         ng = (nb + 63) // 64 + 1
         n_cta = C.c_int32(0)
-        fits = lib().ab_cg_resident_fits(n, None, C.byref(n_cta))
+        rb = C.c_int64(0)
+        fits = lib().ab_cg_resident_fits(n, C.byref(rb), C.byref(n_cta))
         self.part = torch.zeros(max(2 * (nb + ng), 5 * n_cta.value + 1) + 8, dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -142,6 +200,27 @@ class PCG:
         # single-domain solves run as one cooperative kernel when the rows fit
         # in shared memory (ab_cg_resident); otherwise two kernels/iteration
         self.resident = bool(resident and halo is None and fits)
+        # ... with the z gathers served from shared memory (ab_cg_resident_local)
+        # ``order`` (node id per solver row, e.g. an SFC order of the nodes)
+        # renumbers the system P A P^T so every CTA's rows are compact and its
+        # ghost set small; b and x stay in node order.
+        self.local = None
+        if self.resident and local:
+            Ap, perm = A, None
+            if order is not None:
+                perm = order.to(device=dev, dtype=torch.int32).contiguous()
+                Ap = permute_matrix(A, perm)
+            m = cg_local_map(Ap, rb.value, n_cta.value)
+            if m is not None and lib().ab_cg_resident_local_fits(rb.value, m["max_ghost"]) > 0:
+                m["A"] = Ap
+                m["perm"] = perm
+                m["struct"].perm = ptr(perm)
+                m["struct"].prefetch_depth = int(prefetch_depth)
+                pl = perm.to(torch.int64) if perm is not None else None
+                m["dinv"] = dinv[pl].contiguous() if pl is not None else dinv
+                m["fixed"] = (self.fixed[pl].contiguous() if (pl is not None and self.fixed is not None)
+                              else self.fixed)
+                self.local = m
 
     def _m(self, name):
         import contextlib
@@ -153,6 +232,14 @@ class PCG:
         ``zero_b`` re-zeroes b (it is an accumulation buffer of K4)."""
         s = stream_handle()
         A = ctypes.byref(self.A.struct)
+        if self.local is not None:
+            lm = self.local
+            with self._m("K5_cg_resident"):
+                call("ab_cg_resident_local", ctypes.byref(lm["A"].struct), ctypes.byref(lm["struct"]), ptr(b),
+                     ptr(b) if zero_b else None, ptr(lm["fixed"]), ptr(lm["dinv"]), ptr(self.x), ptr(self.z),
+                     int(maxit), float(tol), ptr(self.red), ptr(self.sc), ptr(self.part), s)
+            it = int(self.red[3].item()) if tol > 0 else maxit
+            return self.x, it
         if self.resident:
             with self._m("K5_cg_resident"):
                 call("ab_cg_resident", A, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),

@@ -83,7 +83,8 @@ class FlowSolver:
         self.dinv = torch.empty_like(diag)
         call("ab_reciprocal", n, ptr(diag), ptr(self.dinv), s)
         self.own = own
-        self.pcg = PCG(self.L, self.dinv, fixed=self.p_fixed if pf.any() else None, own=own, halo=halo)
+        self.pcg = PCG(self.L, self.dinv, fixed=self.p_fixed if pf.any() else None, own=own, halo=halo,
+                       order=dm.node_order() if halo is None else None)
         # velocity Dirichlet nodes (sparse list)
         if u_fixed is not None and np.any(u_fixed):
             uf = np.asarray(u_fixed, bool).reshape(n, 3)
