@@ -207,13 +207,28 @@ typedef struct ab_cg_local {
   const int32_t* ghost;
   const int32_t* perm;       /* [n_rows] or NULL */
   int32_t prefetch_depth;
+  int32_t variant;           /* 0: vectors in shared memory; 1: tensor-memory solver (k_cg_tmem) */
+  /* variant 1: the CTA's slices in chunks of `group` slices, each chunk's
+   * values then local columns contiguous: chunk [E0, E1) of entries at byte
+   * 10*E0, values (8 B) first, then columns (2 B). */
+  const unsigned char* packed;
+  int32_t group;
   int32_t pad_;
 } ab_cg_local;
+/* Diagnostics: buf (device, >= 8 * n_cta int64, or NULL to disable) receives
+ * globaltimer stamps of the resident solver's phase boundaries in iteration
+ * 10 (per CTA: loop top, ghosts gathered, phase A reduced, barrier A,
+ * phase B reduced, barrier B). */
+int ab_debug_timeline(int64_t* buf);
 /* 2: fits with x in shared memory, 1: fits with x in global memory, 0: no */
 int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost);
 /* ab_cg_resident with the z gathers served from shared memory: each CTA
  * fetches its ghost z values once per iteration, the SpMV reads z through
  * the 16-bit local columns.  Same iterates as ab_cg_resident. */
+/* > 0 (ring slots) when the tensor-memory solver (variant 1) fits: vectors
+ * x, r, p, q, D^-1 in TMEM, matrix slices streamed by a producer warp into
+ * a shared-memory ring with bulk asynchronous copies. */
+int ab_cg_tmem_fits(int64_t rows_per_cta, int32_t max_ghost, int64_t max_width, int32_t group);
 int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b_in, double* b_zero,
                          const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
                          double* red, double* sc, double* part, void* stream);

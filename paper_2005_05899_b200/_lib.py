@@ -41,7 +41,7 @@ class AbSell(C.Structure):
 class AbCgLocal(C.Structure):
     _fields_ = [("rows_per_cta", i64), ("n_cta", i32), ("max_ghost", i32), ("cols", vp), ("ghost_ptr", vp),
                 ("ghost", vp), ("perm", vp), ("prefetch_depth", i32),
-                ("pad_", i32)]
+                ("variant", i32), ("packed", vp), ("group", i32), ("pad_", i32)]
 
 
 P = C.POINTER
@@ -66,6 +66,8 @@ _SIGS = {
     "ab_cg_resident_fits": ([i64, vp, vp], C.c_int),
     "ab_cg_resident": ([P(AbSell), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp], C.c_int),
     "ab_cg_resident_local_fits": ([i64, i32], C.c_int),
+    "ab_debug_timeline": ([vp], C.c_int),
+    "ab_cg_tmem_fits": ([i64, i32, i64, i32], C.c_int),
     "ab_cg_resident_local": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp],
                              C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),

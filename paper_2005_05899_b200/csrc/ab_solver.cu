@@ -485,6 +485,21 @@ __device__ __forceinline__ void all_sum_par(const double* part, int nb, double* 
 
 constexpr int kLocChunk = 8;
 
+// Optional phase timeline of the resident solvers (ab_debug_timeline):
+// globaltimer stamps of thread 0 of every CTA at the phase boundaries of
+// iteration 10, tl[cta * 8 + k].
+__device__ int64_t* g_timeline = nullptr;
+__device__ __forceinline__ void stamp(int it, int k) {
+  int64_t* tl = g_timeline;
+  if (tl && it == 10 && threadIdx.x == 0) {
+    int64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    tl[blockIdx.x * 8 + k] = t;
+  }
+}
+
+constexpr int kLocRowsPerThread = 8;  // rows_per_cta <= 8 * kResBlock
+
 template <bool XS>
 __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     int64_t n, int64_t rows_per_cta, int max_ghost, const int64_t* __restrict__ sp,
@@ -493,7 +508,6 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     double* b_zero,
     const uint8_t* __restrict__ fixed, const double* __restrict__ dinv, double* __restrict__ x_out, double* zg,
     int maxit, double tol, double* red, double* sc, double* part, unsigned* bar, int pf_depth) {
-  unsigned nbar = 0;
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
   __shared__ double bcast[4];
@@ -510,6 +524,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   double* partA = part;
   double* partB = part + nb;
   double* partI = part + 3 * (size_t)nb;
+  unsigned nbar = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nsl = (nloc + 31) >> 5;
   const int64_t s_first = r0 >> 5;
@@ -531,15 +546,14 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     a0 += ri * zi;
     a1 += ri * ri;
   }
+  if (lane == 0)
+    for (int d = 0; d < pf_depth; ++d)
+      if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
   {
     double v[2] = {a0, a1};
     block_sum<2, kResBlock>(v, sred);
     if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
   }
-  // the first pf_depth slices of every warp go to L2 ahead of phase A
-  if (lane == 0)
-    for (int d = 0; d < pf_depth; ++d)
-      if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
   grid_barrier(bar, ++nbar * nb);
   double t2[2];
   all_sum_par<2>(partI, nb, sred, bcast, t2);
@@ -550,9 +564,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   for (; it < maxit; ++it) {
     if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
     const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    stamp(it, 0);
     // ---- ghost z values of this CTA's columns -> shared memory
     for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + __ldg(gidx + g0 + k));
     __syncthreads();
+    stamp(it, 1);
     // ---- phase A: p = z + beta p; q = A z + beta q (z from shared memory)
     double pq = 0.0;
 #pragma unroll 1
@@ -570,14 +586,23 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         pq += p * q;
       }
     }
+    // D^-1 of this thread's phase-B rows: in flight across the reduction
+    double dv[kLocRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kLocRowsPerThread; ++k) {
+      const int l = threadIdx.x + k * kResBlock;
+      dv[k] = l < nloc ? __ldg(dinv + r0 + l) : 0.0;
+    }
     {
       double v[1] = {pq};
       block_sum<1, kResBlock>(v, sred);
       if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
     }
+    stamp(it, 2);
     grid_barrier(bar, ++nbar * nb);
     double t1[1];
     all_sum_par<1>(partA, nb, sred, bcast, t1);
+    stamp(it, 3);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
     if (lane == 0 && it + 1 < maxit)
@@ -585,34 +610,438 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         if (warp + d * (kResBlock / 32) < nsl)
           prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
     double b0 = 0.0, b1 = 0.0;
-    for (int l = threadIdx.x; l < nloc; l += kResBlock) {
-      if (XS) {
-        sx[l] = fma(alpha, spp[l], sx[l]);
-      } else {
-        const int64_t ni = perm ? (int64_t)perm[r0 + l] : r0 + l;
-        x_out[ni] = fma(alpha, spp[l], x_out[ni]);
+#pragma unroll
+    for (int k = 0; k < kLocRowsPerThread; ++k) {
+      const int l = threadIdx.x + k * kResBlock;
+      if (l < nloc) {
+        if (XS) {
+          sx[l] = fma(alpha, spp[l], sx[l]);
+        } else {
+          const int64_t ni = perm ? (int64_t)perm[r0 + l] : r0 + l;
+          x_out[ni] = fma(alpha, spp[l], x_out[ni]);
+        }
+        const double ri = fma(-alpha, sq[l], sr[l]);
+        const double zi = dv[k] * ri;
+        sr[l] = ri;
+        sz[l] = zi;
+        zg[r0 + l] = zi;
+        b0 += ri * zi;
+        b1 += ri * ri;
       }
-      const double ri = fma(-alpha, sq[l], sr[l]);
-      const double zi = __ldg(dinv + r0 + l) * ri;
-      sr[l] = ri;
-      sz[l] = zi;
-      zg[r0 + l] = zi;
-      b0 += ri * zi;
-      b1 += ri * ri;
     }
     {
       double v[2] = {b0, b1};
       block_sum<2, kResBlock>(v, sred);
       if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
     }
+    stamp(it, 4);
     grid_barrier(bar, ++nbar * nb);
     all_sum_par<2>(partB, nb, sred, bcast, t2);
+    stamp(it, 5);
     rz_old = rz;
     rz = t2[0];
     rr = t2[1];
   }
   if (XS)
     for (int l = threadIdx.x; l < nloc; l += kResBlock) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = sx[l];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    red[AB_RED_RZN] = rz;
+    red[AB_RED_RR] = rr;
+    red[AB_RED_ITERS] = (double)it;
+    sc[AB_SC_BB] = bb;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Resident CG, tensor-memory form (k_cg_tmem).  Same algorithm and local
+// column map as k_cg_resident_local, organised for sm_100a:
+//  * the per-row CG vectors x, r, p, q and D^-1 live in TENSOR MEMORY (256 KB
+//    per SM, tcgen05.ld/st, no tensor-core use): each consumer warp owns the
+//    rows of its slices in its 32-lane quarter of TMEM, so shared memory only
+//    holds z (own rows + ghosts);
+//  * one producer warp streams the CTA's SELL slices (values + 16-bit local
+//    columns) into a shared-memory ring with bulk asynchronous copies
+//    (cp.async.bulk -> UBLKCP, mbarrier full/empty handshake).  The matrix
+//    does not change, so the producer runs ahead across the grid barriers:
+//    the next iteration's first slices land while the reductions complete;
+//  * kTmNC consumer warps gather z from shared memory and synchronise among
+//    themselves with a named barrier; the producer never joins them.
+// Slice sl of the CTA is consumed by warp sl % kTmNC (row slot sl / kTmNC).
+// Iterates equal k_cg_resident_local's (same per-row operation order); the
+// dot products are summed in a different (fixed) tree.
+// ---------------------------------------------------------------------------
+constexpr int kTmNC = 24;
+constexpr int kTmThreads = (kTmNC + 1) * 32;
+constexpr int kTmCols = (512 / (kTmNC / 4)) & ~1;  // TMEM columns per consumer warp
+constexpr int kTmMaxSlots = kTmCols / 10;   // row slots per thread (5 doubles each)
+
+__device__ __forceinline__ uint32_t sa32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kTmNC * 32) : "memory"); }
+
+__device__ __forceinline__ void mb_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mb_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mb_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(sa32(b)) : "memory");
+}
+__device__ __forceinline__ bool mb_test(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(sa32(b)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+__device__ __forceinline__ void mb_wait(uint64_t* b, uint32_t parity) {
+  while (!mb_test(b, parity)) {
+  }
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   sa32(dst)),
+               "l"(src), "r"(bytes), "r"(sa32(b))
+               : "memory");
+}
+
+// TMEM: one double per thread = two 32-bit columns of the thread's lane.
+__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t& lo, uint32_t& hi) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a) : "memory");
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ double tm_val(uint32_t lo, uint32_t hi) {
+  asm volatile("" : "+r"(lo), "+r"(hi));  // keep uses after tcgen05.wait::ld
+  return __hiloint2double((int)hi, (int)lo);
+}
+__device__ __forceinline__ void tm_st(uint32_t a, double v) {
+  const uint32_t lo = (uint32_t)__double2loint(v), hi = (uint32_t)__double2hiint(v);
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(lo), "r"(hi) : "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// Sum over the consumer warps (valid in warp 0); sm >= NV * kTmNC doubles.
+template <int NV>
+__device__ __forceinline__ void cons_sum(double (&v)[NV], double* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < NV; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+  if (lane == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) sm[k * kTmNC + warp] = v[k];
+  cbar();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double t = lane < kTmNC ? sm[k * kTmNC + lane] : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+      v[k] = t;
+    }
+  }
+}
+
+__device__ __forceinline__ void cons_grid_barrier(unsigned* cnt, unsigned target) {
+  cbar();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+  }
+  cbar();
+}
+
+// Ordered sum of nb per-CTA partials (nb <= kTmNC * 32), identical in every CTA.
+template <int NV>
+__device__ __forceinline__ void cons_all_sum(const double* part, int nb, double* sm, double* bcast,
+                                             double (&out)[NV]) {
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = (int)threadIdx.x < nb ? __ldcg(part + (size_t)k * nb + threadIdx.x) : 0.0;
+  cons_sum<NV>(v, sm);
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bcast[k] = v[k];
+  cbar();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
+}
+
+struct TmLayout {
+  int ring;      // slots
+  int maxw;      // widest slice (entries per lane)
+  int kslots;    // row slots per consumer thread
+  int group;     // slices per chunk (one bulk copy)
+};
+
+__global__ void __launch_bounds__(kTmThreads, 1) k_cg_tmem(
+    int64_t n, int64_t rows_per_cta, int max_ghost, TmLayout L, const int64_t* __restrict__ sp,
+    const unsigned char* __restrict__ packed, const int32_t* __restrict__ gptr,
+    const int32_t* __restrict__ gidx, const int32_t* __restrict__ perm, const double* __restrict__ b_in,
+    double* b_zero, const uint8_t* __restrict__ fixed, const double* __restrict__ dinv, double* __restrict__ x_out,
+    double* zg, int maxit, double tol, double* red, double* sc, double* part, unsigned* bar) {
+  extern __shared__ __align__(128) unsigned char tsm[];
+  __shared__ double sred[2 * kTmNC];
+  __shared__ double bcast[4];
+  __shared__ uint32_t s_taddr;
+  __shared__ volatile int s_stop;  // iteration at which the consumers stopped (-1: running)
+  __shared__ volatile int s_seq[64];  // chunk sequence number last issued into each slot
+  const int nb = gridDim.x;
+  const int64_t RB = rows_per_cta;
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int64_t r1 = r0 + RB < n ? r0 + RB : n;
+  const int nloc = r1 > r0 ? (int)(r1 - r0) : 0;
+  const int nsl = (nloc + 31) >> 5;
+  const int64_t s_first = r0 >> 5;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g0 = gptr[blockIdx.x];
+  const int ng = gptr[blockIdx.x + 1] - g0;
+  const int G = L.group;
+  const int nch = (nsl + G - 1) / G;  // chunks per iteration
+  const uint32_t slot_bytes = (uint32_t)(G * L.maxw) * 320u;
+  // shared memory carve-up
+  double* sz = reinterpret_cast<double*>(tsm);                     // [RB + max_ghost]
+  size_t off = ((size_t)(RB + max_ghost) * 8 + 127) & ~(size_t)127;
+  unsigned char* ring = tsm + off;                                 // [ring][slot_bytes]
+  off += (size_t)L.ring * slot_bytes;
+  int64_t* ssp = reinterpret_cast<int64_t*>(tsm + off);            // [nsl + 1]
+  off += ((size_t)(RB / 32 + 1) * 8 + 15) & ~(size_t)15;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tsm + off);          // [ring]
+  uint64_t* empty = full + L.ring;                                  // [ring]
+  off += (size_t)2 * L.ring * 8;
+  int32_t* sgid = reinterpret_cast<int32_t*>(tsm + off);           // [max_ghost]
+
+  for (int k = threadIdx.x; k <= nsl; k += kTmThreads) ssp[k] = sp[s_first + k];
+  for (int k = threadIdx.x; k < ng; k += kTmThreads) sgid[k] = gidx[g0 + k];
+  if (threadIdx.x == 0) {
+    for (int k = 0; k < L.ring; ++k) {
+      mb_init(full + k, 1);
+      mb_init(empty + k, (unsigned)G);
+      s_seq[k] = -1;
+    }
+    s_stop = -1;
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sa32(&s_taddr))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  if (warp == kTmNC) {
+    // ================= producer: stream the slices, iteration after iteration
+    if (lane == 0) {
+      // chunk Q = it * nch + c covers slices [cG, min(cG + G, nsl)): one bulk
+      // copy of their packed values + columns (10 bytes per entry, contiguous
+      // in the packed buffer).  Counters kept incrementally (no division).
+      const int total = maxit * nch;
+      int q = 0, it = 0, c = 0, slot = 0;
+      uint32_t par = 0;
+      for (; q < total; ++q) {
+        bool stop = false;
+        if (q >= L.ring) {
+          while (!mb_test(empty + slot, par ^ 1u)) {
+            const int st = s_stop;
+            if (st >= 0 && it >= st) { stop = true; break; }
+          }
+        }
+        if (!stop) {
+          const int st = s_stop;
+          if (st >= 0 && it >= st) stop = true;
+        }
+        if (stop) break;
+        const int c0 = c * G, c1 = c0 + G < nsl ? c0 + G : nsl;
+        const int64_t e0 = ssp[c0];
+        const uint32_t bytes = (uint32_t)(ssp[c1] - e0) * 10u;
+        mb_expect_tx(full + slot, bytes);
+        bulk_g2s(ring + (size_t)slot * slot_bytes, packed + 10 * e0, bytes, full + slot);
+        for (int k = c1 - c0; k < G; ++k) mb_arrive(empty + slot);  // slices a short chunk lacks
+        s_seq[slot] = q;
+        if (++slot == L.ring) { slot = 0; par ^= 1u; }
+        if (++c == nch) { c = 0; ++it; }
+      }
+      // drain: copies issued but never consumed must land before exit
+      const int st = s_stop;
+      const int consumed = st >= 0 ? st * nch : total;
+      for (int k = (consumed > q - L.ring ? consumed : q - L.ring); k < q; ++k)
+        mb_wait(full + (k % L.ring), (uint32_t)((k / L.ring) & 1));
+    }
+    return;
+  }
+
+  // ================= consumers
+  const uint32_t tbase = s_taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * kTmCols);
+  const int K = L.kslots;
+  auto tcol = [&](int v, int k) -> uint32_t { return tbase + (uint32_t)(v * 2 * K + 2 * k); };
+  enum { VX = 0, VR = 1, VP = 2, VQ = 3, VD = 4 };
+  double* partA = part;
+  double* partB = part + nb;
+  double* partI = part + 3 * (size_t)nb;
+  unsigned nbar = 0;
+
+  // init: r = b (fixed rows 0), z = D^-1 r, x = p = q = 0
+  double a0 = 0.0, a1 = 0.0;
+  for (int k = 0; k < K; ++k) {
+    const int sl = warp + k * kTmNC;
+    const int l = sl * 32 + lane;
+    double ri = 0.0, di = 0.0;
+    if (sl < nsl && l < nloc) {
+      const int64_t i = r0 + l;
+      const int64_t ni = perm ? (int64_t)perm[i] : i;
+      ri = b_in[ni];
+      if (fixed && fixed[i]) ri = 0.0;
+      if (b_zero) b_zero[ni] = 0.0;
+      di = dinv[i];
+      const double zi = di * ri;
+      sz[l] = zi;
+      zg[i] = zi;
+      a0 += ri * zi;
+      a1 += ri * ri;
+    }
+    tm_st(tcol(VX, k), 0.0);
+    tm_st(tcol(VR, k), ri);
+    tm_st(tcol(VP, k), 0.0);
+    tm_st(tcol(VQ, k), 0.0);
+    tm_st(tcol(VD, k), di);
+  }
+  tm_wait_st();
+  {
+    double v[2] = {a0, a1};
+    cons_sum<2>(v, sred);
+    if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
+  }
+  cons_grid_barrier(bar, ++nbar * nb);
+  double t2[2];
+  cons_all_sum<2>(partI, nb, sred, bcast, t2);
+  double rz = t2[0], rr = t2[1];
+  const double bb = rr;
+  double rz_old = 0.0;
+  int it = 0;
+  for (; it < maxit; ++it) {
+    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
+    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    for (int k = threadIdx.x; k < ng; k += kTmNC * 32) sz[RB + k] = __ldcg(zg + sgid[k]);
+    cbar();
+    // ---- phase A
+    double pq = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const int sl = warp + k * kTmNC;
+      if (sl >= nsl) break;  // warp-uniform
+      uint32_t plo, phi, qlo, qhi;
+      tm_ld(tcol(VP, k), plo, phi);
+      tm_ld(tcol(VQ, k), qlo, qhi);
+      const int c = sl / G;
+      const int qi = it * nch + c;
+      const unsigned qd = (unsigned)qi / (unsigned)L.ring;
+      const int slot = (int)((unsigned)qi - qd * (unsigned)L.ring);
+      while (s_seq[slot] != qi) {
+      }
+      mb_wait(full + slot, qd & 1u);
+      const int64_t ce0 = ssp[c * G], ce1 = ssp[(c * G + G) < nsl ? c * G + G : nsl];
+      const int64_t so = ssp[sl] - ce0;
+      const double* sv = reinterpret_cast<const double*>(ring + (size_t)slot * slot_bytes) + so;
+      const uint16_t* sc16 =
+          reinterpret_cast<const uint16_t*>(ring + (size_t)slot * slot_bytes + (size_t)(ce1 - ce0) * 8) + so;
+      const int width = (int)((ssp[sl + 1] - ssp[sl]) >> 5);
+      double acc = 0.0;
+      for (int j0 = 0; j0 < width; j0 += 8) {
+        unsigned cj[8];
+        double aj[8], gj[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const bool ok = j0 + u < width;
+          cj[u] = ok ? (unsigned)sc16[(j0 + u) * 32 + lane] : 0u;
+          aj[u] = ok ? sv[(j0 + u) * 32 + lane] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) gj[u] = sz[cj[u]];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc = fma(aj[u], gj[u], acc);
+      }
+      __syncwarp();
+      if (lane == 0) mb_arrive(empty + slot);
+      tm_wait_ld();
+      const int l = sl * 32 + lane;
+      const double p = fma(beta, tm_val(plo, phi), l < nloc ? sz[l] : 0.0);
+      const double q = fma(beta, tm_val(qlo, qhi), acc);
+      tm_st(tcol(VP, k), p);
+      tm_st(tcol(VQ, k), q);
+      if (l < nloc) pq += p * q;
+    }
+    tm_wait_st();
+    {
+      double v[1] = {pq};
+      cons_sum<1>(v, sred);
+      if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+    }
+    cons_grid_barrier(bar, ++nbar * nb);
+    double t1[1];
+    cons_all_sum<1>(partA, nb, sred, bcast, t1);
+    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+    // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
+    double b0 = 0.0, b1 = 0.0;
+    for (int k = 0; k < K; ++k) {
+      const int sl = warp + k * kTmNC;
+      if (sl >= nsl) break;
+      uint32_t v[5][2];
+      tm_ld(tcol(VX, k), v[0][0], v[0][1]);
+      tm_ld(tcol(VR, k), v[1][0], v[1][1]);
+      tm_ld(tcol(VP, k), v[2][0], v[2][1]);
+      tm_ld(tcol(VQ, k), v[3][0], v[3][1]);
+      tm_ld(tcol(VD, k), v[4][0], v[4][1]);
+      tm_wait_ld();
+      const double xi = fma(alpha, tm_val(v[2][0], v[2][1]), tm_val(v[0][0], v[0][1]));
+      const double ri = fma(-alpha, tm_val(v[3][0], v[3][1]), tm_val(v[1][0], v[1][1]));
+      const double zi = tm_val(v[4][0], v[4][1]) * ri;
+      tm_st(tcol(VX, k), xi);
+      tm_st(tcol(VR, k), ri);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        sz[l] = zi;
+        zg[r0 + l] = zi;
+        b0 += ri * zi;
+        b1 += ri * ri;
+      }
+    }
+    tm_wait_st();
+    {
+      double v[2] = {b0, b1};
+      cons_sum<2>(v, sred);
+      if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
+    }
+    cons_grid_barrier(bar, ++nbar * nb);
+    cons_all_sum<2>(partB, nb, sred, bcast, t2);
+    rz_old = rz;
+    rz = t2[0];
+    rr = t2[1];
+  }
+  if (threadIdx.x == 0) s_stop = it;
+  // x -> node order
+  for (int k = 0; k < K; ++k) {
+    const int sl = warp + k * kTmNC;
+    if (sl >= nsl) break;
+    uint32_t lo, hi;
+    tm_ld(tcol(VX, k), lo, hi);
+    tm_wait_ld();
+    const int l = sl * 32 + lane;
+    if (l < nloc) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = tm_val(lo, hi);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cbar();
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(s_taddr) : "memory");
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     red[AB_RED_RZN] = rz;
     red[AB_RED_RR] = rr;
@@ -760,9 +1189,42 @@ int local_mode(int64_t rb, int32_t max_ghost, size_t* bytes) {
 
 extern "C" {
 
+int ab_debug_timeline(int64_t* buf) {
+  if (cudaMemcpyToSymbol(g_timeline, &buf, sizeof(buf)) != cudaSuccess) return fail("ab_debug_timeline: copy failed");
+  return AB_OK;
+}
+
 int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost) {
   return local_mode(rows_per_cta, max_ghost, nullptr);
 }
+
+namespace {
+// Launch shape of k_cg_tmem for rows_per_cta/max_ghost/max_width, or false.
+bool tmem_layout(int64_t rb, int32_t max_ghost, int64_t max_width, int32_t group, TmLayout* L, size_t* bytes) {
+  int dev = 0, optin = 0, coop = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop || max_width <= 0 || group <= 0 || rb + max_ghost > 65536) return false;
+  const int64_t nsl = rb / 32;
+  const int k = (int)((nsl + kTmNC - 1) / kTmNC);
+  if (k > kTmMaxSlots) return false;
+  const size_t cap = (size_t)optin - 1024;
+  size_t fixed_bytes = (((size_t)(rb + max_ghost) * 8 + 127) & ~(size_t)127) + (((size_t)(nsl + 1) * 8 + 15) & ~(size_t)15) +
+                       (size_t)max_ghost * 4 + 64;
+  const size_t slot = (size_t)max_width * group * 320;
+  if (fixed_bytes >= cap) return false;
+  int ring = (int)((cap - fixed_bytes) / (slot + 16));
+  if (ring > 64) ring = 64;
+  if (ring < 4) return false;
+  L->ring = ring;
+  L->maxw = (int)max_width;
+  L->kslots = k;
+  L->group = group;
+  *bytes = fixed_bytes + (size_t)ring * (slot + 16);
+  return true;
+}
+}  // namespace
 
 int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b_in, double* b_zero,
                          const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
@@ -774,12 +1236,6 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
   ab_cg_resident_fits(n, &rb, &ncta);
   if (rb != m->rows_per_cta || ncta != m->n_cta)
     return fail("ab_cg_resident_local: column map built for another launch shape");
-  size_t smem = 0;
-  const int mode = local_mode(rb, m->max_ghost, &smem);
-  if (mode == 0) return fail("ab_cg_resident_local: system does not fit in shared memory");
-  const void* fn = mode == 2 ? (const void*)k_cg_resident_local<true> : (const void*)k_cg_resident_local<false>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
-    return fail("ab_cg_resident_local: cannot reserve shared memory");
   const int64_t* sp = a->slice_ptr;
   const uint16_t* lcol = m->cols;
   const double* vals = a->vals;
@@ -792,15 +1248,46 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
   unsigned* bar = reinterpret_cast<unsigned*>(part + 5 * (size_t)ncta);
   if (cudaMemsetAsync(bar, 0, sizeof(unsigned), S(stream)) != cudaSuccess)
     return fail("ab_cg_resident_local: cannot reset the barrier counter");
-  void* args[] = {&n,           &rb,          &mg,  (void*)&sp, (void*)&lcol, (void*)&vals, (void*)&gp,
-                  (void*)&gi,   (void*)&pm,   (void*)&b_in, &b_zero, (void*)&fixed, (void*)&dinv, &x, &z,
-                  &mi,          &tol,         &red, &sc, &part, &bar, &depth};
-  cudaError_t e = cudaLaunchCooperativeKernel(fn, dim3(ncta), dim3(kResBlock), args, smem, S(stream));
+  cudaError_t e;
+  TmLayout L{};
+  size_t smem = 0;
+  if (m->variant == 1) {
+    if (!m->packed) return fail("ab_cg_resident_local: the tensor-memory solver needs the packed matrix");
+    if (!tmem_layout(rb, mg, a->max_width, m->group, &L, &smem))
+      return fail("ab_cg_resident_local: system does not fit the tensor-memory solver");
+    if (cudaFuncSetAttribute((const void*)k_cg_tmem, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return fail("ab_cg_resident_local: cannot reserve shared memory");
+    const void* pk = m->packed;
+    void* args[] = {&n,          &rb,         &mg,         &L,           (void*)&sp,   (void*)&pk,
+                    (void*)&gp,  (void*)&gi,  (void*)&pm,  (void*)&b_in, &b_zero,      (void*)&fixed,
+                    (void*)&dinv, &x,         &z,          &mi,          &tol,         &red,
+                    &sc,         &part,       &bar};
+    e = cudaLaunchCooperativeKernel((const void*)k_cg_tmem, dim3(ncta), dim3(kTmThreads), args, smem, S(stream));
+  } else {
+    const int mode = local_mode(rb, mg, &smem);
+    if (mode == 0) return fail("ab_cg_resident_local: system does not fit in shared memory");
+    if (rb > (int64_t)kLocRowsPerThread * kResBlock) return fail("ab_cg_resident_local: too many rows per CTA");
+
+    const void* fn = mode == 2 ? (const void*)k_cg_resident_local<true> : (const void*)k_cg_resident_local<false>;
+    if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail("ab_cg_resident_local: cannot reserve shared memory");
+    void* args[] = {&n,           &rb,          &mg,  (void*)&sp, (void*)&lcol, (void*)&vals, (void*)&gp,
+                    (void*)&gi,   (void*)&pm,   (void*)&b_in, &b_zero, (void*)&fixed, (void*)&dinv, &x, &z,
+                    &mi,          &tol,         &red, &sc, &part, &bar, &depth};
+    e = cudaLaunchCooperativeKernel(fn, dim3(ncta), dim3(kResBlock), args, smem, S(stream));
+  }
   if (e != cudaSuccess) {
     set_error(std::string("ab_cg_resident_local: ") + cudaGetErrorString(e));
     return AB_ECUDA;
   }
   return check_launch("ab_cg_resident_local");
+}
+
+int ab_cg_tmem_fits(int64_t rows_per_cta, int32_t max_ghost, int64_t max_width, int32_t group) {
+  TmLayout L{};
+  size_t b = 0;
+  return tmem_layout(rows_per_cta, max_ghost, max_width, group, &L, &b) ? L.ring : 0;
 }
 
 }  // extern "C"

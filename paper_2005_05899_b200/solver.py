@@ -152,6 +152,33 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
     return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct)
 
 
+def pack_chunks(A: SellMatrix, lcols: torch.Tensor, rows_per_cta: int, group: int) -> torch.Tensor:
+    """Packed matrix stream of the tensor-memory solver (ab_cg_local.packed):
+    the slices of every CTA in chunks of ``group``; chunk [E0, E1) of entries
+    occupies bytes [10 E0, 10 E1): its values, then its 16-bit columns."""
+    sp = A.slice_ptr
+    dev = A.vals.device
+    total = int(sp[-1].item())
+    n_sl = sp.numel() - 1
+    spc = rows_per_cta // 32
+    s = torch.arange(n_sl, device=dev)
+    b = s // spc
+    c_end = torch.minimum(torch.minimum(b * spc + (s - b * spc) // group * group + group, (b + 1) * spc),
+                          torch.full_like(s, n_sl))
+    c_beg = b * spc + (s - b * spc) // group * group
+    counts = sp[1:] - sp[:-1]
+    e = torch.arange(total, device=dev)
+    slice_of = torch.repeat_interleave(s, counts)
+    E0 = sp[c_beg][slice_of]
+    E1 = sp[c_end][slice_of]
+    packed = torch.zeros(total * 10, dtype=torch.uint8, device=dev)
+    pv = packed.view(torch.float64)
+    pc = packed.view(torch.int16)
+    pv[(E0 // 32) * 40 + (e - E0)] = A.vals
+    pc[5 * E0 + 4 * (E1 - E0) + (e - E0)] = lcols
+    return packed
+
+
 def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
     """Assemble L (SPD after Dirichlet rows/cols of ``fixed`` -> identity)."""
     dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
@@ -174,7 +201,8 @@ class PCG:
 
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
-                 order: torch.Tensor | None = None, prefetch_depth: int = 1):
+                 order: torch.Tensor | None = None, prefetch_depth: int = 1,
+                 tmem: bool = False, group: int = 0):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -191,7 +219,7 @@ class PCG:
         n_cta = C.c_int32(0)
         rb = C.c_int64(0)
         fits = lib().ab_cg_resident_fits(n, C.byref(rb), C.byref(n_cta))
-        self.part = torch.zeros(max(2 * (nb + ng), 5 * n_cta.value + 1) + 8, dtype=torch.float64, device=dev)
+        self.part = torch.zeros(max(2 * (nb + ng), 12 * n_cta.value + 1) + 8, dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)
@@ -216,6 +244,14 @@ class PCG:
                 m["perm"] = perm
                 m["struct"].perm = ptr(perm)
                 m["struct"].prefetch_depth = int(prefetch_depth)
+                # tensor-memory solver when it fits (ab_cg_tmem_fits)
+                group = int(group) if group else max(1, -(-16384 // max(1, Ap.max_width * 256)))
+                m["tmem"] = bool(tmem and lib().ab_cg_tmem_fits(rb.value, m["max_ghost"], Ap.max_width, group) > 0)
+                m["struct"].variant = 1 if m["tmem"] else 0
+                if m["tmem"]:
+                    m["packed"] = pack_chunks(Ap, m["cols"], rb.value, group)
+                    m["struct"].packed = ptr(m["packed"])
+                    m["struct"].group = group
                 pl = perm.to(torch.int64) if perm is not None else None
                 m["dinv"] = dinv[pl].contiguous() if pl is not None else dinv
                 m["fixed"] = (self.fixed[pl].contiguous() if (pl is not None and self.fixed is not None)

@@ -22,10 +22,13 @@ b = torch.randn(A.n_rows, dtype=torch.float64, device="cuda")
 b[fixed.cuda()] = 0
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 order = dm.node_order()
-depths = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else [0, 2, 3, 4]
+depths = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else []
 variants = {
-    "local+sfc": dict(order=order),
-    **{f"depth{k}": dict(order=order, prefetch_depth=k) for k in depths},
+    "tmem": dict(order=order),
+    "tmem-g2": dict(order=order, group=2),
+    "tmem-g8": dict(order=order, group=8),
+    "local+sfc": dict(order=order, tmem=False),
+    **{f"depth{k}": dict(order=order, prefetch_depth=k, tmem=False) for k in depths},
     "local": dict(),
     "resident": dict(local=False),
     "two-kernel": dict(resident=False),
@@ -35,7 +38,7 @@ for name, kw in variants.items():
     pcg = PCG(A, dinv, fixed=fixed, **kw)
     info = ""
     if pcg.local is not None:
-        info = f"max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
+        info = f"tmem={pcg.local['tmem']} group={pcg.local['struct'].group} max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
     pcg.solve(b.clone(), its, zero_b=False)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
