@@ -151,6 +151,8 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
         return conn_bytes + 24 * N + 8 * N + 24 * N, 0
     if kernel == "K7_correct":
         return 24 * 3 * N + 8 * N + 16 * N + 24 * 3 * N, 6 * N
+    if kernel == "K67_grad_correct":  # K6 + K7 without the G dp round trip
+        return conn_bytes + 24 * N + 8 * N + 24 * N + 8 * N + 16 * N + 48 * N + 24 * N, 6 * N
     return 0, 0
 
 

@@ -233,6 +233,30 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
                          const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
                          double* red, double* sc, double* part, void* stream);
 
+/* ---- discrete gradient operator B_ab = int N_a grad N_b ----------------
+ * (DESIGN.md §4).  Assembled once into the Laplacian's CSR pattern (3
+ * value planes), stored as SELL-32 with three lane-innermost value planes;
+ * K4 and K6(+K7) become sparse products streaming it at HBM speed. */
+typedef struct ab_sell3 {
+  int64_t n_rows;
+  int64_t n_slices;
+  const int64_t* slice_ptr;
+  const int32_t* cols;
+  const double* vx;
+  const double* vy;
+  const double* vz;
+} ab_sell3;
+int ab_gradop_csr(const ab_mesh* mesh, const int64_t* row_ptr, const int32_t* cols, double* vx, double* vy,
+                  double* vz, void* stream);
+/* K4:  out[a] += scale * sum_b B_ab . u4[b]  (replaces ab_divergence) */
+int ab_gradop_div(const ab_sell3* b, const double* u4, double scale, double* out, void* stream);
+/* K6:  out4[a] += scale * sum_b B_ab p[b]  (replaces ab_gradient) */
+int ab_gradop_grad(const ab_sell3* b, const double* p, double scale, double* out4, void* stream);
+/* K6 + K7 in one pass: gd = B dp; uout = uin - k*minv*gd; p += dp; gp += gd
+ * (single domain: no interface sum between K6 and K7).  uin may == uout. */
+int ab_gradop_correct(const ab_sell3* b, const double* dp, double k, const double* uin, double* uout,
+                      const double* minv, double* p, double* gp, void* stream);
+
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */
 int ab_rk_stage(int64_t n, double a, double b, double k, const double* u0, const double* uprev,

@@ -38,6 +38,11 @@ class AbSell(C.Structure):
                 ("vals", vp)]
 
 
+class AbSell3(C.Structure):
+    _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cols", vp), ("vx", vp), ("vy", vp),
+                ("vz", vp)]
+
+
 class AbCgLocal(C.Structure):
     _fields_ = [("rows_per_cta", i64), ("n_cta", i32), ("max_ghost", i32), ("cols", vp), ("ghost_ptr", vp),
                 ("ghost", vp), ("perm", vp), ("prefetch_depth", i32),
@@ -70,6 +75,10 @@ _SIGS = {
     "ab_cg_tmem_fits": ([i64, i32, i64, i32], C.c_int),
     "ab_cg_resident_local": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp],
                              C.c_int),
+    "ab_gradop_csr": ([P(AbMesh), vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_gradop_div": ([P(AbSell3), vp, f64, vp, vp], C.c_int),
+    "ab_gradop_grad": ([P(AbSell3), vp, f64, vp, vp], C.c_int),
+    "ab_gradop_correct": ([P(AbSell3), vp, f64, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),

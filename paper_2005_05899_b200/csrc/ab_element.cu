@@ -1073,6 +1073,56 @@ __global__ void k_laplacian(CatP c, const int64_t* __restrict__ rp, const int32_
     }
 }
 
+// Discrete gradient operator B_ab = int N_a grad N_b (3 planes) into the
+// CSR pattern of the Laplacian (setup).  With it K4 is b = scale B . u and
+// K6 is G p = B p as sparse products (ab_gradop_div / ab_gradop_grad); the
+// Gauss sums are those of divergence_element / gradient_element.
+template <int R>
+__global__ void k_gradop(CatP c, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                         double* __restrict__ vx, double* __restrict__ vy, double* __restrict__ vz) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.n) return;
+  int nd[NN];
+  load_conn<NN>(c.conn, e, nd);
+  double x[NN][3];
+  load_coords<NN>(c, nd, x);
+  double be[NN][NN][3];
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) be[a][b][0] = be[a][b][1] = be[a][b][2] = 0.0;
+#pragma unroll 1
+  for (int g = 0; g < (RuleT<R>::TET ? 1 : NG); ++g) {
+    double dNdx[NN][3];
+    const double adet = fabs(shape_grads<R, NN>(x, g, dNdx));
+#pragma unroll
+    for (int gg = 0; gg < (RuleT<R>::TET ? NG : 1); ++gg) {
+      const int gi = RuleT<R>::TET ? gg : g;
+      const double f = adet * c_w[R][gi];
+#pragma unroll
+      for (int a = 0; a < NN; ++a) {
+        const double fn = f * c_N[R][gi][a];
+#pragma unroll
+        for (int b = 0; b < NN; ++b)
+#pragma unroll
+          for (int k = 0; k < 3; ++k) be[a][b][k] = fma(fn, dNdx[b][k], be[a][b][k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < NN; ++a)
+#pragma unroll
+    for (int b = 0; b < NN; ++b) {
+      const int64_t pos = csr_find(rp, cols, nd[a], nd[b]);
+      if (pos >= 0) {
+        red_add(vx + pos, be[a][b][0]);
+        red_add(vy + pos, be[a][b][1]);
+        red_add(vz + pos, be[a][b][2]);
+      }
+    }
+}
+
 // centroid = (sum_a x_a) / nnode, sequential in node order (numpy mean over
 // axis 0 of the (nnode,3) gather, reference mesh.py:375).
 template <int R>
@@ -1294,6 +1344,22 @@ int ab_laplacian_csr(const ab_mesh* m, const int64_t* rp, const int32_t* cols, d
     int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
       k_laplacian<decltype(r)::value><<<grid_for(c.n, 128), 128, 0, S(stream)>>>(c, rp, cols, vals);
       return check_launch("ab_laplacian_csr");
+    });
+    if (rc) return rc;
+  }
+  return AB_OK;
+}
+
+int ab_gradop_csr(const ab_mesh* m, const int64_t* rp, const int32_t* cols, double* vx, double* vy, double* vz,
+                  void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  if (!rp || !cols || !vx || !vy || !vz) return fail("ab_gradop_csr: null argument");
+  for (int k = 0; k < m->n_cat; ++k) {
+    CatP c = cat_params(m, k);
+    if (c.n == 0) continue;
+    int rc = dispatch_rule(m->cat[k].rule, [&](auto r) {
+      k_gradop<decltype(r)::value><<<grid_for(c.n, 128), 128, 0, S(stream)>>>(c, rp, cols, vx, vy, vz);
+      return check_launch("ab_gradop_csr");
     });
     if (rc) return rc;
   }

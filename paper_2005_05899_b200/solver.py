@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import AbCgLocal, AbSell, call, lib, ptr, stream_handle
+from ._lib import AbCgLocal, AbSell, AbSell3, call, lib, ptr, stream_handle
 from .device import DeviceMesh
 
 
@@ -189,6 +189,48 @@ def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
         f8 = fixed.to(device=dm.device, dtype=torch.uint8).contiguous()
         call("ab_csr_dirichlet", dm.n_nodes, ptr(row_ptr), ptr(cols), ptr(vals), ptr(f8), stream_handle())
     return csr_to_sell(dm.n_nodes, row_ptr, cols, vals)
+
+
+@dataclass
+class GradOp:
+    """Discrete gradient operator B_ab = int N_a grad N_b (3 planes, SELL-32):
+    K4 is scale B . u, K6 is B p."""
+    n_rows: int
+    slice_ptr: torch.Tensor
+    cols: torch.Tensor
+    vx: torch.Tensor
+    vy: torch.Tensor
+    vz: torch.Tensor
+
+    def __post_init__(self):
+        self.struct = AbSell3(n_rows=self.n_rows, n_slices=self.slice_ptr.numel() - 1, slice_ptr=ptr(self.slice_ptr),
+                              cols=ptr(self.cols), vx=ptr(self.vx), vy=ptr(self.vy), vz=ptr(self.vz))
+
+    @property
+    def nnz_stored(self) -> int:
+        return int(self.cols.numel())
+
+    def div(self, u4: torch.Tensor, scale: float, out: torch.Tensor) -> torch.Tensor:
+        call("ab_gradop_div", ctypes.byref(self.struct), ptr(u4), float(scale), ptr(out), stream_handle())
+        return out
+
+    def grad(self, p: torch.Tensor, scale: float, out4: torch.Tensor) -> torch.Tensor:
+        call("ab_gradop_grad", ctypes.byref(self.struct), ptr(p), float(scale), ptr(out4), stream_handle())
+        return out4
+
+
+def assemble_gradient_operator(mesh, pattern=None) -> GradOp:
+    """B_ab = sum_e int N_a grad N_b on the node-adjacency pattern (the
+    Laplacian's; pass ``pattern=(row_ptr, cols)`` to reuse it)."""
+    dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
+    row_ptr, cols = pattern if pattern is not None else csr_pattern(dm)
+    nnz = cols.numel()
+    v = [torch.zeros(nnz, dtype=torch.float64, device=dm.device) for _ in range(3)]
+    call("ab_gradop_csr", ctypes.byref(dm.struct), ptr(row_ptr), ptr(cols), ptr(v[0]), ptr(v[1]), ptr(v[2]),
+         stream_handle())
+    planes = [csr_to_sell(dm.n_nodes, row_ptr, cols, vk) for vk in v]
+    return GradOp(n_rows=dm.n_nodes, slice_ptr=planes[0].slice_ptr, cols=planes[0].cols, vx=planes[0].vals,
+                  vy=planes[1].vals, vz=planes[2].vals)
 
 
 class PCG:

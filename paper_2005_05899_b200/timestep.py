@@ -28,7 +28,7 @@ import torch
 from ._lib import AbPhys, call, ptr, stream_handle
 from .device import DeviceMesh, nodes_as4
 from .meshgen import MeshArrays
-from .solver import PCG, assemble_laplacian
+from .solver import PCG, assemble_gradient_operator, assemble_laplacian
 
 RK3_A = (0.0, 0.75, 1.0 / 3.0)
 RK3_B = (1.0, 0.25, 2.0 / 3.0)
@@ -53,7 +53,7 @@ class FlowSolver:
     """
 
     def __init__(self, mesh, params: FlowParams | None = None, p_fixed=None, u_fixed=None, u_fixed_values=None,
-                 windows: bool = True, reorder: str | None = "sfc", halo=None, own=None):
+                 windows: bool = True, reorder: str | None = "sfc", halo=None, own=None, ops: str = "spmv"):
         self.params = params or FlowParams()
         self.phys = self.params.struct()
         self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows)
@@ -83,6 +83,12 @@ class FlowSolver:
         self.dinv = torch.empty_like(diag)
         call("ab_reciprocal", n, ptr(diag), ptr(self.dinv), s)
         self.own = own
+        # K4/K6: sparse products with the assembled gradient operator
+        # ("spmv", default) or the element loops ("element")
+        if ops not in ("spmv", "element"):
+            raise ValueError(f"ops must be 'spmv' or 'element', not {ops!r}")
+        self.ops = ops
+        self.Bop = assemble_gradient_operator(dm, pattern=self.L.csr[:2]) if ops == "spmv" else None
         self.pcg = PCG(self.L, self.dinv, fixed=self.p_fixed if pf.any() else None, own=own, halo=halo,
                        order=dm.node_order() if halo is None else None)
         # velocity Dirichlet nodes (sparse list)
@@ -105,6 +111,12 @@ class FlowSolver:
         self.last_cg_iters = 0
         self.timeline = None  # list of (name, start, end) CUDA events when profiling
 
+    def _grad(self, p, out4, scale: float = 1.0):
+        if self.Bop is not None:
+            self.Bop.grad(p, scale, out4)
+        else:
+            call("ab_gradient", ctypes.byref(self.dm.struct), ptr(p), scale, ptr(out4), stream_handle())
+
     # -- state ----------------------------------------------------------------
     def set_state(self, u, p):
         u = torch.as_tensor(u, dtype=torch.float64, device=self.dm.device)
@@ -112,7 +124,7 @@ class FlowSolver:
         self.P.copy_(torch.as_tensor(p, dtype=torch.float64, device=self.dm.device))
         self._bc(self.U0)
         self.GP.zero_()
-        call("ab_gradient", ctypes.byref(self.dm.struct), ptr(self.P), 1.0, ptr(self.GP), stream_handle())
+        self._grad(self.P, self.GP)
         if self.halo is not None:
             self.halo.sum_(self.GP, 3, 4)
 
@@ -172,21 +184,30 @@ class FlowSolver:
                      ptr(self.GP), ptr(self.minv), ptr(self.U), s)
             self._bc(self.U)
         with self._mark("K4_divergence"):
-            call("ab_divergence", ctypes.byref(dm.struct), ptr(self.U), -rho / dt, ptr(self.B), s)
+            if self.Bop is not None:
+                self.Bop.div(self.U, -rho / dt, self.B)
+            else:
+                call("ab_divergence", ctypes.byref(dm.struct), ptr(self.U), -rho / dt, ptr(self.B), s)
         if self.halo is not None:
             with self._mark("X_halo_sum"):
                 self.halo.sum_(self.B, 1, 1)
         self.pcg.mark = self._mark
         x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
         self.last_cg_iters = it
-        with self._mark("K6_gradient"):
-            call("ab_gradient", ctypes.byref(dm.struct), ptr(x), 1.0, ptr(self.GD), s)
-        if self.halo is not None:
-            with self._mark("X_halo_sum"):
-                self.halo.sum_(self.GD, 3, 4)
-        with self._mark("K7_correct"):
-            call("ab_correct", self.n, k, ptr(self.U), ptr(self.U0), ptr(self.GD), ptr(self.minv), ptr(self.P),
-                 ptr(x), ptr(self.GP), s)
+        if self.Bop is not None and self.halo is None:
+            # K6 + K7 fused: u = u_3 - dt/rho M^-1 B dp; p += dp; Gp += B dp
+            with self._mark("K67_grad_correct"):
+                call("ab_gradop_correct", ctypes.byref(self.Bop.struct), ptr(x), k, ptr(self.U), ptr(self.U0),
+                     ptr(self.minv), ptr(self.P), ptr(self.GP), s)
+        else:
+            with self._mark("K6_gradient"):
+                self._grad(x, self.GD)
+            if self.halo is not None:
+                with self._mark("X_halo_sum"):
+                    self.halo.sum_(self.GD, 3, 4)
+            with self._mark("K7_correct"):
+                call("ab_correct", self.n, k, ptr(self.U), ptr(self.U0), ptr(self.GD), ptr(self.minv), ptr(self.P),
+                     ptr(x), ptr(self.GP), s)
         self._bc(self.U0)
 
     def step_host(self, u_host: torch.Tensor, p_host: torch.Tensor, dt: float, cg_iters: int = 50,
@@ -196,7 +217,7 @@ class FlowSolver:
         self.U0[:, :3].copy_(u_host, non_blocking=True)
         self.P.copy_(p_host, non_blocking=True)
         self.GP.zero_()
-        call("ab_gradient", ctypes.byref(self.dm.struct), ptr(self.P), 1.0, ptr(self.GP), stream_handle())
+        self._grad(self.P, self.GP)
         if self.halo is not None:
             self.halo.sum_(self.GP, 3, 4)
         self.step(dt, cg_iters, graph=graph)
@@ -241,7 +262,10 @@ class FlowSolver:
         """Kernels of this library launched by one step (no halo)."""
         ncat = len(self.dm.rules)
         bc = 1 if self.bc_idx is not None else 0
-        return 3 * (ncat + 1 + bc) + ncat + (2 + 2 * cg_iters) + ncat + 1 + bc
+        cg = 1 if self.pcg.resident else 2 + 2 * cg_iters
+        if self.Bop is not None:
+            return 3 * (ncat + 1 + bc) + 1 + cg + 1 + bc
+        return 3 * (ncat + 1 + bc) + ncat + cg + ncat + 1 + bc
 
 
 def time_step(solver: FlowSolver, dt: float, cg_iters: int = 50, cg_tol: float = 0.0):

@@ -72,6 +72,25 @@ def test_divergence_gradient(name, mode):
 
 
 @pytest.mark.parametrize("name", list(MESHES))
+def test_gradient_operator(name):
+    """K4/K6 as sparse products with B_ab = int N_a grad N_b (ab_gradop_*) vs the oracle."""
+    from paper_2005_05899_b200.device import DeviceMesh, nodes_as4
+    from paper_2005_05899_b200.solver import assemble_gradient_operator
+    m = MESHES[name]
+    u, p = _field(m, 1)
+    dm = DeviceMesh(m)
+    B = assemble_gradient_operator(dm)
+    u4 = nodes_as4(torch.from_numpy(u).cuda())
+    out = torch.full((m.n_nodes,), 0.5, dtype=torch.float64, device="cuda")
+    B.div(u4, 2.0, out)  # accumulates
+    assert rel_l2(out.cpu().numpy() - 0.5, 2.0 * fem.divergence(m, u)) <= TOL_RHS
+    g4 = torch.zeros((m.n_nodes, 4), dtype=torch.float64, device="cuda")
+    B.grad(torch.from_numpy(p).cuda(), 1.0, g4)
+    assert rel_l2(g4[:, :3].cpu().numpy(), fem.gradient(m, p)) <= TOL_RHS
+    assert float(g4[:, 3].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("name", list(MESHES))
 def test_laplacian_and_spmv(name):
     from paper_2005_05899_b200.solver import assemble_laplacian
     m = MESHES[name]
@@ -159,7 +178,8 @@ def _bcs(name, m):
 
 @pytest.mark.parametrize("name", ["tet", "hex_periodic", "mixed"])
 @pytest.mark.parametrize("graph", [False, True])
-def test_time_steps_match_oracle(name, graph):
+@pytest.mark.parametrize("ops", ["spmv", "element"])
+def test_time_steps_match_oracle(name, graph, ops):
     from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
     m = MESHES[name]
     bc = _bcs(name, m)
@@ -172,7 +192,7 @@ def test_time_steps_match_oracle(name, graph):
     dt, steps, iters = 2e-3, 3, 40
     ora = fem.FlowOracle(m, **params, **bc)
     st = ora.init_state(u, p)
-    fs = FlowSolver(m, FlowParams(**params), **bc, windows=True, reorder="sfc")
+    fs = FlowSolver(m, FlowParams(**params), **bc, windows=True, reorder="sfc", ops=ops)
     fs.set_state(u, p)
     for _ in range(steps):
         st = ora.step(st, dt, cg_iters=iters)
