@@ -976,11 +976,26 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       double acc[NC];
 #pragma unroll
       for (int q = 0; q < NC; ++q) acc[q] = 0.0;
-      for (int t = s0; t < s1; ++t) {
-        const int slot = mc.wslot[vc.skip_wslot + t];
-        const int a = slot % NN, el = slot / NN;
+      // batches of 8 list entries: all slot ids, then all slot values, then
+      // the adds in list order (two shared-memory round trips per batch
+      // instead of two per entry)
+      for (int t0 = s0; t0 < s1; t0 += 8) {
+        int sl[8];
 #pragma unroll
-        for (int q = 0; q < NC; ++q) acc[q] += slots[(q * NN + a) * BLOCK + el];
+        for (int u = 0; u < 8; ++u) sl[u] = t0 + u < s1 ? (int)mc.wslot[vc.skip_wslot + t0 + u] : -1;
+        double vq[8][NC];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int slot = sl[u] < 0 ? 0 : sl[u];
+          const int a = slot % NN, el = slot / NN;
+#pragma unroll
+          for (int q = 0; q < NC; ++q) vq[u][q] = slots[(q * NN + a) * BLOCK + el];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (sl[u] >= 0)
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc[q] += vq[u][q];
       }
 #pragma unroll
       for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);

@@ -33,7 +33,10 @@ fs.set_state(u, p)
 if not a.no_windows:
     print(fs.dm.window_stats())
 torch.cuda.synchronize()
+# ncu --profile-from-start off sees only the time steps (not the setup)
+torch.cuda.cudart().cudaProfilerStart()
 for _ in range(a.steps):
     fs.step(1e-3, a.cg_iters)
 torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
 print("done")
