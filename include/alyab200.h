@@ -220,7 +220,8 @@ typedef struct ab_cg_local {
  * 10 (per CTA: loop top, ghosts gathered, phase A reduced, barrier A,
  * phase B reduced, barrier B). */
 int ab_debug_timeline(int64_t* buf);
-/* 2: fits with x in shared memory, 1: fits with x in global memory, 0: no */
+/* 0: does not fit; otherwise 1 + (x kept in shared memory) + 2 * (the CTA's
+ * slice pointers and ghost ids copied to shared memory) */
 int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost);
 /* ab_cg_resident with the z gathers served from shared memory: each CTA
  * fetches its ghost z values once per iteration, the SpMV reads z through

@@ -433,22 +433,23 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
 // Shared memory: r, p, q [RB] | x [RB] (XS only; else x lives in x_out) |
 // z [RB] followed by the ghost values [max_ghost].
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void prefetch_slice16(const int64_t* __restrict__ sp, const uint16_t* lcol,
-                                                 const double* sval, int64_t s) {
-  const int64_t b = sp[s];
-  const uint32_t cnt = (uint32_t)(sp[s + 1] - b);
+__device__ __forceinline__ void prefetch_slice16(const int64_t* tsp, const uint16_t* lcol, const double* sval,
+                                                 int sl) {
+  const int64_t b = tsp[sl];
+  const uint32_t cnt = (uint32_t)(tsp[sl + 1] - b);
   if (cnt == 0) return;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lcol + b), "r"(cnt * 2u) : "memory");
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
 }
 
+// tsp: slice pointers of the CTA's slices (local index sl, shared or global)
 template <int CH>
-__device__ __forceinline__ double sell_row_dot_smem(const int64_t* __restrict__ sp, const uint16_t* __restrict__ lcol,
-                                                    const double* __restrict__ sval, const double* zs, int64_t i) {
-  const int64_t s = i >> 5;
-  const int lane = (int)(i & 31);
-  const int64_t base = sp[s] + lane;
-  const int width = (int)((sp[s + 1] - sp[s]) >> 5);
+__device__ __forceinline__ double sell_row_dot_smem(const int64_t* tsp, const uint16_t* __restrict__ lcol,
+                                                    const double* __restrict__ sval, const double* zs, int sl,
+                                                    int lane) {
+  const int64_t b0 = tsp[sl];
+  const int64_t base = b0 + lane;
+  const int width = (int)((tsp[sl + 1] - b0) >> 5);
   double acc = 0.0;
   for (int j0 = 0; j0 < width; j0 += CH) {
     unsigned c[CH];
@@ -500,7 +501,7 @@ __device__ __forceinline__ void stamp(int it, int k) {
 
 constexpr int kLocRowsPerThread = 8;  // rows_per_cta <= 8 * kResBlock
 
-template <bool XS>
+template <bool XS, bool TB>
 __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     int64_t n, int64_t rows_per_cta, int max_ghost, const int64_t* __restrict__ sp,
     const uint16_t* __restrict__ lcol, const double* __restrict__ sval, const int32_t* __restrict__ gptr,
@@ -521,6 +522,9 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   double* sq = spp + RB;
   double* sx = sq + RB;               // XS only
   double* sz = XS ? sx + RB : sx;     // [RB] own rows, then [max_ghost] ghosts
+  // TB: the CTA's slice pointers and ghost ids copied to shared memory
+  int64_t* tsp_s = reinterpret_cast<int64_t*>(sz + RB + max_ghost);
+  int32_t* tg_s = reinterpret_cast<int32_t*>(tsp_s + RB / 32 + 1);
   double* partA = part;
   double* partB = part + nb;
   double* partI = part + 3 * (size_t)nb;
@@ -530,7 +534,13 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   const int64_t s_first = r0 >> 5;
   const int g0 = gptr[blockIdx.x];
   const int ng = gptr[blockIdx.x + 1] - g0;
-  (void)max_ghost;
+  if (TB) {
+    for (int k = threadIdx.x; k <= nsl; k += kResBlock) tsp_s[k] = sp[s_first + k];
+    for (int k = threadIdx.x; k < ng; k += kResBlock) tg_s[k] = gidx[g0 + k];
+    __syncthreads();
+  }
+  const int64_t* tsp = TB ? tsp_s : sp + s_first;
+  const int32_t* tg = TB ? tg_s : gidx + g0;
 
   double a0 = 0.0, a1 = 0.0;
   for (int l = threadIdx.x; l < nloc; l += kResBlock) {
@@ -548,7 +558,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   }
   if (lane == 0)
     for (int d = 0; d < pf_depth; ++d)
-      if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
+      if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(tsp, lcol, sval, warp + d * (kResBlock / 32));
   {
     double v[2] = {a0, a1};
     block_sum<2, kResBlock>(v, sred);
@@ -566,17 +576,16 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
     stamp(it, 0);
     // ---- ghost z values of this CTA's columns -> shared memory
-    for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + __ldg(gidx + g0 + k));
+    for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + tg[k]);
     __syncthreads();
     stamp(it, 1);
     // ---- phase A: p = z + beta p; q = A z + beta q (z from shared memory)
     double pq = 0.0;
 #pragma unroll 1
     for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
-      const int64_t s = s_first + sl;
       if (lane == 0 && sl + pf_depth * (kResBlock / 32) < nsl)
-        prefetch_slice16(sp, lcol, sval, s + pf_depth * (kResBlock / 32));
-      const double az = sell_row_dot_smem<kLocChunk>(sp, lcol, sval, sz, s * 32 + lane);
+        prefetch_slice16(tsp, lcol, sval, sl + pf_depth * (kResBlock / 32));
+      const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
       const int l = sl * 32 + lane;
       if (l < nloc) {
         const double p = fma(beta, spp[l], sz[l]);
@@ -608,7 +617,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     if (lane == 0 && it + 1 < maxit)
       for (int d = 0; d < pf_depth; ++d)
         if (warp + d * (kResBlock / 32) < nsl)
-          prefetch_slice16(sp, lcol, sval, s_first + warp + d * (kResBlock / 32));
+          prefetch_slice16(tsp, lcol, sval, warp + d * (kResBlock / 32));
     double b0 = 0.0, b1 = 0.0;
 #pragma unroll
     for (int k = 0; k < kLocRowsPerThread; ++k) {
@@ -1171,6 +1180,8 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
 namespace {
 // dynamic shared memory of k_cg_resident_local: 2 = x in shared memory too,
 // 1 = x in global memory, 0 = does not fit
+// Shared-memory plan of k_cg_resident_local: 0 = does not fit, else
+// 1 + (x in shared memory) + 2 * (slice/ghost tables in shared memory).
 int local_mode(int64_t rb, int32_t max_ghost, size_t* bytes) {
   int dev = 0, optin = 0, coop = 0;
   cudaGetDevice(&dev);
@@ -1181,9 +1192,15 @@ int local_mode(int64_t rb, int32_t max_ghost, size_t* bytes) {
   if (!coop || max_ghost < 0 || rb + max_ghost > 65536) return 0;
   const size_t xs = (size_t)(5 * rb + max_ghost) * sizeof(double);
   const size_t xg = (size_t)(4 * rb + max_ghost) * sizeof(double);
-  if (xs <= cap) { if (bytes) *bytes = xs; return 2; }
-  if (xg <= cap) { if (bytes) *bytes = xg; return 1; }
-  return 0;
+  const size_t tb = (size_t)(rb / 32 + 1) * 8 + (size_t)max_ghost * 4;
+  int mode = 0;
+  size_t b = 0;
+  if (xs + tb <= cap) { mode = 4; b = xs + tb; }
+  else if (xs <= cap) { mode = 2; b = xs; }
+  else if (xg + tb <= cap) { mode = 3; b = xg + tb; }
+  else if (xg <= cap) { mode = 1; b = xg; }
+  if (bytes) *bytes = b;
+  return mode;
 }
 }  // namespace
 
@@ -1267,9 +1284,11 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
   } else {
     const int mode = local_mode(rb, mg, &smem);
     if (mode == 0) return fail("ab_cg_resident_local: system does not fit in shared memory");
+    const bool xs = mode == 2 || mode == 4, tb = mode >= 3;
     if (rb > (int64_t)kLocRowsPerThread * kResBlock) return fail("ab_cg_resident_local: too many rows per CTA");
 
-    const void* fn = mode == 2 ? (const void*)k_cg_resident_local<true> : (const void*)k_cg_resident_local<false>;
+    const void* fn = xs ? (tb ? (const void*)k_cg_resident_local<true, true> : (const void*)k_cg_resident_local<true, false>)
+                        : (tb ? (const void*)k_cg_resident_local<false, true> : (const void*)k_cg_resident_local<false, false>);
     if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
       return fail("ab_cg_resident_local: cannot reserve shared memory");
     void* args[] = {&n,           &rb,          &mg,  (void*)&sp, (void*)&lcol, (void*)&vals, (void*)&gp,
