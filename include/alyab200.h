@@ -258,6 +258,74 @@ int ab_gradop_grad(const ab_sell3* b, const double* p, double scale, double* out
 int ab_gradop_correct(const ab_sell3* b, const double* dp, double k, const double* uin, double* uout,
                       const double* minv, double* p, double* gp, void* stream);
 
+/* ---- K5 across ranks: resident CG fused with its interface exchange ----
+ * (DESIGN.md §5).  One cooperative kernel per rank solves the decomposed
+ * system without leaving the GPU: after the local SpMV every CTA writes the
+ * partial products of its interface rows straight into the neighbours'
+ * receive arrays (peer memory over NVLink, or the same device for virtual
+ * ranks), signals per-peer arrival counters, and adds what the neighbours
+ * sent; both dot products are reduced across CTAs (grid barrier) and then
+ * across ranks through {value, epoch} records written into every rank's
+ * reduction slots.  Counters and epochs are monotone over the whole run
+ * (evbase), so no buffer is ever reset while a peer may write to it.
+ * One launch may host several ranks ("virtual ranks": CTA groups of one
+ * cooperative grid on one GPU), which is how the protocol is tested on a
+ * single GPU; across GPUs every rank launches its own group and the peer
+ * pointers come from ab_ipc_* handles. */
+#define AB_DD_MAX_PEERS 8
+typedef struct ab_cg_dd_rank {
+  int64_t n_rows, rows_per_cta;
+  int32_t cta0, n_cta;                /* CTAs [cta0, cta0 + n_cta) of the launch */
+  int32_t max_ghost, rank;
+  int32_t n_ranks, pad0_;
+  const int64_t* slice_ptr;           /* SELL-32 of the rank's P L P^T (SFC row order) */
+  const uint16_t* cols;               /* CTA-local columns (ab_cg_local) */
+  const double* vals;
+  const int32_t* ghost_ptr;           /* [n_cta + 1] */
+  const int32_t* ghost;
+  const int32_t* perm;                /* row -> local node (b, x are in node order) */
+  const double* dinv;                 /* row order; D of the assembled global operator */
+  const uint8_t* fixed;               /* row order, nullable */
+  const double* own;                  /* row order: 1 on the rank owning the node, else 0 */
+  const double* b_in;
+  double* b_zero;                     /* nullable */
+  double* x_out;
+  double* zg;                         /* [n_rows] scratch */
+  double* red;                        /* RZN, RR, -, ITERS (-1: peer timeout) */
+  double* sc;                         /* BB */
+  double* part;                       /* >= 6 * n_cta */
+  unsigned* bar;                      /* zeroed before every solve */
+  /* interface: rows whose partial products are exchanged */
+  const uint32_t* ifmask;             /* bit per row */
+  const int32_t* send_ptr;            /* [n_rows + 1] per row into send_peer/send_off (interface rows only) */
+  const int32_t* send_peer;           /* index into peer_* */
+  const int32_t* send_off;            /* offset in that peer's recv array */
+  const int32_t* rrow_ptr;            /* [n_cta + 1] per CTA into rrow */
+  const int32_t* rrow;                /* interface rows, ascending */
+  const int32_t* recv_ptr;            /* [n_if + 1] per interface row into recv_off */
+  const int32_t* recv_off;            /* offsets into recv, ascending peer rank */
+  double* recv;                       /* written by the peers */
+  unsigned long long* cnt_in;         /* [n_ranks]: CTAs of rank q done sending (monotone) */
+  double* red_in;                     /* [3][n_ranks][2][2]: {value, epoch} records per set, rank, value */
+  unsigned long long* evbase;         /* [2]: halo events, reduction epochs completed before this solve */
+  int32_t n_peers, pad1_;
+  int32_t peer_rank[AB_DD_MAX_PEERS];
+  int32_t peer_ncta[AB_DD_MAX_PEERS];
+  double* peer_recv[AB_DD_MAX_PEERS];
+  unsigned long long* peer_cnt[AB_DD_MAX_PEERS];  /* &peer.cnt_in[rank] */
+  double* peer_red[AB_DD_MAX_PEERS];              /* &peer.red_in[0] */
+} ab_cg_dd_rank;
+/* Solve the ranks described by groups[0 .. n_groups) (device array) in one
+ * cooperative launch of sum(n_cta) CTAs; x0 = 0, exactly maxit iterations
+ * or until ||r||/||b|| <= tol (identical decision on every rank). */
+int ab_cg_dd(const ab_cg_dd_rank* groups_dev, int32_t n_groups, int32_t n_cta_total, int32_t maxit, double tol,
+             int64_t max_rows_per_cta, int32_t max_ghost, void* stream);
+/* CUDA IPC: export the allocation holding dev_ptr (64-byte handle + the
+ * pointer's offset in it) / map a peer's allocation (returns its base). */
+int ab_ipc_get_handle(const void* dev_ptr, unsigned char* handle64, int64_t* offset);
+int ab_ipc_open_handle(const unsigned char* handle64, void** dev_ptr);
+int ab_ipc_close(void* dev_ptr);
+
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */
 int ab_rk_stage(int64_t n, double a, double b, double k, const double* u0, const double* uprev,

@@ -79,6 +79,10 @@ _SIGS = {
     "ab_gradop_div": ([P(AbSell3), vp, f64, vp, vp], C.c_int),
     "ab_gradop_grad": ([P(AbSell3), vp, f64, vp, vp], C.c_int),
     "ab_gradop_correct": ([P(AbSell3), vp, f64, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_dd": ([vp, i32, i32, i32, f64, i64, i32, vp], C.c_int),
+    "ab_ipc_get_handle": ([vp, vp, vp], C.c_int),
+    "ab_ipc_open_handle": ([vp, vp], C.c_int),
+    "ab_ipc_close": ([vp], C.c_int),
     "ab_rk_stage": ([i64, f64, f64, f64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_correct": ([i64, f64, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_apply_velocity_bc": ([i64, vp, vp, vp, vp, vp], C.c_int),

@@ -1,0 +1,83 @@
+// Device helpers shared by the resident CG kernels (ab_solver.cu, ab_cg_dd.cu):
+// one 1024-thread CTA per SM, grid barriers on a monotone arrival counter,
+// ordered all-sums of per-CTA partials, SELL-32 rows with 16-bit CTA-local
+// columns read against z in shared memory.
+#pragma once
+#include "ab_common.cuh"
+
+namespace ab {
+
+constexpr int kResBlock = 1024;
+constexpr int kLocChunk = 8;
+
+// Grid barrier on a monotone arrival counter (zeroed before launch): the
+// k-th barrier completes when the counter reaches k * gridDim.x.  One
+// release-reduction per CTA and one acquire-polling thread per CTA; the
+// CTA barriers on both sides extend the ordering to all threads.  Data
+// exchanged across it is read with L2-only loads (ld.cg), so no stale L1
+// lines are possible.
+__device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
+    unsigned v;
+    do {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
+    } while (v < target);
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void prefetch_slice16(const int64_t* tsp, const uint16_t* lcol, const double* sval,
+                                                 int sl) {
+  const int64_t b = tsp[sl];
+  const uint32_t cnt = (uint32_t)(tsp[sl + 1] - b);
+  if (cnt == 0) return;
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lcol + b), "r"(cnt * 2u) : "memory");
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
+}
+
+// tsp: slice pointers of the CTA's slices (local index sl, shared or global)
+template <int CH>
+__device__ __forceinline__ double sell_row_dot_smem(const int64_t* tsp, const uint16_t* __restrict__ lcol,
+                                                    const double* __restrict__ sval, const double* zs, int sl,
+                                                    int lane) {
+  const int64_t b0 = tsp[sl];
+  const int64_t base = b0 + lane;
+  const int width = (int)((tsp[sl + 1] - b0) >> 5);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < width; j0 += CH) {
+    unsigned c[CH];
+    double a[CH];
+#pragma unroll
+    for (int u = 0; u < CH; ++u) {
+      const bool ok = j0 + u < width;
+      c[u] = ok ? (unsigned)__ldcs(lcol + base + (int64_t)(j0 + u) * 32) : 0u;
+      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < CH; ++u) acc = fma(a[u], zs[c[u]], acc);
+  }
+  return acc;
+}
+
+// Ordered sum of nb (<= blockDim) per-CTA partials, all loads in flight at
+// once (one L2 round trip), fixed reduction tree: identical in every CTA.
+template <int NV>
+__device__ __forceinline__ void all_sum_par(const double* part, int nb, double* sred, double* bcast,
+                                            double (&out)[NV]) {
+  double v[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = (int)threadIdx.x < nb ? __ldcg(part + (size_t)k * nb + threadIdx.x) : 0.0;
+  block_sum<NV, kResBlock>(v, sred);
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) bcast[k] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
+}
+
+
+}  // namespace ab

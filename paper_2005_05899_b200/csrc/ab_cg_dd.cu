@@ -1,0 +1,374 @@
+// Resident Jacobi-PCG of a decomposed domain, fused with its interface
+// exchange (include/alyab200.h "K5 across ranks").
+//
+// The element-disjoint decomposition duplicates interface nodes
+// (PAPER.md:325-330): each rank's Laplacian rows at interface nodes hold only
+// that rank's elements, so (A z)_i = sum over the sharing ranks of their
+// partial products, and the dots weight every node once (own = 1 on its
+// lowest rank).  Per iteration, without leaving the kernel:
+//   ghost gather   z of the CTA's remote columns -> shared memory (own rank)
+//   SpMV           t = A_r z per row; interface rows write t straight into
+//                  every sharing rank's receive array (peer memory);
+//                  p = z + beta p, q = t + beta q (interface rows: partial)
+//   signal/wait    per-CTA release-add on each peer's arrival counter, then
+//                  acquire-poll of this rank's counters (monotone over the run)
+//   interface add  q_i += received partials (ascending peer rank), p.q
+//   reduce A       CTAs: grid barrier + ordered all-sum; ranks: {value, epoch}
+//                  records into every rank's slots, summed in rank order
+//   update         x += alpha p, r -= alpha q, z = D^-1 r, r.z, r.r
+//   reduce B       as A; also publishes z to the rank's CTAs
+// Every rank sums the same numbers in the same order, so all ranks take the
+// same alpha, beta and stopping decision.  Peer waits time out (10 s) by
+// setting red[ITERS] = -1 instead of hanging the device.
+#include <cstring>
+
+#include "ab_cg_common.cuh"
+
+namespace ab {
+
+static_assert(sizeof(ab_cg_dd_rank) == 536, "ab_cg_dd_rank layout (mirrored by ddcg.AbCgDdRank)");
+constexpr int kDdRowsPerThread = 8;
+constexpr long long kDdTimeoutNs = 10000000000ll;
+
+__device__ __forceinline__ long long gtime() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acq_sys_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_rel_sys_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_rec_sys(double* p, double v, double e) {
+  asm volatile("st.relaxed.sys.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(e) : "memory");
+}
+__device__ __forceinline__ void ld_rec_sys(const double* p, double& v, double& e) {
+  asm volatile("ld.relaxed.sys.global.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(e) : "l"(p) : "memory");
+}
+
+struct DdCtx {
+  const ab_cg_dd_rank* g;
+  int lcta;          // CTA index within the rank
+  int nb;            // CTAs of the rank
+  int* failed;       // shared flag
+};
+
+// Reduce NV values across the rank's CTAs (grid barrier on g.bar) and then
+// across ranks (records in slot set `set`, epoch `ep`).  v: this CTA's
+// block-reduced values (valid in thread 0).  out: global totals, every thread.
+template <int NV>
+__device__ __forceinline__ void dd_allreduce(const DdCtx& c, double (&v)[NV], int set, double ep, unsigned& nbar,
+                                             double* sred, double* bcast, double (&out)[NV], long long t0) {
+  const ab_cg_dd_rank& g = *c.g;
+  double* part = g.part + (size_t)set * 2 * c.nb;
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) part[(size_t)k * c.nb + c.lcta] = v[k];
+  grid_barrier(g.bar, ++nbar * (unsigned)c.nb);
+  double loc[NV];
+  all_sum_par<NV>(part, c.nb, sred, bcast, loc);
+  const int P = g.n_ranks;
+  if (P == 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = loc[k];
+    return;
+  }
+  // rank totals -> every rank's slot [set][rank][k]
+  if (c.lcta == 0 && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const size_t o = (((size_t)set * P + g.rank) * 2 + k) * 2;
+      st_rec_sys(g.red_in + o, loc[k], ep);
+      for (int q = 0; q < g.n_peers; ++q) st_rec_sys(g.peer_red[q] + o, loc[k], ep);
+    }
+  }
+  // thread q polls rank q's records (local memory), ordered sum over ranks
+  double w[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) w[k] = 0.0;
+  if ((int)threadIdx.x < P) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      const double* rec = g.red_in + (((size_t)set * P + threadIdx.x) * 2 + k) * 2;
+      double val, e;
+      for (;;) {
+        ld_rec_sys(rec, val, e);
+        if (e == ep) break;
+        if (gtime() - t0 > kDdTimeoutNs) { *c.failed = 1; val = 0.0; break; }
+      }
+      w[k] = val;
+    }
+  }
+  // ranks in order: gather to warp 0 lanes, sequential sum (P <= 32)
+  if (threadIdx.x < 32) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double acc = 0.0;
+      for (int q = 0; q < P; ++q) acc += __shfl_sync(0xffffffffu, w[k], q);
+      if (threadIdx.x == 0) bcast[k] = acc;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __restrict__ groups, int n_groups,
+                                                        int maxit, double tol) {
+  extern __shared__ double smem[];
+  __shared__ double sred[2 * (kResBlock / 32)];
+  __shared__ double bcast[4];
+  __shared__ int s_failed;
+  // ---- which rank (group) this CTA works for
+  int gi = 0;
+  while (gi + 1 < n_groups && (int)blockIdx.x >= groups[gi + 1].cta0) ++gi;
+  const ab_cg_dd_rank& g = groups[gi];
+  const int lcta = (int)blockIdx.x - g.cta0;
+  if (threadIdx.x == 0) s_failed = 0;
+  DdCtx c{&g, lcta, g.n_cta, &s_failed};
+  const long long t0 = gtime();
+  const int64_t n = g.n_rows;
+  const int64_t RB = g.rows_per_cta;
+  const int64_t r0 = (int64_t)lcta * RB;
+  const int64_t r1 = r0 + RB < n ? r0 + RB : n;
+  const int nloc = r1 > r0 ? (int)(r1 - r0) : 0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (nloc + 31) >> 5;
+  const int64_t s_first = r0 >> 5;
+  const int g0 = g.ghost_ptr[lcta];
+  const int ng = g.ghost_ptr[lcta + 1] - g0;
+  double* sr = smem;
+  double* spp = sr + RB;
+  double* sq = spp + RB;
+  double* sx = sq + RB;
+  double* sz = sx + RB;  // [RB] own rows, then ghosts
+  uint32_t* smask = reinterpret_cast<uint32_t*>(sz + RB + g.max_ghost);  // [RB / 32] interface bits
+  const int64_t* tsp = g.slice_ptr + s_first;
+  const int32_t* tg = g.ghost + g0;
+  const uint16_t* lcol = g.cols;
+  const double* sval = g.vals;
+  const int P = g.n_ranks;
+  const unsigned long long hbase = g.evbase[0];
+  const double ebase = (double)g.evbase[1];
+  double ep = ebase;
+  unsigned nbar = 0;
+  for (int k = threadIdx.x; k < nsl; k += kResBlock) smask[k] = g.ifmask[(r0 >> 5) + k];
+  const int ri0 = g.rrow_ptr[lcta], ri1 = g.rrow_ptr[lcta + 1];
+
+  // ---- init: r = b (fixed rows 0), z = D^-1 r, x = p = q = 0
+  double a0 = 0.0, a1 = 0.0;
+  for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+    const int64_t i = r0 + l;
+    const int64_t ni = g.perm[i];
+    double ri = g.b_in[ni];
+    if (g.fixed && g.fixed[i]) ri = 0.0;
+    if (g.b_zero) g.b_zero[ni] = 0.0;
+    const double zi = g.dinv[i] * ri;
+    sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0; sx[l] = 0.0;
+    g.zg[i] = zi;
+    const double w = g.own[i];
+    a0 += w * ri * zi;
+    a1 += w * ri * ri;
+  }
+  double t2[2];
+  {
+    double v[2] = {a0, a1};
+    block_sum<2, kResBlock>(v, sred);
+    ep += 1.0;
+    dd_allreduce<2>(c, v, 0, ep, nbar, sred, bcast, t2, t0);
+  }
+  double rz = t2[0], rr = t2[1];
+  const double bb = rr;
+  double rz_old = 0.0;
+  int it = 0;
+  for (; it < maxit; ++it) {
+    if (s_failed) break;
+    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
+    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(g.zg + tg[k]);
+    __syncthreads();
+    // ---- SpMV; interface rows ship their partial product to the sharers
+    double pq = 0.0;
+#pragma unroll 1
+    for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
+      const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        const double p = fma(beta, spp[l], sz[l]);
+        const double q = fma(beta, sq[l], az);
+        spp[l] = p;
+        sq[l] = q;
+        if ((smask[sl] >> lane) & 1u) {
+          const int64_t i = r0 + l;
+          for (int k = g.send_ptr[i]; k < g.send_ptr[i + 1]; ++k) g.peer_recv[g.send_peer[k]][g.send_off[k]] = az;
+        } else {
+          pq += g.own[r0 + l] * p * q;
+        }
+      }
+    }
+    if (P > 1) {
+      // this CTA's sends are complete -> one arrival on every peer's counter
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence_system();
+        for (int q = 0; q < g.n_peers; ++q) red_rel_sys_u64(g.peer_cnt[q], 1ull);
+      }
+      // wait for every CTA of every peer (counters are monotone over the run)
+      if ((int)threadIdx.x < g.n_peers) {
+        const int q = g.peer_rank[threadIdx.x];
+        const unsigned long long want = (hbase + (unsigned long long)it + 1ull) * (unsigned long long)g.peer_ncta[threadIdx.x];
+        while (ld_acq_sys_u64(g.cnt_in + q) < want) {
+          if (gtime() - t0 > kDdTimeoutNs) { s_failed = 1; break; }
+        }
+      }
+      __syncthreads();
+      // interface rows: add the neighbours' partials in ascending rank order
+      for (int k = ri0 + (int)threadIdx.x; k < ri1; k += kResBlock) {
+        const int64_t i = g.rrow[k];
+        const int l = (int)(i - r0);
+        double q = sq[l];
+        for (int e = g.recv_ptr[k]; e < g.recv_ptr[k + 1]; ++e) q += __ldcg(g.recv + g.recv_off[e]);
+        sq[l] = q;
+        pq += g.own[i] * spp[l] * q;
+      }
+    }
+    double t1[1];
+    {
+      double v[1] = {pq};
+      block_sum<1, kResBlock>(v, sred);
+      ep += 1.0;
+      dd_allreduce<1>(c, v, 1, ep, nbar, sred, bcast, t1, t0);
+    }
+    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+    // ---- update
+    double dv[kDdRowsPerThread];
+#pragma unroll
+    for (int k = 0; k < kDdRowsPerThread; ++k) {
+      const int l = threadIdx.x + k * kResBlock;
+      dv[k] = l < nloc ? __ldg(g.dinv + r0 + l) : 0.0;
+    }
+    double b0 = 0.0, b1 = 0.0;
+#pragma unroll
+    for (int k = 0; k < kDdRowsPerThread; ++k) {
+      const int l = threadIdx.x + k * kResBlock;
+      if (l < nloc) {
+        sx[l] = fma(alpha, spp[l], sx[l]);
+        const double ri = fma(-alpha, sq[l], sr[l]);
+        const double zi = dv[k] * ri;
+        sr[l] = ri;
+        sz[l] = zi;
+        g.zg[r0 + l] = zi;
+        const double w = g.own[r0 + l];
+        b0 += w * ri * zi;
+        b1 += w * ri * ri;
+      }
+    }
+    {
+      double v[2] = {b0, b1};
+      block_sum<2, kResBlock>(v, sred);
+      ep += 1.0;
+      dd_allreduce<2>(c, v, 2, ep, nbar, sred, bcast, t2, t0);
+    }
+    rz_old = rz;
+    rz = t2[0];
+    rr = t2[1];
+  }
+  for (int l = threadIdx.x; l < nloc; l += kResBlock) g.x_out[g.perm[r0 + l]] = sx[l];
+  // every CTA of the rank has read evbase before its first reduction
+  if (lcta == 0 && threadIdx.x == 0) {
+    g.red[AB_RED_RZN] = rz;
+    g.red[AB_RED_RR] = rr;
+    g.red[AB_RED_ITERS] = s_failed ? -1.0 : (double)it;
+    g.sc[AB_SC_BB] = bb;
+    g.evbase[0] = hbase + (unsigned long long)it;
+    g.evbase[1] = (unsigned long long)ep;
+  }
+}
+
+}  // namespace ab
+
+using namespace ab;
+
+extern "C" {
+
+int ab_cg_dd(const ab_cg_dd_rank* groups_dev, int32_t n_groups, int32_t n_cta_total, int32_t maxit, double tol,
+             int64_t max_rows_per_cta, int32_t max_ghost, void* stream) {
+  if (!groups_dev || n_groups <= 0 || n_cta_total <= 0) return fail("ab_cg_dd: empty launch");
+  if (max_rows_per_cta > (int64_t)kDdRowsPerThread * kResBlock || max_rows_per_cta % 32)
+    return fail("ab_cg_dd: rows per CTA must be a multiple of 32 and <= 8192");
+  int dev = 0, optin = 0, coop = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (!coop) return fail("ab_cg_dd: cooperative launch unsupported");
+  if (n_cta_total > sms) return fail("ab_cg_dd: more CTAs than SMs");
+  const size_t smem = (size_t)(5 * max_rows_per_cta + max_ghost) * 8 + (size_t)(max_rows_per_cta / 32) * 4;
+  if (smem + 1024 > (size_t)optin) return fail("ab_cg_dd: rows + ghosts do not fit in shared memory");
+  if (cudaFuncSetAttribute((const void*)k_cg_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+      cudaSuccess)
+    return fail("ab_cg_dd: cannot reserve shared memory");
+  int ng = n_groups, mi = maxit;
+  void* args[] = {(void*)&groups_dev, &ng, &mi, &tol};
+  cudaError_t e =
+      cudaLaunchCooperativeKernel((const void*)k_cg_dd, dim3(n_cta_total), dim3(kResBlock), args, smem, S(stream));
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_cg_dd: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  return check_launch("ab_cg_dd");
+}
+
+int ab_ipc_get_handle(const void* dev_ptr, unsigned char* handle64, int64_t* offset) {
+  if (!dev_ptr || !handle64 || !offset) return fail("ab_ipc_get_handle: null argument");
+  // the handle names the whole allocation: report dev_ptr's offset in it
+  // (pool allocators hand out pieces of larger blocks)
+  typedef int (*GetRange)(unsigned long long*, size_t*, unsigned long long);
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return fail("ab_ipc_get_handle: cuMemGetAddressRange unavailable");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (reinterpret_cast<GetRange>(fn)(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0)
+    return fail("ab_ipc_get_handle: cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_ipc_get_handle: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  memcpy(handle64, &h, 64);
+  *offset = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return AB_OK;
+}
+
+int ab_ipc_open_handle(const unsigned char* handle64, void** dev_ptr) {
+  if (!handle64 || !dev_ptr) return fail("ab_ipc_open_handle: null argument");
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle64, 64);
+  cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_ipc_open_handle: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  return AB_OK;
+}
+
+int ab_ipc_close(void* dev_ptr) {
+  if (!dev_ptr) return AB_OK;
+  cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+  if (e != cudaSuccess) {
+    set_error(std::string("ab_ipc_close: ") + cudaGetErrorString(e));
+    return AB_ECUDA;
+  }
+  return AB_OK;
+}
+
+}  // extern "C"

@@ -7,7 +7,7 @@
 //   update: x += alpha p, r -= alpha q, z = D^-1 r, r.z and r.r partials.
 // Scalars (alpha, beta) are formed on the device from the reduction slots,
 // so the loop never synchronises with the host.
-#include "ab_common.cuh"
+#include "ab_cg_common.cuh"
 
 namespace ab {
 
@@ -258,7 +258,6 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_update(int64_t n, const double*
 // SM); otherwise the kernels above run.  Launched cooperatively so that all
 // CTAs are co-resident for the grid barriers.
 // ---------------------------------------------------------------------------
-constexpr int kResBlock = 1024;
 
 // Bulk prefetch of one SELL slice (column indices + values) into L2.
 __device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, const int32_t* scol,
@@ -268,24 +267,6 @@ __device__ __forceinline__ void prefetch_slice(const int64_t* __restrict__ sp, c
   if (cnt == 0) return;
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(scol + b), "r"(cnt * 4u) : "memory");
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
-}
-
-// Grid barrier on a monotone arrival counter (zeroed before launch): the
-// k-th barrier completes when the counter reaches k * gridDim.x.  One
-// release-reduction per CTA and one acquire-polling thread per CTA; the
-// CTA barriers on both sides extend the ordering to all threads.  Data
-// exchanged across it is read with L2-only loads (ld.cg), so no stale L1
-// lines are possible.
-__device__ __forceinline__ void grid_barrier(unsigned* cnt, unsigned target) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(cnt) : "memory");
-    unsigned v;
-    do {
-      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(cnt) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
 }
 
 // Ordered sum of nb per-CTA partials (layout part[k*nb+b]); identical in
@@ -433,58 +414,6 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
 // Shared memory: r, p, q [RB] | x [RB] (XS only; else x lives in x_out) |
 // z [RB] followed by the ghost values [max_ghost].
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void prefetch_slice16(const int64_t* tsp, const uint16_t* lcol, const double* sval,
-                                                 int sl) {
-  const int64_t b = tsp[sl];
-  const uint32_t cnt = (uint32_t)(tsp[sl + 1] - b);
-  if (cnt == 0) return;
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lcol + b), "r"(cnt * 2u) : "memory");
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(sval + b), "r"(cnt * 8u) : "memory");
-}
-
-// tsp: slice pointers of the CTA's slices (local index sl, shared or global)
-template <int CH>
-__device__ __forceinline__ double sell_row_dot_smem(const int64_t* tsp, const uint16_t* __restrict__ lcol,
-                                                    const double* __restrict__ sval, const double* zs, int sl,
-                                                    int lane) {
-  const int64_t b0 = tsp[sl];
-  const int64_t base = b0 + lane;
-  const int width = (int)((tsp[sl + 1] - b0) >> 5);
-  double acc = 0.0;
-  for (int j0 = 0; j0 < width; j0 += CH) {
-    unsigned c[CH];
-    double a[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const bool ok = j0 + u < width;
-      c[u] = ok ? (unsigned)__ldcs(lcol + base + (int64_t)(j0 + u) * 32) : 0u;
-      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
-    }
-#pragma unroll
-    for (int u = 0; u < CH; ++u) acc = fma(a[u], zs[c[u]], acc);
-  }
-  return acc;
-}
-
-// Ordered sum of nb (<= blockDim) per-CTA partials, all loads in flight at
-// once (one L2 round trip), fixed reduction tree: identical in every CTA.
-template <int NV>
-__device__ __forceinline__ void all_sum_par(const double* part, int nb, double* sred, double* bcast,
-                                            double (&out)[NV]) {
-  double v[NV];
-#pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = (int)threadIdx.x < nb ? __ldcg(part + (size_t)k * nb + threadIdx.x) : 0.0;
-  block_sum<NV, kResBlock>(v, sred);
-  if (threadIdx.x == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) bcast[k] = v[k];
-  }
-  __syncthreads();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) out[k] = bcast[k];
-}
-
-constexpr int kLocChunk = 8;
 
 // Optional phase timeline of the resident solvers (ab_debug_timeline):
 // globaltimer stamps of thread 0 of every CTA at the phase boundaries of
