@@ -57,28 +57,22 @@ struct DdCtx {
   int* failed;       // shared flag
 };
 
-// Reduce NV values across the rank's CTAs (grid barrier on g.bar) and then
-// across ranks (records in slot set `set`, epoch `ep`).  v: this CTA's
-// block-reduced values (valid in thread 0).  out: global totals, every thread.
+// Cross-CTA part of a reduction: NV block-reduced values (valid in thread
+// 0) -> grid barrier on g.bar -> ordered rank total `loc` in every thread;
+// with several ranks the total is published as {value, epoch} records into
+// every rank's slot set `set`.
 template <int NV>
-__device__ __forceinline__ void dd_allreduce(const DdCtx& c, double (&v)[NV], int set, double ep, unsigned& nbar,
-                                             double* sred, double* bcast, double (&out)[NV], long long t0) {
+__device__ __forceinline__ void dd_publish(const DdCtx& c, double (&v)[NV], int set, double ep, unsigned& nbar,
+                                           double* sred, double* bcast, double (&loc)[NV]) {
   const ab_cg_dd_rank& g = *c.g;
   double* part = g.part + (size_t)set * 2 * c.nb;
   if (threadIdx.x == 0)
 #pragma unroll
     for (int k = 0; k < NV; ++k) part[(size_t)k * c.nb + c.lcta] = v[k];
   grid_barrier(g.bar, ++nbar * (unsigned)c.nb);
-  double loc[NV];
   all_sum_par<NV>(part, c.nb, sred, bcast, loc);
   const int P = g.n_ranks;
-  if (P == 1) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) out[k] = loc[k];
-    return;
-  }
-  // rank totals -> every rank's slot [set][rank][k]
-  if (c.lcta == 0 && threadIdx.x == 0) {
+  if (P > 1 && c.lcta == 0 && threadIdx.x == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const size_t o = (((size_t)set * P + g.rank) * 2 + k) * 2;
@@ -86,7 +80,20 @@ __device__ __forceinline__ void dd_allreduce(const DdCtx& c, double (&v)[NV], in
       for (int q = 0; q < g.n_peers; ++q) st_rec_sys(g.peer_red[q] + o, loc[k], ep);
     }
   }
-  // thread q polls rank q's records (local memory), ordered sum over ranks
+}
+
+// Cross-rank part: thread q polls rank q's record (local memory), then the
+// totals are summed in rank order (identical on every rank).
+template <int NV>
+__device__ __forceinline__ void dd_collect(const DdCtx& c, int set, double ep, double* bcast, const double (&loc)[NV],
+                                           double (&out)[NV], long long t0) {
+  const ab_cg_dd_rank& g = *c.g;
+  const int P = g.n_ranks;
+  if (P == 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) out[k] = loc[k];
+    return;
+  }
   double w[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) w[k] = 0.0;
@@ -103,7 +110,7 @@ __device__ __forceinline__ void dd_allreduce(const DdCtx& c, double (&v)[NV], in
       w[k] = val;
     }
   }
-  // ranks in order: gather to warp 0 lanes, sequential sum (P <= 32)
+  __syncthreads();  // bcast of the previous use has been read
   if (threadIdx.x < 32) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -124,10 +131,18 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
   __shared__ double sred[2 * (kResBlock / 32)];
   __shared__ double bcast[4];
   __shared__ int s_failed;
+  __shared__ ab_cg_dd_rank s_g;  // the rank's descriptor, read with LDS from here on
+  __shared__ uint32_t s_taddr;
   // ---- which rank (group) this CTA works for
   int gi = 0;
   while (gi + 1 < n_groups && (int)blockIdx.x >= groups[gi + 1].cta0) ++gi;
-  const ab_cg_dd_rank& g = groups[gi];
+  {
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(groups + gi);
+    uint32_t* dst = reinterpret_cast<uint32_t*>(&s_g);
+    for (int k = threadIdx.x; k < (int)(sizeof(ab_cg_dd_rank) / 4); k += kResBlock) dst[k] = src[k];
+    __syncthreads();
+  }
+  const ab_cg_dd_rank& g = s_g;
   const int lcta = (int)blockIdx.x - g.cta0;
   if (threadIdx.x == 0) s_failed = 0;
   DdCtx c{&g, lcta, g.n_cta, &s_failed};
@@ -145,11 +160,19 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
   double* sr = smem;
   double* spp = sr + RB;
   double* sq = spp + RB;
-  double* sx = sq + RB;
-  double* sz = sx + RB;  // [RB] own rows, then ghosts
-  uint32_t* smask = reinterpret_cast<uint32_t*>(sz + RB + g.max_ghost);  // [RB / 32] interface bits
-  const int64_t* tsp = g.slice_ptr + s_first;
-  const int32_t* tg = g.ghost + g0;
+  double* sz = sq + RB;  // [RB] own rows, then ghosts
+  // x lives in tensor memory: thread (warp w, lane) keeps x of its phase-B
+  // rows l = threadIdx.x + k * kResBlock in columns 2k, 2k + 1 of its lane
+  // (warp w's 32-lane quarter, 64-column slice of its warp group)
+  const uint32_t taddr = tmem_alloc_all(&s_taddr);
+  const uint32_t tx = taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+  // shared tables: interface bits, ownership bits, slice pointers, ghost ids
+  uint32_t* smask = reinterpret_cast<uint32_t*>(sz + RB + g.max_ghost);  // [RB / 32]
+  uint32_t* sown = smask + RB / 32;                                       // [RB / 32]
+  int64_t* tsp_s = reinterpret_cast<int64_t*>(sown + RB / 32);                  // [RB / 32 + 1], 8-aligned
+  int32_t* tg_s = reinterpret_cast<int32_t*>(tsp_s + RB / 32 + 1);        // [max_ghost]
+  const int64_t* tsp = tsp_s;
+  const int32_t* tg = tg_s;
   const uint16_t* lcol = g.cols;
   const double* sval = g.vals;
   const int P = g.n_ranks;
@@ -158,6 +181,17 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
   double ep = ebase;
   unsigned nbar = 0;
   for (int k = threadIdx.x; k < nsl; k += kResBlock) smask[k] = g.ifmask[(r0 >> 5) + k];
+  for (int k = threadIdx.x; k <= nsl; k += kResBlock) tsp_s[k] = g.slice_ptr[s_first + k];
+  for (int k = threadIdx.x; k < ng; k += kResBlock) tg_s[k] = g.ghost[g0 + k];
+  for (int k = threadIdx.x; k < nsl; k += kResBlock) {  // own[] is 0/1: one bit per row
+    uint32_t w = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int64_t i = r0 + 32 * k + b;
+      if (i < n && g.own[i] != 0.0) w |= 1u << b;
+    }
+    sown[k] = w;
+  }
+  __syncthreads();
   const int ri0 = g.rrow_ptr[lcta], ri1 = g.rrow_ptr[lcta + 1];
 
   // ---- init: r = b (fixed rows 0), z = D^-1 r, x = p = q = 0
@@ -169,123 +203,181 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
     if (g.fixed && g.fixed[i]) ri = 0.0;
     if (g.b_zero) g.b_zero[ni] = 0.0;
     const double zi = g.dinv[i] * ri;
-    sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0; sx[l] = 0.0;
+    sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
     g.zg[i] = zi;
-    const double w = g.own[i];
-    a0 += w * ri * zi;
-    a1 += w * ri * ri;
+    if ((sown[l >> 5] >> (l & 31)) & 1u) {
+      a0 += ri * zi;
+      a1 += ri * ri;
+    }
   }
-  double t2[2];
+#pragma unroll
+  for (int k = 0; k < kDdRowsPerThread; ++k) tm_st(tx + 2 * k, 0.0);
+  tm_wait_st();
+  double t2[2], l2[2];
   {
     double v[2] = {a0, a1};
     block_sum<2, kResBlock>(v, sred);
     ep += 1.0;
-    dd_allreduce<2>(c, v, 0, ep, nbar, sred, bcast, t2, t0);
+    dd_publish<2>(c, v, 0, ep, nbar, sred, bcast, l2);
+    dd_collect<2>(c, 0, ep, bcast, l2, t2, t0);
   }
   double rz = t2[0], rr = t2[1];
   const double bb = rr;
   double rz_old = 0.0;
   int it = 0;
+  // The r.z / r.r records of iteration i are collected only after the SpMV
+  // of iteration i + 1 has been computed and shipped (that SpMV needs z,
+  // not beta): the cross-rank wait of reduction B overlaps the matrix
+  // stream.  A(z) per row waits in TMEM (columns 16 + 2k) for beta.
+  bool pending = false;
+  double epB = 0.0;
+  unsigned long long hev = 0;  // halo events of this solve
   for (; it < maxit; ++it) {
     if (s_failed) break;
-    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
-    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    if (!pending && tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
     for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(g.zg + tg[k]);
     __syncthreads();
-    // ---- SpMV; interface rows ship their partial product to the sharers
-    double pq = 0.0;
+    // ---- SpMV: A z per row -> TMEM; interface rows ship it to the sharers
 #pragma unroll 1
-    for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
+    for (int k = 0; k * (kResBlock / 32) + warp < nsl; ++k) {
+      const int sl = warp + k * (kResBlock / 32);
       const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      tm_st(tx + 16 + 2 * k, az);
       const int l = sl * 32 + lane;
-      if (l < nloc) {
-        const double p = fma(beta, spp[l], sz[l]);
-        const double q = fma(beta, sq[l], az);
-        spp[l] = p;
-        sq[l] = q;
-        if ((smask[sl] >> lane) & 1u) {
-          const int64_t i = r0 + l;
-          for (int k = g.send_ptr[i]; k < g.send_ptr[i + 1]; ++k) g.peer_recv[g.send_peer[k]][g.send_off[k]] = az;
-        } else {
-          pq += g.own[r0 + l] * p * q;
-        }
+      if (l < nloc && ((smask[sl] >> lane) & 1u)) {
+        const int64_t i = r0 + l;
+        for (int e = g.send_ptr[i]; e < g.send_ptr[i + 1]; ++e) g.peer_recv[g.send_peer[e]][g.send_off[e]] = az;
       }
     }
-    if (P > 1) {
-      // this CTA's sends are complete -> one arrival on every peer's counter
+    ++hev;
+    if (P > 1) {  // this CTA's sends are complete -> one arrival on every peer's counter
       __syncthreads();
       if (threadIdx.x == 0) {
-        __threadfence_system();
+        if (g.pad0_) __threadfence(); else __threadfence_system();  // pad0_ = 1: every peer on this device
         for (int q = 0; q < g.n_peers; ++q) red_rel_sys_u64(g.peer_cnt[q], 1ull);
       }
-      // wait for every CTA of every peer (counters are monotone over the run)
+    }
+    if (pending) {  // reduction B of the previous iteration
+      dd_collect<2>(c, 2, epB, bcast, l2, t2, t0);
+      rz_old = rz;
+      rz = t2[0];
+      rr = t2[1];
+      pending = false;
+      if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
+    }
+    const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
+    if (P > 1) {  // every CTA of every peer has shipped (monotone counters)
       if ((int)threadIdx.x < g.n_peers) {
         const int q = g.peer_rank[threadIdx.x];
-        const unsigned long long want = (hbase + (unsigned long long)it + 1ull) * (unsigned long long)g.peer_ncta[threadIdx.x];
+        const unsigned long long want = (hbase + hev) * (unsigned long long)g.peer_ncta[threadIdx.x];
         while (ld_acq_sys_u64(g.cnt_in + q) < want) {
           if (gtime() - t0 > kDdTimeoutNs) { s_failed = 1; break; }
         }
       }
-      __syncthreads();
-      // interface rows: add the neighbours' partials in ascending rank order
-      for (int k = ri0 + (int)threadIdx.x; k < ri1; k += kResBlock) {
-        const int64_t i = g.rrow[k];
-        const int l = (int)(i - r0);
-        double q = sq[l];
-        for (int e = g.recv_ptr[k]; e < g.recv_ptr[k + 1]; ++e) q += __ldcg(g.recv + g.recv_off[e]);
+    }
+    tm_wait_st();
+    __syncthreads();
+    // ---- p = z + beta p, q = A z + beta q (+ neighbours' partials), p.q
+    double pq = 0.0;
+#pragma unroll 1
+    for (int k = 0; k * (kResBlock / 32) + warp < nsl; ++k) {
+      const int sl = warp + k * (kResBlock / 32);
+      uint32_t lo, hi;
+      tm_ld(tx + 16 + 2 * k, lo, hi);
+      tm_wait_ld();
+      const double az = tm_val(lo, hi);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        const double p = fma(beta, spp[l], sz[l]);
+        double q = fma(beta, sq[l], az);
+        if ((smask[sl] >> lane) & 1u) {
+          const int64_t i = r0 + l;
+          // rrow is ascending: find this row's receive range
+          int lo_k = ri0, hi_k = ri1 - 1;
+          while (lo_k < hi_k) {
+            const int mid = (lo_k + hi_k) >> 1;
+            if (g.rrow[mid] < i) lo_k = mid + 1; else hi_k = mid;
+          }
+          for (int e = g.recv_ptr[lo_k]; e < g.recv_ptr[lo_k + 1]; ++e) q += __ldcg(g.recv + g.recv_off[e]);
+          if ((sown[sl] >> lane) & 1u) pq += p * q;
+        } else {
+          pq += p * q;  // non-interface rows are owned
+        }
+        spp[l] = p;
         sq[l] = q;
-        pq += g.own[i] * spp[l] * q;
       }
     }
-    double t1[1];
-    {
-      double v[1] = {pq};
-      block_sum<1, kResBlock>(v, sred);
-      ep += 1.0;
-      dd_allreduce<1>(c, v, 1, ep, nbar, sred, bcast, t1, t0);
-    }
-    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
-    // ---- update
+    // D^-1 of this thread's update rows: in flight across reduction A
     double dv[kDdRowsPerThread];
 #pragma unroll
     for (int k = 0; k < kDdRowsPerThread; ++k) {
       const int l = threadIdx.x + k * kResBlock;
       dv[k] = l < nloc ? __ldg(g.dinv + r0 + l) : 0.0;
     }
+    double t1[1], l1[1];
+    {
+      double v[1] = {pq};
+      block_sum<1, kResBlock>(v, sred);
+      ep += 1.0;
+      dd_publish<1>(c, v, 1, ep, nbar, sred, bcast, l1);
+      dd_collect<1>(c, 1, ep, bcast, l1, t1, t0);
+    }
+    const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+    // ---- x += alpha p, r -= alpha q, z = D^-1 r
     double b0 = 0.0, b1 = 0.0;
+    uint32_t xw[kDdRowsPerThread][2];
+#pragma unroll
+    for (int k = 0; k < kDdRowsPerThread; ++k) tm_ld(tx + 2 * k, xw[k][0], xw[k][1]);
+    tm_wait_ld();
 #pragma unroll
     for (int k = 0; k < kDdRowsPerThread; ++k) {
       const int l = threadIdx.x + k * kResBlock;
+      const double xo = tm_val(xw[k][0], xw[k][1]);
+      tm_st(tx + 2 * k, l < nloc ? fma(alpha, spp[l], xo) : xo);
       if (l < nloc) {
-        sx[l] = fma(alpha, spp[l], sx[l]);
         const double ri = fma(-alpha, sq[l], sr[l]);
         const double zi = dv[k] * ri;
         sr[l] = ri;
         sz[l] = zi;
         g.zg[r0 + l] = zi;
-        const double w = g.own[r0 + l];
-        b0 += w * ri * zi;
-        b1 += w * ri * ri;
+        if ((sown[l >> 5] >> (l & 31)) & 1u) {
+          b0 += ri * zi;
+          b1 += ri * ri;
+        }
       }
     }
     {
       double v[2] = {b0, b1};
       block_sum<2, kResBlock>(v, sred);
       ep += 1.0;
-      dd_allreduce<2>(c, v, 2, ep, nbar, sred, bcast, t2, t0);
+      epB = ep;
+      dd_publish<2>(c, v, 2, ep, nbar, sred, bcast, l2);  // local grid barrier: z published in the rank
+      pending = true;
     }
+  }
+  if (pending) {
+    dd_collect<2>(c, 2, epB, bcast, l2, t2, t0);
     rz_old = rz;
     rz = t2[0];
     rr = t2[1];
   }
-  for (int l = threadIdx.x; l < nloc; l += kResBlock) g.x_out[g.perm[r0 + l]] = sx[l];
+  tm_wait_st();
+#pragma unroll
+  for (int k = 0; k < kDdRowsPerThread; ++k) {
+    uint32_t lo, hi;
+    tm_ld(tx + 2 * k, lo, hi);
+    tm_wait_ld();
+    const int l = threadIdx.x + k * kResBlock;
+    if (l < nloc) g.x_out[g.perm[r0 + l]] = tm_val(lo, hi);
+  }
+  tmem_free_all(taddr);
   // every CTA of the rank has read evbase before its first reduction
   if (lcta == 0 && threadIdx.x == 0) {
     g.red[AB_RED_RZN] = rz;
     g.red[AB_RED_RR] = rr;
     g.red[AB_RED_ITERS] = s_failed ? -1.0 : (double)it;
     g.sc[AB_SC_BB] = bb;
-    g.evbase[0] = hbase + (unsigned long long)it;
+    g.evbase[0] = hbase + hev;
     g.evbase[1] = (unsigned long long)ep;
   }
 }
@@ -308,7 +400,8 @@ int ab_cg_dd(const ab_cg_dd_rank* groups_dev, int32_t n_groups, int32_t n_cta_to
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (!coop) return fail("ab_cg_dd: cooperative launch unsupported");
   if (n_cta_total > sms) return fail("ab_cg_dd: more CTAs than SMs");
-  const size_t smem = (size_t)(5 * max_rows_per_cta + max_ghost) * 8 + (size_t)(max_rows_per_cta / 32) * 4;
+  const size_t smem = (size_t)(4 * max_rows_per_cta + max_ghost) * 8 + (size_t)(max_rows_per_cta / 32 + 1) * 8 +
+                      (size_t)(max_rows_per_cta / 32 + 1) * 8 + (size_t)max_ghost * 4 + 16;
   if (smem + 1024 > (size_t)optin) return fail("ab_cg_dd: rows + ghosts do not fit in shared memory");
   if (cudaFuncSetAttribute((const void*)k_cg_dd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
       cudaSuccess)

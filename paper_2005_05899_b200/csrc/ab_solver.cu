@@ -613,7 +613,6 @@ constexpr int kTmThreads = (kTmNC + 1) * 32;
 constexpr int kTmCols = (512 / (kTmNC / 4)) & ~1;  // TMEM columns per consumer warp
 constexpr int kTmMaxSlots = kTmCols / 10;   // row slots per thread (5 doubles each)
 
-__device__ __forceinline__ uint32_t sa32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void cbar() { asm volatile("bar.sync 1, %0;" ::"n"(kTmNC * 32) : "memory"); }
 
 __device__ __forceinline__ void mb_init(uint64_t* b, unsigned count) {
@@ -645,20 +644,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
                : "memory");
 }
 
-// TMEM: one double per thread = two 32-bit columns of the thread's lane.
-__device__ __forceinline__ void tm_ld(uint32_t a, uint32_t& lo, uint32_t& hi) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0, %1}, [%2];" : "=r"(lo), "=r"(hi) : "r"(a) : "memory");
-}
-__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-__device__ __forceinline__ double tm_val(uint32_t lo, uint32_t hi) {
-  asm volatile("" : "+r"(lo), "+r"(hi));  // keep uses after tcgen05.wait::ld
-  return __hiloint2double((int)hi, (int)lo);
-}
-__device__ __forceinline__ void tm_st(uint32_t a, double v) {
-  const uint32_t lo = (uint32_t)__double2loint(v), hi = (uint32_t)__double2hiint(v);
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(a), "r"(lo), "r"(hi) : "memory");
-}
-__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 
 // Sum over the consumer warps (valid in warp 0); sm >= NV * kTmNC doubles.
 template <int NV>

@@ -163,6 +163,7 @@ class DDRank:
         s.rrow_ptr, s.rrow, s.recv_ptr, s.recv_off = (ptr(self.rrow_ptr), ptr(self.rrow), ptr(self.recv_ptr),
                                                       ptr(self.recv_off))
         s.recv, s.cnt_in, s.red_in, s.evbase = ptr(self.recv), ptr(self.cnt_in), ptr(self.red_in), ptr(self.evbase)
+        s.pad0_ = 1 if getattr(self, "same_device", False) else 0
         s.n_peers = len(self.peers)
         for k, q in enumerate(self.peers):
             s.peer_rank[k] = q
@@ -171,6 +172,14 @@ class DDRank:
             s.peer_cnt[k] = self.peer_cnt[q]
             s.peer_red[k] = self.peer_red[q]
         return s
+
+    def fits(self) -> bool:
+        """Shared memory of ab_cg_dd for this rank (z + ghosts + tables)."""
+        dev = self.A.vals.device
+        optin = getattr(torch.cuda.get_device_properties(dev), "shared_memory_per_block_optin", 232448)
+        rb, mg = self.rb, self.map["max_ghost"]
+        need = (4 * rb + mg) * 8 + 2 * (rb // 32 + 1) * 8 + mg * 4 + 16
+        return need + 1024 <= optin and rb <= 8192
 
     @property
     def iterations(self) -> int:
@@ -206,11 +215,58 @@ class DDSolve:
              self.max_ghost, stream_handle())
 
 
+class FusedDDSolver:
+    """The decomposed pressure solve of one rank of a multi-GPU run (one
+    process per GPU): ab_cg_dd with peer buffers mapped through CUDA IPC.
+    ``solve(b, maxit, tol)`` mirrors PCG.solve; b is interface-summed."""
+
+    def __init__(self, dm, A: SellMatrix, dinv: torch.Tensor, fixed, plan, b: torch.Tensor, group=None):
+        import torch.distributed as dist
+        dev = dinv.device
+        n_ranks = plan.n_ranks
+
+        def all_ok(ok: bool, what: str):  # collective: every rank takes the same branch
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+            if int(t.item()) == 0:
+                raise RuntimeError(f"fused decomposed CG: {what} failed on some rank")
+
+        ms = torch.tensor([max([0] + [len(v) for v in plan.shared.values()])], dtype=torch.int64, device=dev)
+        dist.all_reduce(ms, op=dist.ReduceOp.MAX, group=group)
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        try:
+            self.rank = DDRank(plan.rank, n_ranks, A, dinv, plan.own, plan.shared, dm.node_order(), sms,
+                               fixed=fixed, max_shared=int(ms.item()))
+            ok = self.rank.fits()
+        except Exception:
+            ok = False
+        all_ok(ok, "setup")
+        try:
+            ipc_ranks(self.rank, group)
+            ok = True
+        except Exception:
+            ok = False
+        all_ok(ok, "peer mapping (CUDA IPC)")
+        self.launch = DDSolve([self.rank], [b], zero_b=True)
+        self.b = b
+
+    @property
+    def x(self) -> torch.Tensor:
+        return self.rank.x
+
+    def solve(self, b: torch.Tensor, maxit: int, tol: float = 0.0):
+        assert b.data_ptr() == self.b.data_ptr(), "the fused solver is bound to its right-hand side buffer"
+        self.launch.run(maxit, tol)
+        it = self.rank.iterations if tol > 0 else maxit
+        return self.rank.x, it
+
+
 def virtual_ranks(ranks: list):
     """Wire ranks hosted by one process on one GPU (peer pointers = device
     pointers of the other ranks' buffers)."""
     ex = [r.exports() for r in ranks]
     for r in ranks:
+        r.same_device = True
         for q in r.peers:
             r.connect(q, ex[q]["recv"], ex[q]["cnt_in"], ex[q]["red_in"], ex[q]["n_cta"])
     return ranks
@@ -227,10 +283,16 @@ def ipc_ranks(rank: DDRank, group=None):
         call("ab_ipc_get_handle", ptr(t), h, C.byref(off))
         return bytes(h), off.value
 
-    mine = {"recv": handle(rank.recv), "cnt_in": handle(rank.cnt_in), "red_in": handle(rank.red_in),
-            "n_cta": rank.n_cta}
+    try:
+        mine = {"recv": handle(rank.recv), "cnt_in": handle(rank.cnt_in), "red_in": handle(rank.red_in),
+                "n_cta": rank.n_cta}
+    except Exception as e:  # still take part in the exchange, then fail
+        mine = {"error": str(e)}
     allx = [None] * rank.n_ranks
     dist.all_gather_object(allx, mine, group=group)
+    bad = [q for q, x in enumerate(allx) if "error" in x]
+    if bad:
+        raise RuntimeError(f"CUDA IPC export failed on ranks {bad}")
     rank._ipc = []
     for q in rank.peers:
         ptrs = {}

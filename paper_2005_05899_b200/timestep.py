@@ -53,7 +53,8 @@ class FlowSolver:
     """
 
     def __init__(self, mesh, params: FlowParams | None = None, p_fixed=None, u_fixed=None, u_fixed_values=None,
-                 windows: bool = True, reorder: str | None = "sfc", halo=None, own=None, ops: str = "spmv"):
+                 windows: bool = True, reorder: str | None = "sfc", halo=None, own=None, ops: str = "spmv",
+                 fused_cg: bool | None = None):
         self.params = params or FlowParams()
         self.phys = self.params.struct()
         self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows)
@@ -106,10 +107,53 @@ class FlowSolver:
         self.U0, self.U, self.R, self.GP, self.GD = z4(), z4(), z4(), z4(), z4()
         self.P = torch.zeros(n, dtype=torch.float64, device=dev)
         self.B = torch.zeros(n, dtype=torch.float64, device=dev)
+        # decomposed domains on NCCL (one GPU per rank): the pressure solve runs
+        # as one kernel per rank fused with its interface exchange over peer
+        # memory (ddcg.FusedDDSolver), validated once against the NCCL-driven
+        # two-kernel solve; fused_cg=False keeps the latter
+        self.ddcg = None
+        if halo is not None and fused_cg is not False and self._nccl(halo):
+            self.ddcg = self._fused_solver(dm, pf, fused_cg)
         self.graph = None
         self.graph_key = None
         self.last_cg_iters = 0
         self.timeline = None  # list of (name, start, end) CUDA events when profiling
+
+    @staticmethod
+    def _nccl(halo) -> bool:
+        import torch.distributed as dist
+        return dist.is_initialized() and dist.get_backend(halo.group) == "nccl"
+
+    def _fused_solver(self, dm, pf, required):
+        import torch.distributed as dist
+        from .ddcg import FusedDDSolver
+        plan = self.halo.plan
+        fixed = self.p_fixed if pf.any() else None
+        try:
+            dd = FusedDDSolver(dm, self.L, self.dinv, fixed, plan, self.B, group=self.halo.group)
+            # validation solve: same iterate as the NCCL-driven kernels
+            g = torch.Generator(device="cpu").manual_seed(1234)
+            bh = torch.randn(len(plan.l2g), generator=g, dtype=torch.float64).to(self.B.device)
+            self.B.copy_(bh)
+            self.halo.sum_(self.B, 1, 1)
+            b0 = self.B.clone()
+            x_dd, _ = dd.solve(self.B, 8)
+            x_dd = x_dd.clone()
+            self.B.copy_(b0)
+            x_ref, _ = self.pcg.solve(self.B, 8)
+            d = torch.tensor([float((x_dd - x_ref).abs().max() / x_ref.abs().max().clamp_min(1e-300))],
+                             dtype=torch.float64, device=self.B.device)
+            dist.all_reduce(d, op=dist.ReduceOp.MAX, group=self.halo.group)
+            self.B.zero_()
+            if float(d.item()) > 1e-10:
+                raise RuntimeError(f"fused decomposed CG disagrees with the NCCL solve ({float(d.item()):.2e})")
+            return dd
+        except Exception as e:  # keep the NCCL-driven solve
+            if required:
+                raise
+            import warnings
+            warnings.warn(f"fused decomposed CG unavailable, using the NCCL-driven solve: {e}")
+            return None
 
     def _grad(self, p, out4, scale: float = 1.0):
         if self.Bop is not None:
@@ -192,7 +236,11 @@ class FlowSolver:
             with self._mark("X_halo_sum"):
                 self.halo.sum_(self.B, 1, 1)
         self.pcg.mark = self._mark
-        x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
+        if self.ddcg is not None:
+            with self._mark("K5_cg_fused_dd"):
+                x, it = self.ddcg.solve(self.B, cg_iters, tol=cg_tol)
+        else:
+            x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
         self.last_cg_iters = it
         if self.Bop is not None and self.halo is None:
             # K6 + K7 fused: u = u_3 - dt/rho M^-1 B dp; p += dp; Gp += B dp
