@@ -88,3 +88,16 @@ def test_dd_cg_single_rank_is_the_resident_solver():
     xr, _, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 12)
     assert rel_l2(ranks[0].x.cpu().numpy(), xr[subs[0][1].l2g]) <= 1e-10
     assert float(bt.abs().max()) == 0.0  # zero_b re-zeroes the accumulation buffer
+
+
+def test_ipc_wiring_two_processes_one_gpu():
+    """ddcg.ipc_ranks (CUDA IPC handles exchanged over torch.distributed, the
+    multi-GPU wiring) driven by two processes sharing one GPU."""
+    import subprocess
+    import sys
+    from pathlib import Path
+    root = Path(__file__).resolve().parents[1]
+    r = subprocess.run([sys.executable, str(root / "tools" / "ipc_dd_check.py")], capture_output=True, text=True,
+                       timeout=300)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "ipc wiring ok" in r.stdout
