@@ -133,7 +133,7 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
     from paper_2005_05899_b200.meshgen import NODE_COUNT, RULE_KIND
     conn_bytes = sum(4 * NODE_COUNT[RULE_KIND[r]] * e for r, e in counts.items())
     N = n_nodes
-    if kernel == "K5_cg_resident":  # SURVEY §8(d) K5 per iteration: 12Z + 4(N+1) + 104N
+    if kernel in ("K5_cg_resident", "K5_cg_fused_dd"):  # SURVEY §8(d) K5 per iteration: 12Z + 4(N+1) + 104N
         return cg_iters * (12 * nnz + 4 * (N + 1) + 104 * N), cg_iters * (2 * nnz + 12 * N)
     if kernel == "K5_cg_spmv":      # vals+cols, z gathered once, p & q read + written
         return 12 * nnz + 8 * N + 32 * N, 2 * nnz + 4 * N

@@ -129,31 +129,47 @@ class FlowSolver:
         from .ddcg import FusedDDSolver
         plan = self.halo.plan
         fixed = self.p_fixed if pf.any() else None
+        def consensus(ok: bool) -> bool:  # every rank takes the same branch
+            t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.B.device)
+            dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.halo.group)
+            return bool(int(t.item()))
+
+        err = None
         try:
             dd = FusedDDSolver(dm, self.L, self.dinv, fixed, plan, self.B, group=self.halo.group)
+        except Exception as e:  # FusedDDSolver's own checks are collective
+            dd, err = None, e
+        if dd is not None:
             # validation solve: same iterate as the NCCL-driven kernels
             g = torch.Generator(device="cpu").manual_seed(1234)
             bh = torch.randn(len(plan.l2g), generator=g, dtype=torch.float64).to(self.B.device)
             self.B.copy_(bh)
             self.halo.sum_(self.B, 1, 1)
             b0 = self.B.clone()
-            x_dd, _ = dd.solve(self.B, 8)
-            x_dd = x_dd.clone()
-            self.B.copy_(b0)
-            x_ref, _ = self.pcg.solve(self.B, 8)
-            d = torch.tensor([float((x_dd - x_ref).abs().max() / x_ref.abs().max().clamp_min(1e-300))],
-                             dtype=torch.float64, device=self.B.device)
-            dist.all_reduce(d, op=dist.ReduceOp.MAX, group=self.halo.group)
+            try:
+                x_dd, _ = dd.solve(self.B, 8)
+                x_dd = x_dd.clone()
+                ran = dd.rank.iterations == 8
+            except Exception as e:
+                ran, err = False, e
+            if consensus(ran):
+                self.B.copy_(b0)
+                x_ref, _ = self.pcg.solve(self.B, 8)
+                d = torch.tensor([float((x_dd - x_ref).abs().max() / x_ref.abs().max().clamp_min(1e-300))],
+                                 dtype=torch.float64, device=self.B.device)
+                dist.all_reduce(d, op=dist.ReduceOp.MAX, group=self.halo.group)
+                if float(d.item()) > 1e-10:
+                    dd, err = None, RuntimeError(f"fused decomposed CG disagrees with the NCCL solve "
+                                                 f"({float(d.item()):.2e})")
+            else:
+                dd = None
             self.B.zero_()
-            if float(d.item()) > 1e-10:
-                raise RuntimeError(f"fused decomposed CG disagrees with the NCCL solve ({float(d.item()):.2e})")
-            return dd
-        except Exception as e:  # keep the NCCL-driven solve
+        if dd is None:
             if required:
-                raise
+                raise RuntimeError(f"fused decomposed CG unavailable: {err}")
             import warnings
-            warnings.warn(f"fused decomposed CG unavailable, using the NCCL-driven solve: {e}")
-            return None
+            warnings.warn(f"fused decomposed CG unavailable, using the NCCL-driven solve: {err}")
+        return dd
 
     def _grad(self, p, out4, scale: float = 1.0):
         if self.Bop is not None:
