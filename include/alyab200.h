@@ -207,13 +207,18 @@ typedef struct ab_cg_local {
   const int32_t* ghost;
   const int32_t* perm;       /* [n_rows] or NULL */
   int32_t prefetch_depth;
-  int32_t variant;           /* 0: vectors in shared memory; 1: tensor-memory solver (k_cg_tmem) */
+  int32_t variant;           /* 0: vectors in shared memory; 1: tensor-memory solver (k_cg_tmem);
+                                2: single-reduction (Chronopoulos-Gear) form (k_cg_cg1) */
   /* variant 1: the CTA's slices in chunks of `group` slices, each chunk's
    * values then local columns contiguous: chunk [E0, E1) of entries at byte
    * 10*E0, values (8 B) first, then columns (2 B). */
   const unsigned char* packed;
   int32_t group;
   int32_t pad_;
+  /* variant 2 (single-reduction form, k_cg_cg1): the CTAs owning each CTA's
+   * ghost rows, nbr[nbr_ptr[b] .. nbr_ptr[b+1]) */
+  const int32_t* nbr_ptr;
+  const int32_t* nbr;
 } ab_cg_local;
 /* Diagnostics: buf (device, >= 8 * n_cta int64, or NULL to disable) receives
  * globaltimer stamps of the resident solver's phase boundaries in iteration

@@ -979,6 +979,216 @@ static unsigned cg_grid(int64_t n) {
   return (unsigned)(g < kCgGrid ? g : kCgGrid);
 }
 
+// ---------------------------------------------------------------------------
+// Single-reduction resident CG (Chronopoulos-Gear form, k_cg_cg1).  Same
+// preconditioned CG in exact arithmetic, reorganised so that each iteration
+// has ONE grid-wide reduction:
+//   s = A z (SpMV on z); gamma = r.z, delta = z.s, rr = r.r  -> one reduction
+//   beta = gamma / gamma_old;  alpha = gamma / (delta - beta gamma / alpha_old)
+//   p = z + beta p;  q = s + beta q (= A p);  x += alpha p;  r -= alpha q;
+//   z = D^-1 r  -> published to the neighbouring CTAs by per-CTA epoch flags
+// The second grid barrier of the two-reduction form becomes a wait on the
+// CTAs that own this CTA's ghost rows (z visibility is the only thing the
+// next SpMV needs); the grid barrier of the reduction follows every SpMV, so
+// no CTA can overwrite z while a neighbour still gathers it.  x and s = A z
+// wait in tensor memory (columns 0-15 / 16-31 of the thread's lane), r, p,
+// q, z + ghosts stay in shared memory.  Row mapping everywhere: slice sl =
+// warp + 32 k, lane = row in the slice.
+// ---------------------------------------------------------------------------
+constexpr int kCg1Rounds = 8;  // slices per warp: rows_per_cta <= 8 * 1024
+
+__global__ void __launch_bounds__(kResBlock, 1) k_cg_cg1(
+    int64_t n, int64_t rows_per_cta, int max_ghost, const int64_t* __restrict__ sp,
+    const uint16_t* __restrict__ lcol, const double* __restrict__ sval, const int32_t* __restrict__ gptr,
+    const int32_t* __restrict__ gidx, const int32_t* __restrict__ nbr_ptr, const int32_t* __restrict__ nbr,
+    const int32_t* __restrict__ perm, const double* __restrict__ b_in, double* b_zero,
+    const uint8_t* __restrict__ fixed, const double* __restrict__ dinv, double* __restrict__ x_out, double* zg,
+    int maxit, double tol, double* red, double* sc, double* part, unsigned* bar, unsigned* flags) {
+  extern __shared__ double smem[];
+  __shared__ double sred[3 * (kResBlock / 32)];
+  __shared__ double bcast[4];
+  __shared__ uint32_t s_taddr;
+  const int nb = gridDim.x;
+  const int64_t RB = rows_per_cta;
+  const int64_t r0 = (int64_t)blockIdx.x * RB;
+  const int64_t r1 = r0 + RB < n ? r0 + RB : n;
+  const int nloc = r1 > r0 ? (int)(r1 - r0) : 0;
+  double* sr = smem;
+  double* spp = sr + RB;
+  double* sq = spp + RB;
+  double* sz = sq + RB;  // [RB] own rows, then [max_ghost] ghosts
+  int64_t* tsp = reinterpret_cast<int64_t*>(sz + RB + max_ghost);
+  int32_t* tg = reinterpret_cast<int32_t*>(tsp + RB / 32 + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nsl = (nloc + 31) >> 5;
+  const int64_t s_first = r0 >> 5;
+  const int g0 = gptr[blockIdx.x];
+  const int ng = gptr[blockIdx.x + 1] - g0;
+  const int nb0 = nbr_ptr[blockIdx.x], nnb = nbr_ptr[blockIdx.x + 1] - nb0;
+  for (int k = threadIdx.x; k <= nsl; k += kResBlock) tsp[k] = sp[s_first + k];
+  for (int k = threadIdx.x; k < ng; k += kResBlock) tg[k] = gidx[g0 + k];
+  const uint32_t taddr = tmem_alloc_all(&s_taddr);  // includes __syncthreads
+  const uint32_t tx = taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+  unsigned nbar = 0;
+
+  // ---- init: r = b (fixed rows 0), z = D^-1 r, x = p = q = 0
+#pragma unroll
+  for (int k = 0; k < kCg1Rounds; ++k) {
+    const int sl = warp + k * (kResBlock / 32);
+    const int l = sl * 32 + lane;
+    if (sl < nsl && l < nloc) {
+      const int64_t i = r0 + l;
+      const int64_t ni = perm ? (int64_t)perm[i] : i;
+      double ri = b_in[ni];
+      if (fixed && fixed[i]) ri = 0.0;
+      if (b_zero) b_zero[ni] = 0.0;
+      const double zi = dinv[i] * ri;
+      sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
+      zg[i] = zi;
+    }
+    tm_st(tx + 2 * k, 0.0);
+  }
+  tm_wait_st();
+  grid_barrier(bar, ++nbar * nb);  // z visible to every CTA
+
+  double gamma_old = 0.0, alpha_old = 0.0, bb = 0.0, gamma = 0.0, rr = 0.0;
+  int it = 0;
+  bool converged = false;
+  for (; it < maxit; ++it) {
+    // ---- ghost z -> shared memory
+    for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + tg[k]);
+    __syncthreads();
+    // ---- s = A z -> TMEM; local gamma = r.z, delta = z.s, rr = r.r
+    double dg = 0.0, dd = 0.0, dr = 0.0;
+#pragma unroll 1
+    for (int k = 0; k * (kResBlock / 32) + warp < nsl; ++k) {
+      const int sl = warp + k * (kResBlock / 32);
+      const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      tm_st(tx + 16 + 2 * k, az);
+      const int l = sl * 32 + lane;
+      if (l < nloc) {
+        const double zi = sz[l], ri = sr[l];
+        dg += ri * zi;
+        dd += zi * az;
+        dr += ri * ri;
+      }
+    }
+    // D^-1 of this thread's rows: in flight across the reduction
+    double dv[kCg1Rounds];
+#pragma unroll
+    for (int k = 0; k < kCg1Rounds; ++k) {
+      const int l = (warp + k * (kResBlock / 32)) * 32 + lane;
+      dv[k] = l < nloc ? __ldg(dinv + r0 + l) : 0.0;
+    }
+    double t3[3];
+    {
+      double v[3] = {dg, dd, dr};
+      block_sum<3, kResBlock>(v, sred);
+      if (threadIdx.x == 0) {
+        part[blockIdx.x] = v[0];
+        part[nb + blockIdx.x] = v[1];
+        part[2 * nb + blockIdx.x] = v[2];
+      }
+      grid_barrier(bar, ++nbar * nb);
+      all_sum_par<3>(part, nb, sred, bcast, t3);
+    }
+    gamma = t3[0];
+    rr = t3[2];
+    if (it == 0) bb = rr;
+    if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) {
+      converged = true;
+      break;
+    }
+    const double delta = t3[1];
+    double alpha, beta;
+    if (it == 0) {
+      beta = 0.0;
+      alpha = delta != 0.0 ? gamma / delta : 0.0;
+    } else {
+      beta = gamma_old != 0.0 ? gamma / gamma_old : 0.0;
+      const double den = delta - (alpha_old != 0.0 ? beta * gamma / alpha_old : 0.0);
+      alpha = den != 0.0 ? gamma / den : 0.0;
+    }
+    // ---- p = z + beta p, q = s + beta q, x += alpha p, r -= alpha q, z = D^-1 r
+    tm_wait_st();
+#pragma unroll
+    for (int k = 0; k < kCg1Rounds; ++k) {
+      const int sl = warp + k * (kResBlock / 32);
+      if (sl >= nsl) break;  // warp-uniform
+      uint32_t xl, xh, sl32, sh;
+      tm_ld(tx + 2 * k, xl, xh);
+      tm_ld(tx + 16 + 2 * k, sl32, sh);
+      tm_wait_ld();
+      const double xo = tm_val(xl, xh), si = tm_val(sl32, sh);
+      const int l = sl * 32 + lane;
+      double xn = xo;
+      if (l < nloc) {
+        const double p = fma(beta, spp[l], sz[l]);
+        const double q = fma(beta, sq[l], si);
+        xn = fma(alpha, p, xo);
+        const double ri = fma(-alpha, q, sr[l]);
+        const double zi = dv[k] * ri;
+        spp[l] = p;
+        sq[l] = q;
+        sr[l] = ri;
+        sz[l] = zi;
+        zg[r0 + l] = zi;
+      }
+      tm_st(tx + 2 * k, xn);
+    }
+    gamma_old = gamma;
+    alpha_old = alpha;
+    // ---- publish z; wait for the CTAs owning this CTA's ghost rows
+    __syncthreads();
+    if (threadIdx.x == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flags + blockIdx.x), "r"((unsigned)(it + 1))
+                   : "memory");
+    if ((int)threadIdx.x < nnb) {
+      const unsigned* f = flags + nbr[nb0 + threadIdx.x];
+      unsigned v;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      } while (v < (unsigned)(it + 1));
+    }
+    __syncthreads();
+  }
+  if (!converged) {  // residual of the final iterate (one more reduction)
+    double v[2] = {0.0, 0.0};
+    for (int l = threadIdx.x; l < nloc; l += kResBlock) {
+      v[0] += sr[l] * sz[l];
+      v[1] += sr[l] * sr[l];
+    }
+    block_sum<2, kResBlock>(v, sred);
+    if (threadIdx.x == 0) {
+      part[blockIdx.x] = v[0];
+      part[nb + blockIdx.x] = v[1];
+    }
+    grid_barrier(bar, ++nbar * nb);
+    double t2[2];
+    all_sum_par<2>(part, nb, sred, bcast, t2);
+    gamma = t2[0];
+    rr = t2[1];
+    if (maxit == 0) bb = rr;
+  }
+  tm_wait_st();
+#pragma unroll
+  for (int k = 0; k < kCg1Rounds; ++k) {
+    const int sl = warp + k * (kResBlock / 32);
+    uint32_t lo, hi;
+    tm_ld(tx + 2 * k, lo, hi);
+    tm_wait_ld();
+    const int l = sl * 32 + lane;
+    if (sl < nsl && l < nloc) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = tm_val(lo, hi);
+  }
+  tmem_free_all(taddr);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    red[AB_RED_RZN] = gamma;
+    red[AB_RED_RR] = rr;
+    red[AB_RED_ITERS] = (double)it;
+    sc[AB_SC_BB] = bb;
+  }
+}
+
 }  // namespace ab
 
 using namespace ab;
@@ -1093,8 +1303,6 @@ int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const u
 }  // extern "C"
 
 namespace {
-// dynamic shared memory of k_cg_resident_local: 2 = x in shared memory too,
-// 1 = x in global memory, 0 = does not fit
 // Shared-memory plan of k_cg_resident_local: 0 = does not fit, else
 // 1 + (x in shared memory) + 2 * (slice/ghost tables in shared memory).
 int local_mode(int64_t rb, int32_t max_ghost, size_t* bytes) {
@@ -1183,7 +1391,29 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
   cudaError_t e;
   TmLayout L{};
   size_t smem = 0;
-  if (m->variant == 1) {
+  if (m->variant == 2) {
+    if (!m->nbr_ptr || !m->nbr) return fail("ab_cg_resident_local: the single-reduction solver needs nbr lists");
+    if (rb > (int64_t)kCg1Rounds * kResBlock) return fail("ab_cg_resident_local: too many rows per CTA");
+    smem = (size_t)(4 * rb + mg) * 8 + (size_t)(rb / 32 + 1) * 8 + (size_t)mg * 4;
+    int optin = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    if (smem + 1024 > (size_t)optin) return fail("ab_cg_resident_local: system does not fit in shared memory");
+    if (cudaFuncSetAttribute((const void*)k_cg_cg1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return fail("ab_cg_resident_local: cannot reserve shared memory");
+    // per-CTA z epoch flags behind the partials, zeroed per solve
+    unsigned* flags = reinterpret_cast<unsigned*>(part + 8 * (size_t)ncta);
+    if (cudaMemsetAsync(flags, 0, sizeof(unsigned) * (size_t)ncta, S(stream)) != cudaSuccess)
+      return fail("ab_cg_resident_local: cannot reset the flags");
+    const int32_t* np_ = m->nbr_ptr;
+    const int32_t* nb_ = m->nbr;
+    void* args[] = {&n,          &rb,         &mg,           (void*)&sp,    (void*)&lcol, (void*)&vals,
+                    (void*)&gp,  (void*)&gi,  (void*)&np_,   (void*)&nb_,   (void*)&pm,   (void*)&b_in,
+                    &b_zero,     (void*)&fixed, (void*)&dinv, &x,           &z,           &mi,
+                    &tol,        &red,        &sc,           &part,         &bar,         &flags};
+    e = cudaLaunchCooperativeKernel((const void*)k_cg_cg1, dim3(ncta), dim3(kResBlock), args, smem, S(stream));
+  } else if (m->variant == 1) {
     if (!m->packed) return fail("ab_cg_resident_local: the tensor-memory solver needs the packed matrix");
     if (!tmem_layout(rb, mg, a->max_width, m->group, &L, &smem))
       return fail("ab_cg_resident_local: system does not fit the tensor-memory solver");

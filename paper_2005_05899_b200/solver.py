@@ -146,10 +146,20 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
     if rows_per_cta + max_ghost > 65536:
         return None
     lcols = torch.where(lc >= 32768, lc - 65536, lc).to(torch.int16).contiguous()
+    # CTAs owning each CTA's ghost rows (single-reduction solver's z flags)
+    owner = (uk % n) // rows_per_cta
+    pair = torch.unique(g_cta * n_cta + owner)
+    nbr = (pair % n_cta).to(torch.int32).contiguous()
+    nbr_ptr = torch.zeros(n_cta + 1, dtype=torch.int64, device=dev)
+    nbr_ptr[1:] = torch.cumsum(torch.bincount(pair // n_cta, minlength=n_cta), 0)
+    nbr_ptr = nbr_ptr.to(torch.int32).contiguous()
+    if int((nbr_ptr[1:] - nbr_ptr[:-1]).max().item()) > 1024:
+        return None
     ghost_ptr = ghost_ptr.to(torch.int32).contiguous()
     struct = AbCgLocal(rows_per_cta=rows_per_cta, n_cta=n_cta, max_ghost=max_ghost, cols=ptr(lcols),
-                       ghost_ptr=ptr(ghost_ptr), ghost=ptr(ghost))
-    return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct)
+                       ghost_ptr=ptr(ghost_ptr), ghost=ptr(ghost), nbr_ptr=ptr(nbr_ptr), nbr=ptr(nbr))
+    return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct, nbr=nbr,
+                nbr_ptr=nbr_ptr)
 
 
 def pack_chunks(A: SellMatrix, lcols: torch.Tensor, rows_per_cta: int, group: int) -> torch.Tensor:
@@ -244,7 +254,7 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1,
-                 tmem: bool = False, group: int = 0):
+                 tmem: bool = False, group: int = 0, single_reduction: bool = False):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -290,6 +300,9 @@ class PCG:
                 group = int(group) if group else max(1, -(-16384 // max(1, Ap.max_width * 256)))
                 m["tmem"] = bool(tmem and lib().ab_cg_tmem_fits(rb.value, m["max_ghost"], Ap.max_width, group) > 0)
                 m["struct"].variant = 1 if m["tmem"] else 0
+                m["cg1"] = bool(single_reduction and not m["tmem"])
+                if m["cg1"]:
+                    m["struct"].variant = 2
                 if m["tmem"]:
                     m["packed"] = pack_chunks(Ap, m["cols"], rb.value, group)
                     m["struct"].packed = ptr(m["packed"])

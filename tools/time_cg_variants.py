@@ -24,9 +24,8 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 order = dm.node_order()
 depths = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else []
 variants = {
-    "tmem": dict(order=order),
-    "tmem-g2": dict(order=order, group=2),
-    "tmem-g8": dict(order=order, group=8),
+    "cg1": dict(order=order, single_reduction=True),
+    "tmem": dict(order=order, tmem=True),
     "local+sfc": dict(order=order, tmem=False),
     **{f"depth{k}": dict(order=order, prefetch_depth=k, tmem=False) for k in depths},
     "local": dict(),
@@ -38,7 +37,7 @@ for name, kw in variants.items():
     pcg = PCG(A, dinv, fixed=fixed, **kw)
     info = ""
     if pcg.local is not None:
-        info = f"tmem={pcg.local['tmem']} group={pcg.local['struct'].group} max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
+        info = f"cg1={pcg.local.get('cg1')} tmem={pcg.local['tmem']} group={pcg.local['struct'].group} max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
     pcg.solve(b.clone(), its, zero_b=False)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
