@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
     ap.add_argument("--cg-iters", type=int, default=CG_ITERS)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-windows", action="store_true")
@@ -70,14 +70,18 @@ def build_workload(name: str, n_ranks: int):
         desc = {"workload": "C2: jittered Kuhn TET04 box (BASELINE configs[1])", "cells": [n * n_ranks, n, n],
                 "elements": mesh.n_elements, "nodes": mesh.n_nodes, "kinds": {"tet4": mesh.n_elements}}
     else:
-        scale = n_ranks ** (1.0 / 3.0)
-        mesh = meshgen.c3_mesh(scale)
+        if name == "c4":  # BASELINE configs[3] at N = 1: 300 x 300 x 490 cells, 40 prism layers (~249M elements)
+            mesh = meshgen.c4_mesh()
+        else:
+            mesh = meshgen.c3_mesh(n_ranks ** (1.0 / 3.0))
         u = np.zeros((mesh.n_nodes, 3))
         u[:, 0] = 1.0
         p = np.zeros(mesh.n_nodes)
         bc = meshgen.channel_bcs(mesh)
         params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
-        desc = {"workload": "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2])",
+        desc = {"workload": ("C4: ~250M-element mixed boundary-layer box on one GPU (BASELINE configs[3], N = 1)"
+                             if name == "c4" else
+                             "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2])"),
                 "elements": mesh.n_elements, "nodes": mesh.n_nodes,
                 "kinds": {r: int(c.shape[0]) for r, c in mesh.conn.items()}}
     return mesh, u, p, bc, params, desc

@@ -275,6 +275,12 @@ def c3_mesh(scale=1.0):
     return boundary_layer_mesh(nx, nx, nz, layers, hex_fraction=0.25)
 
 
+def c4_mesh():
+    """BASELINE.json configs[3]: 300x300x490 cells, 40 prism layers, 25% hex
+    patch -> ~249M elements / 44.5M nodes."""
+    return boundary_layer_mesh(300, 300, 490, 40, hex_fraction=0.25)
+
+
 # ---------------------------------------------------------------------------
 # Initial / boundary conditions of the BASELINE configurations (SURVEY §8(d))
 # ---------------------------------------------------------------------------

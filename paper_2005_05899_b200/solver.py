@@ -57,17 +57,23 @@ class SellMatrix:
         return y
 
 
-def csr_pattern(dm: DeviceMesh):
-    """Unique (row, col) pairs of all element node pairs, row-major sorted."""
+def csr_pattern(dm: DeviceMesh, chunk: int = 1 << 23):
+    """Unique (row, col) pairs of all element node pairs, row-major sorted.
+    Elements are processed in chunks (per-chunk unique first), so the peak
+    memory stays ~ chunk * nnode^2 keys even for 250M-element meshes."""
     N = dm.n_nodes
     keys = []
     for conn in dm.conn:
-        c = conn.to(torch.int64)
-        nn = c.shape[1]
-        rows = c.repeat_interleave(nn, dim=1).reshape(-1)
-        cols = c.repeat(1, nn).reshape(-1)
-        keys.append(torch.unique(rows * N + cols))
+        nn = conn.shape[1]
+        for e0 in range(0, conn.shape[0], chunk):
+            c = conn[e0:e0 + chunk].to(torch.int64)
+            k = (c[:, :, None] * N + c[:, None, :]).reshape(-1)
+            keys.append(torch.unique(k))
+            del c, k
+        if len(keys) > 8:  # keep the list short: merge partial results
+            keys = [torch.unique(torch.cat(keys))]
     key = torch.unique(torch.cat(keys))
+    del keys
     rows = key // N
     cols = (key % N).to(torch.int32)
     counts = torch.bincount(rows, minlength=N)
