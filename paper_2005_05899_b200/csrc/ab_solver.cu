@@ -441,6 +441,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
   __shared__ double bcast[4];
+  __shared__ uint32_t s_taddr;
   const int nb = gridDim.x;
   const int64_t RB = rows_per_cta;
   const int64_t r0 = (int64_t)blockIdx.x * RB;
@@ -449,8 +450,8 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   double* sr = smem;
   double* spp = sr + RB;
   double* sq = spp + RB;
-  double* sx = sq + RB;               // XS only
-  double* sz = XS ? sx + RB : sx;     // [RB] own rows, then [max_ghost] ghosts
+  double* sd = sq + RB;               // XS: D^-1 of the rows (x is in tensor memory)
+  double* sz = XS ? sd + RB : sd;     // [RB] own rows, then [max_ghost] ghosts
   // TB: the CTA's slice pointers and ghost ids copied to shared memory
   int64_t* tsp_s = reinterpret_cast<int64_t*>(sz + RB + max_ghost);
   int32_t* tg_s = reinterpret_cast<int32_t*>(tsp_s + RB / 32 + 1);
@@ -468,6 +469,16 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     for (int k = threadIdx.x; k < ng; k += kResBlock) tg_s[k] = gidx[g0 + k];
     __syncthreads();
   }
+  // XS: x of this thread's phase-B rows l = threadIdx.x + k * kResBlock in
+  // tensor memory, columns 2k, 2k + 1 of the thread's lane
+  uint32_t taddr = 0, tx = 0;
+  if (XS) {
+    taddr = tmem_alloc_all(&s_taddr);
+    tx = taddr + ((uint32_t)(32 * (warp & 3)) << 16) + (uint32_t)((warp >> 2) * 64);
+#pragma unroll
+    for (int k = 0; k < kLocRowsPerThread; ++k) tm_st(tx + 2 * k, 0.0);
+    tm_wait_st();
+  }
   const int64_t* tsp = TB ? tsp_s : sp + s_first;
   const int32_t* tg = TB ? tg_s : gidx + g0;
 
@@ -480,7 +491,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     if (b_zero) b_zero[ni] = 0.0;
     const double zi = dinv[i] * ri;
     sr[l] = ri; sz[l] = zi; spp[l] = 0.0; sq[l] = 0.0;
-    if (XS) sx[l] = 0.0; else x_out[ni] = 0.0;
+    if (XS) sd[l] = dinv[i]; else x_out[ni] = 0.0;
     zg[i] = zi;
     a0 += ri * zi;
     a1 += ri * ri;
@@ -515,6 +526,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
       if (lane == 0 && sl + pf_depth * (kResBlock / 32) < nsl)
         prefetch_slice16(tsp, lcol, sval, sl + pf_depth * (kResBlock / 32));
       const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      if (sl == warp) stamp(it, 7);
       const int l = sl * 32 + lane;
       if (l < nloc) {
         const double p = fma(beta, spp[l], sz[l]);
@@ -524,12 +536,14 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         pq += p * q;
       }
     }
-    // D^-1 of this thread's phase-B rows: in flight across the reduction
+    // D^-1 of this thread's phase-B rows (global form): in flight across the reduction
     double dv[kLocRowsPerThread];
+    if (!XS) {
 #pragma unroll
-    for (int k = 0; k < kLocRowsPerThread; ++k) {
-      const int l = threadIdx.x + k * kResBlock;
-      dv[k] = l < nloc ? __ldg(dinv + r0 + l) : 0.0;
+      for (int k = 0; k < kLocRowsPerThread; ++k) {
+        const int l = threadIdx.x + k * kResBlock;
+        dv[k] = l < nloc ? __ldg(dinv + r0 + l) : 0.0;
+      }
     }
     {
       double v[1] = {pq};
@@ -548,18 +562,26 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         if (warp + d * (kResBlock / 32) < nsl)
           prefetch_slice16(tsp, lcol, sval, warp + d * (kResBlock / 32));
     double b0 = 0.0, b1 = 0.0;
+    uint32_t xw[kLocRowsPerThread][2];
+    if (XS) {
+#pragma unroll
+      for (int k = 0; k < kLocRowsPerThread; ++k) tm_ld(tx + 2 * k, xw[k][0], xw[k][1]);
+      tm_wait_ld();
+    }
 #pragma unroll
     for (int k = 0; k < kLocRowsPerThread; ++k) {
       const int l = threadIdx.x + k * kResBlock;
+      if (XS) {
+        const double xo = tm_val(xw[k][0], xw[k][1]);
+        tm_st(tx + 2 * k, l < nloc ? fma(alpha, spp[l], xo) : xo);
+      }
       if (l < nloc) {
-        if (XS) {
-          sx[l] = fma(alpha, spp[l], sx[l]);
-        } else {
+        if (!XS) {
           const int64_t ni = perm ? (int64_t)perm[r0 + l] : r0 + l;
           x_out[ni] = fma(alpha, spp[l], x_out[ni]);
         }
         const double ri = fma(-alpha, sq[l], sr[l]);
-        const double zi = dv[k] * ri;
+        const double zi = (XS ? sd[l] : dv[k]) * ri;
         sr[l] = ri;
         sz[l] = zi;
         zg[r0 + l] = zi;
@@ -567,6 +589,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         b1 += ri * ri;
       }
     }
+    stamp(it, 6);
     {
       double v[2] = {b0, b1};
       block_sum<2, kResBlock>(v, sred);
@@ -580,8 +603,18 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     rz = t2[0];
     rr = t2[1];
   }
-  if (XS)
-    for (int l = threadIdx.x; l < nloc; l += kResBlock) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = sx[l];
+  if (XS) {
+    tm_wait_st();
+#pragma unroll
+    for (int k = 0; k < kLocRowsPerThread; ++k) {
+      uint32_t lo, hi;
+      tm_ld(tx + 2 * k, lo, hi);
+      tm_wait_ld();
+      const int l = threadIdx.x + k * kResBlock;
+      if (l < nloc) x_out[perm ? (int64_t)perm[r0 + l] : r0 + l] = tm_val(lo, hi);
+    }
+    tmem_free_all(taddr);
+  }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     red[AB_RED_RZN] = rz;
     red[AB_RED_RR] = rr;
