@@ -116,6 +116,20 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
 int ab_momentum_rhs(const ab_mesh* mesh, const ab_phys* phys, const double* u4, double* rhs4,
                     void* stream);
 
+/* ---- K8: boundary assembly of the equilibrium wall model ---------------
+ * (Algorithm 1 line 4).  Wall faces as
+ * node quadruples (-1 in slot 3 for triangles) plus the off-face nodes of
+ * the owning element (-1 padded) that define the exchange point; rhs4
+ * accumulates -rho u_tau^2 u_t/|u_t| A/n_face_nodes per face node, u_tau
+ * from Reichardt's law. */
+typedef struct ab_wall {
+  int64_t n_faces;
+  const int32_t* face;  /* [n_faces][4] */
+  const int32_t* off;   /* [n_faces][4] */
+} ab_wall;
+int ab_wall_traction(const ab_wall* w, const ab_phys* phys, const double* coords4, const double* u4, double* rhs4,
+                     void* stream);
+
 /* ---- K4: divergence  out[a] += scale * sum_e int N_a div(u) ------------- */
 int ab_divergence(const ab_mesh* mesh, const double* u4, double scale, double* out, void* stream);
 

@@ -12,9 +12,11 @@ Parity status
   against golden vectors produced by running the reference itself
   (tests/golden/make_golden.py -> tests/golden/reference_mass.npz).
 * PARITY UNPINNED (the reference has no Navier-Stokes code): the
-  momentum RHS, divergence/gradient, Laplacian, Jacobi-PCG and the RK3
-  fractional step below are restated from PAPER.md:192-237 with the decisions
-  of SURVEY.md Appendix A fixed in DESIGN.md §3.  They are cross-checked by
+  momentum RHS, divergence/gradient, Laplacian, Jacobi-PCG, the RK3
+  fractional step and the equilibrium wall model (boundary assembly,
+  Algorithm 1 line 4) below are restated from
+  PAPER.md:192-237 with the decisions of SURVEY.md Appendix A fixed in
+  DESIGN.md §3.  They are cross-checked by
   property tests (partition of unity, EMAC energy neutrality, SPD Laplacian,
   PCG vs scipy spsolve, TGV energy decay), not by the reference.
 
@@ -399,6 +401,108 @@ RK3_A = (0.0, 0.75, 1.0 / 3.0)
 RK3_B = (1.0, 0.25, 2.0 / 3.0)
 
 
+# ---------------------------------------------------------------------------
+# Boundary assembly: equilibrium wall model (Algorithm 1 line 4, PAPER.md:214,
+# :228, :256-257).  The cited wall-law paper is not in /root/reference: the
+# law (Reichardt), exchange location and face integration are the decisions
+# of DESIGN.md §3.
+# ---------------------------------------------------------------------------
+# local faces per kind, VTK node order, quads listed around their perimeter
+FACES = {
+    "tet": [(0, 1, 2), (0, 1, 3), (1, 2, 3), (0, 2, 3)],
+    "pyr": [(0, 1, 2, 3), (0, 1, 4), (1, 2, 4), (2, 3, 4), (3, 0, 4)],
+    "pri": [(0, 1, 2), (3, 4, 5), (0, 1, 4, 3), (1, 2, 5, 4), (2, 0, 3, 5)],
+    "hex": [(0, 1, 2, 3), (4, 5, 6, 7), (0, 1, 5, 4), (1, 2, 6, 5), (2, 3, 7, 6), (3, 0, 4, 7)],
+}
+KAPPA = 0.41
+REICHARDT_ITERS = 12
+
+
+def wall_faces(mesh, on_wall):
+    """Boundary faces whose nodes all satisfy ``on_wall`` (bool per node):
+    (face nodes (F,4), -1 padded for triangles; off-face nodes of the owning
+    element (F,4), -1 padded), ordered by (category, element, local face)."""
+    on_wall = np.asarray(on_wall, bool)
+    fn, off = [], []
+    for _tag, rule, conn, _ids in mesh.categories():
+        kind = RULE_KIND[rule]
+        nn = NNODE[kind]
+        for f in FACES[kind]:
+            hit = on_wall[conn[:, list(f)]].all(axis=1)
+            if not hit.any():
+                continue
+            rest = [a for a in range(nn) if a not in f]
+            F = np.full((int(hit.sum()), 4), -1, np.int64)
+            F[:, :len(f)] = conn[hit][:, list(f)]
+            O = np.full((int(hit.sum()), 4), -1, np.int64)
+            O[:, :len(rest)] = conn[hit][:, rest[:4]] if len(rest) <= 4 else conn[hit][:, rest[:4]]
+            fn.append((conn[hit].shape[0], F, O, np.nonzero(hit)[0], kind, f))
+    if not fn:
+        return np.zeros((0, 4), np.int64), np.zeros((0, 4), np.int64)
+    return np.concatenate([x[1] for x in fn]), np.concatenate([x[2] for x in fn])
+
+
+def reichardt_uplus(yp):
+    """Reichardt's law u+ (y+) and its derivative."""
+    e11, e3 = np.exp(-yp / 11.0), np.exp(-yp / 3.0)
+    up = np.log1p(KAPPA * yp) / KAPPA + 7.8 * (1.0 - e11 - (yp / 11.0) * e3)
+    dup = 1.0 / (1.0 + KAPPA * yp) + 7.8 * (e11 / 11.0 - e3 / 11.0 + (yp / 33.0) * e3)
+    return up, dup
+
+
+def reichardt_utau(ut, y, nu, iters=REICHARDT_ITERS):
+    """u_tau with ut = u_tau u+(y u_tau / nu): Newton from the viscous-
+    sublayer guess sqrt(nu ut / y), a fixed number of iterations."""
+    ut = np.asarray(ut, float)
+    live = ut > 0.0                     # no tangential velocity: no shear
+    ut_l = np.where(live, ut, 1.0)
+    utau = np.sqrt(nu * ut_l / y)
+    for _ in range(iters):
+        yp = y * utau / nu
+        up, dup = reichardt_uplus(yp)
+        f = utau * up - ut_l
+        df = up + yp * dup
+        utau = np.maximum(utau - f / df, 0.0)
+    return np.where(live, utau, 0.0)
+
+
+def wall_traction(mesh, faces, off, u, rho=1.0, mu=1.0):
+    """Boundary assembly of the wall model: per wall face, the exchange point
+    is the mean of the owning element's off-face nodes (velocity u_e, wall
+    distance y to the face plane); tau_w = rho u_tau^2 from Reichardt's law
+    on |u_t|, u_t = u_e - (u_e.n) n; every face node receives
+    -tau_w u_t/|u_t| * A_face / n_face_nodes.  Returns (N,3)."""
+    R = np.zeros((mesh.n_nodes, 3))
+    if faces.shape[0] == 0:
+        return R
+    X = mesh.coords
+    nf = (faces >= 0).sum(axis=1)
+    no = (off >= 0).sum(axis=1)
+    fx = np.where((faces >= 0)[..., None], X[np.maximum(faces, 0)], 0.0)           # (F,4,3)
+    xc = fx.sum(axis=1) / nf[:, None]
+    ox = np.where((off >= 0)[..., None], X[np.maximum(off, 0)], 0.0)
+    xe = ox.sum(axis=1) / no[:, None]
+    ue = np.where((off >= 0)[..., None], u[np.maximum(off, 0)], 0.0).sum(axis=1) / no[:, None]
+    a = np.cross(fx[:, 1] - fx[:, 0], fx[:, 2] - fx[:, 0])
+    quad = nf == 4
+    b = np.cross(fx[:, 2] - fx[:, 0], fx[:, 3] - fx[:, 0])
+    area = 0.5 * np.linalg.norm(a, axis=1) + np.where(quad, 0.5 * np.linalg.norm(b, axis=1), 0.0)
+    nv = a + np.where(quad[:, None], b, 0.0)
+    nv = nv / np.linalg.norm(nv, axis=1)[:, None]
+    nv = np.where((np.einsum("fi,fi->f", nv, xc - xe) < 0.0)[:, None], -nv, nv)    # outward
+    y = np.abs(np.einsum("fi,fi->f", xe - xc, nv))
+    un = np.einsum("fi,fi->f", ue, nv)
+    utv = ue - un[:, None] * nv
+    utm = np.linalg.norm(utv, axis=1)
+    utau = reichardt_utau(utm, y, mu / rho)
+    coef = np.where(utm > 0.0, -rho * utau * utau / np.where(utm > 0.0, utm, 1.0) * area / nf, 0.0)
+    contrib = coef[:, None] * utv                                                   # per face node
+    for k in range(4):
+        m = faces[:, k] >= 0
+        np.add.at(R, faces[m, k], contrib[m])
+    return R
+
+
 class FlowOracle:
     """Incremental-projection fractional step with SSP-RK3 momentum stages.
 
@@ -411,8 +515,9 @@ class FlowOracle:
     """
 
     def __init__(self, mesh, rho=1.0, mu=1.0, c_vreman=0.0, p_fixed=None,
-                 u_fixed=None, u_fixed_values=None):
+                 u_fixed=None, u_fixed_values=None, wall=None):
         self.mesh = mesh
+        self.wall = wall  # (faces, off) of wall_faces(): boundary assembly per stage
         self.rho, self.mu, self.c_vreman = rho, mu, c_vreman
         n = mesh.n_nodes
         self.p_fixed = np.zeros(n, bool) if p_fixed is None else np.asarray(p_fixed, bool)
@@ -435,6 +540,8 @@ class FlowOracle:
         k = dt / self.rho
         for s in range(3):
             R = momentum_rhs(self.mesh, u, self.rho, self.mu, self.c_vreman)
+            if self.wall is not None:
+                R = R + wall_traction(self.mesh, *self.wall, u, self.rho, self.mu)
             u = RK3_A[s] * u0 + RK3_B[s] * (u + k * self.minv[:, None] * (R - st["gp"]))
             u[self.u_fixed] = self.u_fixed_values[self.u_fixed]
         b = -(self.rho / dt) * divergence(self.mesh, u)

@@ -43,6 +43,10 @@ class AbSell3(C.Structure):
                 ("vz", vp)]
 
 
+class AbWall(C.Structure):
+    _fields_ = [("n_faces", i64), ("face", vp), ("off", vp)]
+
+
 class AbCgLocal(C.Structure):
     _fields_ = [("rows_per_cta", i64), ("n_cta", i32), ("max_ghost", i32), ("cols", vp), ("ghost_ptr", vp),
                 ("ghost", vp), ("perm", vp), ("prefetch_depth", i32),
@@ -59,6 +63,7 @@ _SIGS = {
     "ab_mass": ([P(AbMesh), i32, vp, vp, vp, i32, vp], C.c_int),
     "ab_momentum_rhs": ([P(AbMesh), P(AbPhys), vp, vp, vp], C.c_int),
     "ab_divergence": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
+    "ab_wall_traction": ([P(AbWall), P(AbPhys), vp, vp, vp, vp], C.c_int),
     "ab_gradient": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
     "ab_laplacian_csr": ([P(AbMesh), vp, vp, vp, vp], C.c_int),
     "ab_csr_dirichlet": ([i64, vp, vp, vp, vp, vp], C.c_int),

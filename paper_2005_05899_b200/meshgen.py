@@ -302,6 +302,25 @@ def c2_initial(coords, seed=20200131, noise=0.01):
     return u + rng.normal(0.0, noise, size=u.shape), np.zeros(coords.shape[0])
 
 
+def wall_model_bcs(mesh: MeshArrays):
+    """C3-C5 with the equilibrium wall model on z = 0 (Algorithm 1 line 4):
+    inflow u = (1,0,0) at x = 0, zero normal velocity on the wall (the wall
+    shear comes from the wall law), p = 0 at x = 1.  Returns (bcs, (faces,
+    off)) for FlowSolver(**bcs, wall=(faces, off))."""
+    from .wall import wall_faces
+    x = mesh.coords
+    n = mesh.n_nodes
+    uf = np.zeros((n, 3), bool)
+    uv = np.zeros((n, 3))
+    inflow = np.abs(x[:, 0] - x[:, 0].min()) < 1e-12
+    wall = np.abs(x[:, 2] - x[:, 2].min()) < 1e-12
+    uf[wall, 2] = True
+    uf[inflow] = True
+    uv[inflow] = (1.0, 0.0, 0.0)
+    pf = np.abs(x[:, 0] - x[:, 0].max()) < 1e-12
+    return dict(p_fixed=pf, u_fixed=uf, u_fixed_values=uv), wall_faces(mesh, wall)
+
+
 def channel_bcs(mesh: MeshArrays):
     """C3-C5 boundary conditions: inflow u = (1,0,0) at x = 0, no-slip at
     z = 0, p = 0 at x = 1."""

@@ -54,11 +54,16 @@ class FlowSolver:
 
     def __init__(self, mesh, params: FlowParams | None = None, p_fixed=None, u_fixed=None, u_fixed_values=None,
                  windows: bool = True, reorder: str | None = "sfc", halo=None, own=None, ops: str = "spmv",
-                 fused_cg: bool | None = None):
+                 fused_cg: bool | None = None, wall=None):
         self.params = params or FlowParams()
         self.phys = self.params.struct()
         self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows)
         dm = self.dm
+        # boundary assembly (Algorithm 1 line 4): wall model faces, (faces, off) or a WallModel
+        if wall is not None and not hasattr(wall, "add_traction"):
+            from .wall import WallModel
+            wall = WallModel(*wall, device=dm.device)
+        self.wall = wall if (wall is not None and wall.n_faces > 0) else None
         n = dm.n_nodes
         dev = dm.device
         self.n = n
@@ -236,6 +241,9 @@ class FlowSolver:
             uin = self.U0 if st == 0 else self.U
             with self._mark("K2_momentum"):
                 call("ab_momentum_rhs", ctypes.byref(dm.struct), ctypes.byref(self.phys), ptr(uin), ptr(self.R), s)
+            if self.wall is not None:
+                with self._mark("K8_wall"):
+                    self.wall.add_traction(self.phys, dm.coords4, uin, self.R)
             if self.halo is not None:
                 with self._mark("X_halo_sum"):
                     self.halo.sum_(self.R, 3, 4)
@@ -324,7 +332,7 @@ class FlowSolver:
 
     def launches_per_step(self, cg_iters: int) -> int:
         """Kernels of this library launched by one step (no halo)."""
-        ncat = len(self.dm.rules)
+        ncat = len(self.dm.rules) + (1 if self.wall is not None else 0)
         bc = 1 if self.bc_idx is not None else 0
         cg = 1 if self.pcg.resident else 2 + 2 * cg_iters
         if self.Bop is not None:

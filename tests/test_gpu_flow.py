@@ -90,6 +90,40 @@ def test_gradient_operator(name):
     assert float(g4[:, 3].abs().max()) == 0.0
 
 
+def test_wall_traction_matches_oracle():
+    """K8 (ab_wall_traction) vs oracle/fem.py:wall_traction on the mixed mesh."""
+    from paper_2005_05899_b200.timestep import FlowParams
+    from paper_2005_05899_b200.wall import assemble_wall_traction
+    m = MESHES["mixed"]
+    _, (F, O) = meshgen.wall_model_bcs(m)
+    u, _ = _field(m, 5)
+    ref = fem.wall_traction(m, F, O, u, 1.3, 2e-3)
+    got = assemble_wall_traction(m, F, O, u, FlowParams(rho=1.3, mu=2e-3)).cpu().numpy()
+    assert np.abs(ref).max() > 0
+    assert rel_l2(got, ref) <= TOL_RHS
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_time_steps_with_wall_model(graph):
+    """Full Algorithm 1 step (element + boundary assembly) vs the oracle."""
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+    m = MESHES["mixed"]
+    bc, wall = meshgen.wall_model_bcs(m)
+    u, p = _field(m, 6)
+    params = dict(rho=1.0, mu=0.01, c_vreman=0.07)
+    ora = fem.FlowOracle(m, **params, **bc, wall=wall)
+    st = ora.init_state(u, p)
+    fs = FlowSolver(m, FlowParams(**params), **bc, wall=wall)
+    assert fs.wall is not None and fs.wall.n_faces == wall[0].shape[0]
+    fs.set_state(u, p)
+    for _ in range(3):
+        st = ora.step(st, 2e-3, cg_iters=40)
+        fs.step(2e-3, cg_iters=40, graph=graph)
+    torch.cuda.synchronize()
+    assert rel_l2(fs.u.cpu().numpy(), st["u"]) <= TOL_STATE
+    assert rel_l2(fs.p.cpu().numpy(), st["p"]) <= TOL_STATE
+
+
 @pytest.mark.parametrize("name", list(MESHES))
 def test_laplacian_and_spmv(name):
     from paper_2005_05899_b200.solver import assemble_laplacian

@@ -97,3 +97,32 @@ def test_balance_metrics_match_reference():
         assert np.array_equal(mt.per_rank, e["per_rank"]) and np.array_equal(mt.deviations, e["deviations"])
     with pytest.raises(ValueError):
         TimingSample(1, np.array([1.0, 0.0]))
+
+
+def test_wall_model_oracle_properties():
+    """Equilibrium wall model (oracle/fem.py:wall_traction): Reichardt's law is
+    solved to rounding, the traction opposes the tangential exchange velocity,
+    normal velocity produces none, and the product's face extraction equals
+    the oracle's."""
+    from paper_2005_05899_b200 import meshgen
+    from paper_2005_05899_b200.wall import wall_faces
+    ut = np.array([1e-3, 0.1, 1.0, 10.0])
+    for y in (1e-4, 1e-2, 0.3):
+        utau = fem.reichardt_utau(ut, np.full(4, y), 1e-3)
+        up, _ = fem.reichardt_uplus(y * utau / 1e-3)
+        assert np.all(np.abs(utau * up - ut) <= 1e-13 * ut)
+    m = meshgen.c3_mesh(0.05)
+    on = np.abs(m.coords[:, 2] - m.coords[:, 2].min()) < 1e-12
+    F, O = fem.wall_faces(m, on)
+    Fp, Op = wall_faces(m, on)
+    assert np.array_equal(F, Fp) and np.array_equal(O, Op)
+    assert F.shape[0] > 0 and np.all(on[F[F >= 0]])
+    u = np.zeros((m.n_nodes, 3))
+    assert np.abs(fem.wall_traction(m, F, O, u, 1.0, 1e-3)).max() == 0.0
+    u[:, 2] = 0.7                                  # normal to the wall: no shear
+    assert np.abs(fem.wall_traction(m, F, O, u, 1.0, 1e-3)).max() <= 1e-15
+    u[:, 0], u[:, 1] = 1.0, -0.5                   # tangential part (1, -0.5)
+    R = fem.wall_traction(m, F, O, u, 1.2, 1e-3)
+    assert np.all(R[:, 2] == 0.0)
+    f = R.sum(axis=0)
+    assert f[0] < 0 and f[1] > 0 and abs(f[0] / f[1] + 2.0) <= 1e-12   # parallel to -(1, -0.5)
