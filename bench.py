@@ -66,6 +66,7 @@ def build_workload(name: str, n_ranks: int):
         mesh = meshgen.box_tets(n * n_ranks, n, n, lengths=(float(n_ranks), 1.0, 1.0), jitter=0.2, seed=20200131)
         u, p = meshgen.c2_initial(mesh.coords)
         bc = dict(p_fixed=meshgen.boundary_nodes(mesh))
+        wall_nodes = None
         params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
         desc = {"workload": "C2: jittered Kuhn TET04 box (BASELINE configs[1])", "cells": [n * n_ranks, n, n],
                 "elements": mesh.n_elements, "nodes": mesh.n_nodes, "kinds": {"tet4": mesh.n_elements}}
@@ -77,14 +78,19 @@ def build_workload(name: str, n_ranks: int):
         u = np.zeros((mesh.n_nodes, 3))
         u[:, 0] = 1.0
         p = np.zeros(mesh.n_nodes)
-        bc = meshgen.channel_bcs(mesh)
+        # full Algorithm 1 step: element + boundary assembly (equilibrium wall
+        # model on z = 0, zero normal velocity there)
+        bc, _faces = meshgen.wall_model_bcs(mesh)
+        wall_nodes = np.abs(mesh.coords[:, 2] - mesh.coords[:, 2].min()) < 1e-12
         params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
         desc = {"workload": ("C4: ~250M-element mixed boundary-layer box on one GPU (BASELINE configs[3], N = 1)"
                              if name == "c4" else
                              "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2])"),
                 "elements": mesh.n_elements, "nodes": mesh.n_nodes,
                 "kinds": {r: int(c.shape[0]) for r, c in mesh.conn.items()}}
-    return mesh, u, p, bc, params, desc
+    if wall_nodes is not None:
+        desc["wall"] = "equilibrium wall model (Reichardt) on z = 0, K8 per RK stage"
+    return mesh, u, p, bc, params, desc, wall_nodes
 
 
 class ClockSampler:
@@ -222,13 +228,16 @@ def run_native(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    mesh, u_g, p_g, bc_g, params, desc = build_workload(args.workload, ws)
+    mesh, u_g, p_g, bc_g, params, desc, wall_g = build_workload(args.workload, ws)
     n_elem_total = mesh.n_elements
     rebalance = None
 
     def make_solver(parts=None):
         if ws == 1:
-            s_ = FlowSolver(mesh, FlowParams(**params), **bc_g, windows=not args.no_windows, reorder="sfc")
+            from paper_2005_05899_b200.wall import wall_faces
+            wall = wall_faces(mesh, wall_g) if wall_g is not None else None
+            s_ = FlowSolver(mesh, FlowParams(**params), **bc_g, windows=not args.no_windows, reorder="sfc",
+                            wall=wall)
             s_.set_state(u_g, p_g)
             return s_, mesh.n_elements
         from paper_2005_05899_b200.decompose import decompose
@@ -236,8 +245,10 @@ def run_native(args):
         sub, plan = decompose(mesh, parts, ws, rank)
         l2g = plan.l2g
         halo = HaloExchanger(plan, "cuda")
+        from paper_2005_05899_b200.wall import wall_faces
+        wall = wall_faces(sub, wall_g[l2g]) if wall_g is not None else None
         s_ = FlowSolver(sub, FlowParams(**params), **{k: np.asarray(v)[l2g] for k, v in bc_g.items()},
-                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own)
+                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own, wall=wall)
         s_.set_state(u_g[l2g], p_g[l2g])
         return s_, sub.n_elements
 
@@ -364,7 +375,8 @@ def run_native(args):
         "unit": "M element-steps/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": dict(desc, step="3x(K2+K3) + K4 + PCG(%d it, Jacobi) + K6 + K7" % args.cg_iters,
+        "config": dict(desc, step=("3x(K2+%sK3) + K4 + PCG(%d it, Jacobi) + K6 + K7"
+                                   % ("K8+" if wall_g is not None else "", args.cg_iters)),
                        cg_iters=args.cg_iters, dt=DT, physics=params, cuda_graph=graph,
                        scatter="windowed" if not args.no_windows else "atomics",
                        l2="flushed (512 MB write) between timed steps", parallelism=f"dd{ws}"),
