@@ -14,8 +14,11 @@ u = torch.randn((m.n_nodes, 4), dtype=torch.float64, device="cuda")
 p = torch.randn(m.n_nodes, dtype=torch.float64, device="cuda")
 out4 = torch.zeros_like(u)
 out1 = torch.zeros_like(p)
-ph = FlowParams(1.0, 1e-3, 0.07).struct()
-for mode in ("direct", "window", "pipelined"):
+import os
+cv = float(os.environ.get("AB_CVREMAN", "0.07"))
+ph = FlowParams(1.0, 1e-3, cv).struct()
+modes = os.environ.get("AB_MODES", "direct,window,pipelined").split(",")
+for mode in modes:
     dm = DeviceMesh(m, reorder="sfc", windows=mode != "direct", pipelined=mode == "pipelined")
     res = {}
     for name, fn in (("K2", lambda: call("ab_momentum_rhs", ctypes.byref(dm.struct), ctypes.byref(ph), ptr(u),
