@@ -162,6 +162,10 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
     if int((nbr_ptr[1:] - nbr_ptr[:-1]).max().item()) > 1024:
         return None
     ghost_ptr = ghost_ptr.to(torch.int32).contiguous()
+    if ghost.numel() == 0:  # no remote columns at all: keep a valid (unused) array
+        ghost = torch.zeros(1, dtype=torch.int32, device=dev)
+    if nbr.numel() == 0:
+        nbr = torch.zeros(1, dtype=torch.int32, device=dev)
     struct = AbCgLocal(rows_per_cta=rows_per_cta, n_cta=n_cta, max_ghost=max_ghost, cols=ptr(lcols),
                        ghost_ptr=ptr(ghost_ptr), ghost=ptr(ghost), nbr_ptr=ptr(nbr_ptr), nbr=ptr(nbr))
     return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct, nbr=nbr,
