@@ -97,6 +97,47 @@ __device__ __forceinline__ void tm_st(uint32_t a, double v) {
 }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// 8 doubles / 8 packed 16-bit values per thread (16 / 4 columns)
+__device__ __forceinline__ void tm_st8d(uint32_t a, const double (&v)[8]) {
+  uint32_t w[16];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    w[2 * k] = (uint32_t)__double2loint(v[k]);
+    w[2 * k + 1] = (uint32_t)__double2hiint(v[k]);
+  }
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16};" ::"r"(a),
+      "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]), "r"(w[8]), "r"(w[9]),
+      "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]), "r"(w[14]), "r"(w[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld8d(uint32_t a, uint32_t (&w)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15}, [%16];"
+      : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]), "=r"(w[6]), "=r"(w[7]), "=r"(w[8]),
+        "=r"(w[9]), "=r"(w[10]), "=r"(w[11]), "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+      : "r"(a)
+      : "memory");
+}
+__device__ __forceinline__ void tm_st4u(uint32_t a, const uint32_t (&w)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(w[0]), "r"(w[1]),
+               "r"(w[2]), "r"(w[3])
+               : "memory");
+}
+__device__ __forceinline__ void tm_ld4u(uint32_t a, uint32_t (&w)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+               : "r"(a)
+               : "memory");
+}
+template <int N>
+__device__ __forceinline__ void tm_fence_regs(uint32_t (&w)[N]) {  // keep uses after tcgen05.wait::ld
+#pragma unroll
+  for (int k = 0; k < N; ++k) asm volatile("" : "+r"(w[k]));
+}
+
 // TMEM allocation of all 512 columns by warp 0 (one CTA per SM), address in *slot.
 __device__ __forceinline__ uint32_t tmem_alloc_all(uint32_t* slot) {
   if ((threadIdx.x >> 5) == 0) {

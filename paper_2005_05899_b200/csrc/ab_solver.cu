@@ -469,6 +469,8 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     for (int k = threadIdx.x; k < ng; k += kResBlock) tg_s[k] = gidx[g0 + k];
     __syncthreads();
   }
+  const int64_t* tsp = TB ? tsp_s : sp + s_first;
+  const int32_t* tg = TB ? tg_s : gidx + g0;
   // XS: x of this thread's phase-B rows l = threadIdx.x + k * kResBlock in
   // tensor memory, columns 2k, 2k + 1 of the thread's lane
   uint32_t taddr = 0, tx = 0;
@@ -479,8 +481,36 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     for (int k = 0; k < kLocRowsPerThread; ++k) tm_st(tx + 2 * k, 0.0);
     tm_wait_st();
   }
-  const int64_t* tsp = TB ? tsp_s : sp + s_first;
-  const int32_t* tg = TB ? tg_s : gidx + g0;
+  // XS: the warp's first slice (if at most 16 wide) stays in tensor memory
+  // for the whole solve - values in columns 16-47, 16-bit columns packed two
+  // per 32-bit column in 48-55 - so every iteration starts computing without
+  // waiting for the matrix stream
+  bool tm_slice = false;
+  int w0 = 0;
+  if (XS && warp < nsl) {
+    w0 = (int)((tsp[warp + 1] - tsp[warp]) >> 5);
+    tm_slice = w0 <= 16;
+  }
+  if (XS && tm_slice) {
+    const int64_t base = tsp[warp] + lane;
+#pragma unroll
+    for (int j0 = 0; j0 < 16; j0 += 8) {
+      double a[8];
+      uint32_t cw[4];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] = j0 + u < w0 ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const unsigned c0 = j0 + 2 * u < w0 ? (unsigned)__ldcs(lcol + base + (int64_t)(j0 + 2 * u) * 32) : 0u;
+        const unsigned c1 = j0 + 2 * u + 1 < w0 ? (unsigned)__ldcs(lcol + base + (int64_t)(j0 + 2 * u + 1) * 32)
+                                                 : 0u;
+        cw[u] = c0 | (c1 << 16);
+      }
+      tm_st8d(tx + 16 + 2 * j0, a);
+      tm_st4u(tx + 48 + j0 / 2, cw);
+    }
+    tm_wait_st();
+  }
 
   double a0 = 0.0, a1 = 0.0;
   for (int l = threadIdx.x; l < nloc; l += kResBlock) {
@@ -497,7 +527,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     a1 += ri * ri;
   }
   if (lane == 0)
-    for (int d = 0; d < pf_depth; ++d)
+    for (int d = (XS && tm_slice) ? 1 : 0; d < pf_depth + ((XS && tm_slice) ? 1 : 0); ++d)
       if (warp + d * (kResBlock / 32) < nsl) prefetch_slice16(tsp, lcol, sval, warp + d * (kResBlock / 32));
   {
     double v[2] = {a0, a1};
@@ -525,7 +555,26 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     for (int sl = warp; sl < nsl; sl += kResBlock / 32) {
       if (lane == 0 && sl + pf_depth * (kResBlock / 32) < nsl)
         prefetch_slice16(tsp, lcol, sval, sl + pf_depth * (kResBlock / 32));
-      const double az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      double az;
+      if (XS && sl == warp && tm_slice) {  // __syncwarp-uniform branch: whole warp
+        az = 0.0;
+#pragma unroll
+        for (int j0 = 0; j0 < 16; j0 += 8) {
+          uint32_t aw[16], cw[4];
+          tm_ld8d(tx + 16 + 2 * j0, aw);
+          tm_ld4u(tx + 48 + j0 / 2, cw);
+          tm_wait_ld();
+          tm_fence_regs(aw);
+          tm_fence_regs(cw);
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const unsigned c = (cw[u >> 1] >> (16 * (u & 1))) & 0xffffu;
+            az = fma(__hiloint2double((int)aw[2 * u + 1], (int)aw[2 * u]), sz[c], az);
+          }
+        }
+      } else {
+        az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
+      }
       if (sl == warp) stamp(it, 7);
       const int l = sl * 32 + lane;
       if (l < nloc) {
@@ -558,7 +607,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
     if (lane == 0 && it + 1 < maxit)
-      for (int d = 0; d < pf_depth; ++d)
+      for (int d = (XS && tm_slice) ? 1 : 0; d < pf_depth + ((XS && tm_slice) ? 1 : 0); ++d)
         if (warp + d * (kResBlock / 32) < nsl)
           prefetch_slice16(tsp, lcol, sval, warp + d * (kResBlock / 32));
     double b0 = 0.0, b1 = 0.0;
