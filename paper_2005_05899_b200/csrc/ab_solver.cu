@@ -419,8 +419,9 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident(
 // globaltimer stamps of thread 0 of every CTA at the phase boundaries of
 // iteration 10, tl[cta * 8 + k].
 __device__ int64_t* g_timeline = nullptr;
-__device__ __forceinline__ void stamp(int it, int k) {
-  int64_t* tl = g_timeline;
+// tl: g_timeline read once at kernel start (a global load per stamp sat on
+// the critical path after every barrier)
+__device__ __forceinline__ void stamp(int64_t* tl, int it, int k) {
   if (tl && it == 10 && threadIdx.x == 0) {
     int64_t t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -438,6 +439,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     double* b_zero,
     const uint8_t* __restrict__ fixed, const double* __restrict__ dinv, double* __restrict__ x_out, double* zg,
     int maxit, double tol, double* red, double* sc, double* part, unsigned* bar, int pf_depth) {
+  int64_t* const tl = g_timeline;
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
   __shared__ double bcast[4];
@@ -544,11 +546,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   for (; it < maxit; ++it) {
     if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
     const double beta = rz_old != 0.0 ? rz / rz_old : 0.0;
-    stamp(it, 0);
+    stamp(tl, it, 0);
     // ---- ghost z values of this CTA's columns -> shared memory
     for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(zg + tg[k]);
     __syncthreads();
-    stamp(it, 1);
+    stamp(tl, it, 1);
     // ---- phase A: p = z + beta p; q = A z + beta q (z from shared memory)
     double pq = 0.0;
 #pragma unroll 1
@@ -575,7 +577,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
       } else {
         az = sell_row_dot_smem<kLocChunk>(tsp, lcol, sval, sz, sl, lane);
       }
-      if (sl == warp) stamp(it, 7);
+      if (sl == warp) stamp(tl, it, 7);
       const int l = sl * 32 + lane;
       if (l < nloc) {
         const double p = fma(beta, spp[l], sz[l]);
@@ -599,11 +601,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
       block_sum<1, kResBlock>(v, sred);
       if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
     }
-    stamp(it, 2);
+    stamp(tl, it, 2);
     grid_barrier(bar, ++nbar * nb);
     double t1[1];
     all_sum_par<1>(partA, nb, sred, bcast, t1);
-    stamp(it, 3);
+    stamp(tl, it, 3);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
     if (lane == 0 && it + 1 < maxit)
@@ -638,16 +640,16 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
         b1 += ri * ri;
       }
     }
-    stamp(it, 6);
+    stamp(tl, it, 6);
     {
       double v[2] = {b0, b1};
       block_sum<2, kResBlock>(v, sred);
       if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
     }
-    stamp(it, 4);
+    stamp(tl, it, 4);
     grid_barrier(bar, ++nbar * nb);
     all_sum_par<2>(partB, nb, sred, bcast, t2);
-    stamp(it, 5);
+    stamp(tl, it, 5);
     rz_old = rz;
     rz = t2[0];
     rr = t2[1];
