@@ -247,8 +247,11 @@ def run_native(args):
         halo = HaloExchanger(plan, "cuda")
         from paper_2005_05899_b200.wall import wall_faces
         wall = wall_faces(sub, wall_g[l2g]) if wall_g is not None else None
+        # AB_FUSED_CG=1 forces the fused decomposed CG also on gloo (ranks sharing one GPU)
+        fused = True if os.environ.get("AB_FUSED_CG") == "1" else None
         s_ = FlowSolver(sub, FlowParams(**params), **{k: np.asarray(v)[l2g] for k, v in bc_g.items()},
-                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own, wall=wall)
+                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own, wall=wall,
+                        fused_cg=fused)
         s_.set_state(u_g[l2g], p_g[l2g])
         return s_, sub.n_elements
 

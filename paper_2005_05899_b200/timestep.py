@@ -117,7 +117,8 @@ class FlowSolver:
         # memory (ddcg.FusedDDSolver), validated once against the NCCL-driven
         # two-kernel solve; fused_cg=False keeps the latter
         self.ddcg = None
-        if halo is not None and fused_cg is not False and self._nccl(halo):
+        # (fused_cg=True also forces it on other backends, e.g. gloo ranks sharing one GPU in tests)
+        if halo is not None and (fused_cg is True or (fused_cg is None and self._nccl(halo))):
             self.ddcg = self._fused_solver(dm, pf, fused_cg)
         self.graph = None
         self.graph_key = None

@@ -28,7 +28,7 @@ def _mesh():
     return meshgen.c3_mesh(0.06)
 
 
-def _worker(rank, world, port, out_dir):
+def _worker(rank, world, port, out_dir, fused=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     torch.cuda.set_device(0)
@@ -43,8 +43,10 @@ def _worker(rank, world, port, out_dir):
     halo = HaloExchanger(plan, "cuda")
     bc = {k: np.asarray(v)[plan.l2g] for k, v in meshgen.channel_bcs(m).items()}
     u, p = meshgen.c2_initial(m.coords)
-    fs = FlowSolver(sub, FlowParams(1.0, 1e-2, 0.07), **bc, halo=halo, own=halo.own)
+    fs = FlowSolver(sub, FlowParams(1.0, 1e-2, 0.07), **bc, halo=halo, own=halo.own,
+                    fused_cg=True if fused else False)
     assert not fs.pcg.resident
+    assert (fs.ddcg is not None) == fused
     fs.set_state(u[plan.l2g], p[plan.l2g])
     for _ in range(2):
         fs.step(1e-3, cg_iters=25)
@@ -54,11 +56,15 @@ def _worker(rank, world, port, out_dir):
     dist.destroy_process_group()
 
 
-def test_two_ranks_one_gpu_match_single_domain_oracle(tmp_path):
+@pytest.mark.parametrize("fused", [False, True])
+def test_two_ranks_one_gpu_match_single_domain_oracle(tmp_path, fused):
+    """fused=True: the pressure solve of each rank is ab_cg_dd over CUDA-IPC
+    peer buffers (the multi-GPU path; the two processes' kernels time-slice
+    on the shared GPU), validated against the NCCL-driven form at setup."""
     from oracle import fem
     from paper_2005_05899_b200 import meshgen
     world = 2
-    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path), fused), nprocs=world, join=True)
     m = _mesh()
     u0, p0 = meshgen.c2_initial(m.coords)
     ora = fem.FlowOracle(m, 1.0, 1e-2, 0.07, **meshgen.channel_bcs(m))
