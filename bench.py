@@ -137,7 +137,8 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters: int = CG_ITERS):
+def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters: int = CG_ITERS,
+                     n_faces: int = 0):
     """Algorithmic bytes (and flops for K2) per launch, layout-independent
     (SURVEY §8(d) per-unit figures): int32 indices, fp64 values."""
     from paper_2005_05899_b200.meshgen import NODE_COUNT, RULE_KIND
@@ -161,6 +162,8 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
         return conn_bytes + 24 * N + 8 * N + 24 * N, 0
     if kernel == "K7_correct":
         return 24 * 3 * N + 8 * N + 16 * N + 24 * 3 * N, 6 * N
+    if kernel == "K8_wall":           # per face: 8 node ids, <= 8 coordinates, 4 exchange velocities, 4 rhs RMW
+        return n_faces * (32 + 8 * 24 + 4 * 24 + 4 * 48), 0
     if kernel == "K67_grad_correct":  # K6 + K7 without the G dp round trip
         return conn_bytes + 24 * N + 8 * N + 24 * N + 8 * N + 16 * N + 48 * N + 24 * N, 6 * N
     return 0, 0
@@ -188,6 +191,19 @@ def load_traffic():
     return {}
 
 
+def host_cpu() -> dict:
+    """CPU model and logical core count of the host."""
+    model = "unknown"
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"cpu_model": model, "nproc": os.cpu_count()}
+
+
 def cpu_baseline_sample(steps: int = 2):
     """Oracle port (numpy, 1 thread) on a bounded sample of the C2 workload."""
     from threadpoolctl import threadpool_limits
@@ -205,7 +221,7 @@ def cpu_baseline_sample(steps: int = 2):
         dt = time.perf_counter() - t0
     return {"value": m.n_elements * steps / dt / 1e6, "unit": "M element-steps/s", "cores": 1, "kind": "port",
             "sample": f"oracle/fem.py FlowOracle, jittered Kuhn TET04 24^3 cells ({m.n_elements} elements), "
-                      f"{steps} full steps (CG {CG_ITERS} it), numpy single thread"}
+                      f"{steps} full steps (CG {CG_ITERS} it), numpy single thread", **host_cpu()}
 
 
 def run_native(args):
@@ -347,7 +363,8 @@ def run_native(args):
     nnz = solver.L.nnz
     kern = {}
     for name, ts in per.items():
-        B, F = algorithmic_cost(name, counts, solver.n, nnz, args.cg_iters)
+        B, F = algorithmic_cost(name, counts, solver.n, nnz, args.cg_iters,
+                                n_faces=solver.wall.n_faces if solver.wall is not None else 0)
         avg = float(np.mean(ts))
         kern[name] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
                       "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,
@@ -454,7 +471,7 @@ def run_reference(args):
            "config": {"workload": "C2 sample (BASELINE configs[1] algorithm, bounded size)", "cg_iters": CG_ITERS,
                       "parallelism": f"{cores} CPU processes"},
            "cpu_baseline": {"value": round(value, 5), "unit": "M element-steps/s", "cores": cores, "kind": "port",
-                            "sample": sample},
+                            "sample": sample, **host_cpu()},
            "e2e": {"value": round(value, 5), "unit": "M element-steps/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
