@@ -181,6 +181,15 @@ def load_peaks():
     return 6650.0, "fallback"
 
 
+def load_fp64_peak():
+    """Measured FP64 FMA peak (tools/lab/fp64_peak.cu -> profiles/fp64_peak.json)."""
+    p = ROOT / "profiles" / "fp64_peak.json"
+    try:
+        return float(json.loads(p.read_text())["fp64_fma_tflops"]), "measured (tools/lab/fp64_peak.cu)"
+    except Exception:
+        return 37.0, "nominal"
+
+
 def load_traffic():
     p = ROOT / "profiles" / "ncu_traffic.json"
     if p.exists():
@@ -376,6 +385,14 @@ def run_native(args):
             "frac": round(kern[dom]["gbs"] / peak, 4), "peak_source": peak_kind,
             "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"],
             "alg_bytes_definition": "SURVEY.md §8(d) per-unit figure x units per launch"}
+    # the element assembly's binding roof is the FP64 pipe
+    roof_k2 = None
+    if "K2_momentum" in kern and kern["K2_momentum"]["gflops"]:
+        fp_peak, fp_src = load_fp64_peak()
+        ach = kern["K2_momentum"]["gflops"] / 1e3
+        roof_k2 = {"kernel": "K2_momentum", "bound": "fp64", "achieved": round(ach, 3), "peak": fp_peak,
+                   "unit": "TFLOP/s", "frac": round(ach / fp_peak, 4), "peak_source": fp_src,
+                   "flops_definition": "tet4: 664 fp64 flops per element (ncu-counted DFMA/DMUL/DADD), DESIGN.md §4"}
     if dom == "K5_cg_resident":
         # what this design must move at minimum per iteration: the stored SELL
         # entries (8 B value + 2 B local column, ab_cg_local), the z write and
@@ -400,6 +417,7 @@ def run_native(args):
                        cg_iters=args.cg_iters, dt=DT, physics=params, cuda_graph=graph,
                        scatter="windowed" if not args.no_windows else "atomics",
                        l2="flushed (512 MB write) between timed steps", parallelism=f"dd{ws}"),
+        "roofline_assembly": roof_k2,
         "e2e": {"value": round(n_elem_total * args.steps / (e2e_ms / 1e3) / 1e6, 3), "unit": "M element-steps/s",
                 "h2d_bytes_per_step": bytes_io, "d2h_bytes_per_step": bytes_io,
                 "api": "FlowSolver.step_host (pinned host u,p -> step -> host)"},
