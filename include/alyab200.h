@@ -228,7 +228,8 @@ typedef struct ab_cg_local {
    * 10*E0, values (8 B) first, then columns (2 B). */
   const unsigned char* packed;
   int32_t group;
-  int32_t pad_;
+  int32_t force_mode;        /* variant 0: 0 = best shared-memory plan; 1..4 = the plan of
+                                ab_cg_resident_local_fits (testing: every plan is exercised) */
   /* variant 2 (single-reduction form, k_cg_cg1): the CTAs owning each CTA's
    * ghost rows, nbr[nbr_ptr[b] .. nbr_ptr[b+1]) */
   const int32_t* nbr_ptr;

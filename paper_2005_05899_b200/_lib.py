@@ -50,7 +50,7 @@ class AbWall(C.Structure):
 class AbCgLocal(C.Structure):
     _fields_ = [("rows_per_cta", i64), ("n_cta", i32), ("max_ghost", i32), ("cols", vp), ("ghost_ptr", vp),
                 ("ghost", vp), ("perm", vp), ("prefetch_depth", i32),
-                ("variant", i32), ("packed", vp), ("group", i32), ("pad_", i32),
+                ("variant", i32), ("packed", vp), ("group", i32), ("force_mode", i32),
                 ("nbr_ptr", vp), ("nbr", vp)]
 
 

@@ -1511,8 +1511,15 @@ int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b
                     &sc,         &part,       &bar};
     e = cudaLaunchCooperativeKernel((const void*)k_cg_tmem, dim3(ncta), dim3(kTmThreads), args, smem, S(stream));
   } else {
-    const int mode = local_mode(rb, mg, &smem);
+    int mode = local_mode(rb, mg, &smem);
     if (mode == 0) return fail("ab_cg_resident_local: system does not fit in shared memory");
+    if (m->force_mode > 0) {  // a smaller plan than the best one (tests)
+      if (m->force_mode > mode) return fail("ab_cg_resident_local: forced plan does not fit");
+      mode = m->force_mode;
+      const size_t xsb = (size_t)(5 * rb + mg) * 8, xgb = (size_t)(4 * rb + mg) * 8;
+      const size_t tbb = (size_t)(rb / 32 + 1) * 8 + (size_t)mg * 4;
+      smem = (mode == 2 || mode == 4 ? xsb : xgb) + (mode >= 3 ? tbb : 0);
+    }
     const bool xs = mode == 2 || mode == 4, tb = mode >= 3;
     if (rb > (int64_t)kLocRowsPerThread * kResBlock) return fail("ab_cg_resident_local: too many rows per CTA");
 

@@ -264,7 +264,7 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1,
-                 tmem: bool = False, group: int = 0, single_reduction: bool = False):
+                 tmem: bool = False, group: int = 0, single_reduction: bool = False, force_mode: int = 0):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -306,6 +306,7 @@ class PCG:
                 m["perm"] = perm
                 m["struct"].perm = ptr(perm)
                 m["struct"].prefetch_depth = int(prefetch_depth)
+                m["struct"].force_mode = int(force_mode)
                 # tensor-memory solver when it fits (ab_cg_tmem_fits)
                 group = int(group) if group else max(1, -(-16384 // max(1, Ap.max_width * 256)))
                 m["tmem"] = bool(tmem and lib().ab_cg_tmem_fits(rb.value, m["max_ghost"], Ap.max_width, group) > 0)

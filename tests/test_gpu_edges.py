@@ -116,3 +116,24 @@ def test_zero_velocity_stays_at_rest():
         fs.step(1e-3, cg_iters=20, graph=True)
     torch.cuda.synchronize()
     assert float(fs.u.abs().max()) == 0.0 and float(fs.p.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("mode", [1, 2, 3, 4])
+def test_resident_local_every_shared_memory_plan(mode):
+    """k_cg_resident_local's four shared-memory plans (x in TMEM or global,
+    tables in shared or global memory) give the oracle's iterate."""
+    from paper_2005_05899_b200.device import DeviceMesh
+    from paper_2005_05899_b200.solver import PCG, assemble_laplacian
+    m = meshgen.box_tets(12, 9, 7, jitter=0.2, seed=6)
+    fixed = meshgen.boundary_nodes(m)
+    L = fem.laplacian(m, fixed)
+    b = np.random.default_rng(8).standard_normal(m.n_nodes)
+    b[fixed] = 0.0
+    dm = DeviceMesh(m)
+    A = assemble_laplacian(dm, torch.from_numpy(fixed))
+    pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), order=dm.node_order(), force_mode=mode)
+    x, _ = pcg.solve(torch.from_numpy(b).cuda(), 9, zero_b=False)
+    xr, _, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 9)
+    assert rel_l2(x.cpu().numpy(), xr) <= 1e-10
+    x2, it = pcg.solve(torch.from_numpy(b).cuda(), 2000, tol=1e-11, zero_b=False)
+    assert pcg.residual() <= 1e-11
