@@ -31,7 +31,9 @@ def __getattr__(name):
                       "hilbert_keys_batch", "partition_chunked", "project_to_bins", "split_1d", "store_partition",
                       "load_partition", "sfc_partition"),
         "balance": ("BalanceMetrics", "Phase", "TimingSample", "compute_metrics", "gpu_timer",
-                    "throughput_coefficients", "distributed_timer"),
+                    "throughput_coefficients", "distributed_timer", "RegressionMode", "CorrectionState",
+                    "RegressionFit", "IterationRecord", "BalanceReport", "observe", "fit", "update_coefficients",
+                    "rank_model_coefficients", "run_balancing_loop", "DELTA_MIN", "BETA_MIN", "DEFAULT_WLR_GROWTH"),
         "solver": ("SellMatrix", "assemble_laplacian", "pcg_solve"),
         "timestep": ("FlowParams", "FlowSolver", "time_step", "run"),
         "ops": ("assemble_momentum", "assemble_divergence", "assemble_gradient"),

@@ -14,6 +14,13 @@ Fixtures:
   reference_sfc.npz    hilbert_keys_batch / hilbert_decode / project_to_bins /
                        split_1d / partition_chunked outputs (reference sfc.py)
   reference_balance.json  compute_metrics examples (reference balance.py:82-92)
+  reference_dlb.json   run_balancing_loop (SLR/WLR regression DLB, reference
+                       balance.py:95-346) on the 10k fixture mesh with
+                       noise-free affine per-rank cost models
+                       t_k = W_k / theta_k + c_k (the reference's own
+                       simulate_times for noise_sigma = 0, coexec.py:69-98)
+
+    python tests/golden/make_golden.py dlb   # only reference_dlb.json
 """
 
 from __future__ import annotations
@@ -165,7 +172,46 @@ def balance_fixture():
     return ex
 
 
+# (name, theta per rank, fixed cost per rank, mode, tol, max_iters)
+DLB_CASES = (
+    ("hetero6_wlr", [1, 1, 1, 1, 5, 5], [0.0] * 6, "wlr", 0.02, 20),
+    ("affine4_slr", [1, 2, 1, 3], [0.01, 0.0, 0.02, 0.005], "slr", 0.01, 15),
+    ("homog8_wlr", [1.0] * 8, [0.0] * 8, "wlr", 0.02, 5),
+    # the bundled hetero_s20 plan (2 nodes x (16 cores + 2 GPU ranks at
+    # theta 20)): SURVEY F8-ii, where the regression plateaus then diverges
+    ("hetero_s20_wlr", ([1.0] * 16 + [20.0] * 2) * 2, [0.0] * 36, "wlr", 0.02, 30),
+)
+
+
+def dlb_fixture():
+    m = load_fixture_mesh()
+    cfg = rs.SfcConfig(level=8)
+    seq = rs.project_to_bins(m, cfg)
+    cases = []
+    for name, theta, cost, mode, tol, iters in DLB_CASES:
+        th, c = np.array(theta, dtype=float), np.array(cost, dtype=float)
+
+        def timer(part, th=th, c=c):
+            return rb.TimingSample(iteration=0, times=part.subdomain_weights / th + c)
+
+        rep = rb.run_balancing_loop(m, cfg, len(th), timer, mode=rb.RegressionMode(mode), tol=tol,
+                                    max_iters=iters, bins=seq)
+        cases.append({"name": name, "theta": theta, "cost": cost, "mode": mode, "tol": tol, "max_iters": iters,
+                      "converged": rep.converged,
+                      "lambda": [r.lam.tolist() for r in rep.iterations],
+                      "times": [r.times.tolist() for r in rep.iterations],
+                      "subdomain_weights": [r.partition.subdomain_weights.tolist() for r in rep.iterations],
+                      "imbalance": [r.metrics.imbalance for r in rep.iterations],
+                      "json": rep.to_json_dict(final_partition_ref="part.txt"),
+                      "csv": rep.convergence_csv() if len(th) <= 8 else None})
+    return {"reference_version": coexbal.__version__, "level": 8, "cases": cases}
+
+
 def main():
+    if sys.argv[1:] == ["dlb"]:
+        (HERE / "reference_dlb.json").write_text(json.dumps(dlb_fixture()))
+        print("wrote", HERE / "reference_dlb.json")
+        return
     out: dict = {}
     mass_fixture("mixed", connected_mixed_mesh(), out)
     mass_fixture("soup", rm.generate_synthetic_full_mesh(300, hex_fraction=0.3, seed=3), out)
@@ -175,6 +221,7 @@ def main():
     np.savez_compressed(HERE / "reference_sfc.npz", **out)
     (HERE / "reference_balance.json").write_text(json.dumps(
         {"reference_version": coexbal.__version__, "examples": balance_fixture()}, indent=1))
+    (HERE / "reference_dlb.json").write_text(json.dumps(dlb_fixture()))
     print("wrote fixtures to", HERE)
 
 
