@@ -245,7 +245,9 @@ int ab_debug_timeline(int64_t* buf);
 int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost);
 /* ab_cg_resident with the z gathers served from shared memory: each CTA
  * fetches its ghost z values once per iteration, the SpMV reads z through
- * the 16-bit local columns.  Same iterates as ab_cg_resident. */
+ * the 16-bit local columns.  Same iterates as ab_cg_resident.  `part` >=
+ * 8 * n_cta + 20 * ceil4(n_cta) doubles (grid-barrier counter at 5 * n_cta,
+ * replicated partial tables from 8 * n_cta). */
 /* > 0 (ring slots) when the tensor-memory solver (variant 1) fits: vectors
  * x, r, p, q, D^-1 in TMEM, matrix slices streamed by a producer warp into
  * a shared-memory ring with bulk asynchronous copies. */

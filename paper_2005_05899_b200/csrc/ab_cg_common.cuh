@@ -61,6 +61,50 @@ __device__ __forceinline__ double sell_row_dot_smem(const int64_t* tsp, const ui
   return acc;
 }
 
+// Replicated per-CTA partials (resident solvers): the NV values of CTA b are
+// written to kRep copies of a [NV][nbp] table (nbp = nb rounded up to 4),
+// and CTA b reads copy b % kRep with 16-byte loads, so each 32-byte sector is
+// requested by nb / kRep CTAs once instead of by every CTA four times.  The
+// sum is a fixed tree (per-thread 4, warp xor tree, two warps per value):
+// identical in every CTA, deterministic.  Needs nb <= 256.
+constexpr int kRep = 4;
+__host__ __device__ inline int rep_nbp(int nb) { return (nb + 3) & ~3; }
+
+template <int NV>
+__device__ __forceinline__ void put_partial_rep(double* tab, int nb, const double (&v)[NV]) {
+  const int nbp = rep_nbp(nb);
+#pragma unroll
+  for (int r = 0; r < kRep; ++r)
+#pragma unroll
+    for (int k = 0; k < NV; ++k) tab[((size_t)r * NV + k) * nbp + blockIdx.x] = v[k];
+}
+
+template <int NV>
+__device__ __forceinline__ void all_sum_rep(const double* tab, int nb, double* srep /* >= 2 * NV */,
+                                            double (&out)[NV]) {
+  const int nbp = rep_nbp(nb);
+  const double* rp = tab + (size_t)(blockIdx.x % kRep) * NV * nbp;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (warp < 2 * NV) {
+    const int k = warp >> 1, c = ((warp & 1) << 5) + lane, i = 4 * c;
+    double s = 0.0;
+    if (i < nb) {
+      const double2 a = __ldcg(reinterpret_cast<const double2*>(rp + (size_t)k * nbp + i));
+      const double2 b = __ldcg(reinterpret_cast<const double2*>(rp + (size_t)k * nbp + i + 2));
+      s = a.x;
+      if (i + 1 < nb) s += a.y;
+      if (i + 2 < nb) s += b.x;
+      if (i + 3 < nb) s += b.y;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) srep[warp] = s;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) out[k] = srep[2 * k] + srep[2 * k + 1];
+}
+
 // Ordered sum of nb (<= blockDim) per-CTA partials, all loads in flight at
 // once (one L2 round trip), fixed reduction tree: identical in every CTA.
 template <int NV>

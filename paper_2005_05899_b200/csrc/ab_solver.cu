@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   int64_t* const tl = g_timeline;
   extern __shared__ double smem[];
   __shared__ double sred[2 * (kResBlock / 32)];
-  __shared__ double bcast[4];
+  __shared__ double srep[4];
   __shared__ uint32_t s_taddr;
   const int nb = gridDim.x;
   const int64_t RB = rows_per_cta;
@@ -457,9 +457,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   // TB: the CTA's slice pointers and ghost ids copied to shared memory
   int64_t* tsp_s = reinterpret_cast<int64_t*>(sz + RB + max_ghost);
   int32_t* tg_s = reinterpret_cast<int32_t*>(tsp_s + RB / 32 + 1);
-  double* partA = part;
-  double* partB = part + nb;
-  double* partI = part + 3 * (size_t)nb;
+  // replicated partial tables (all_sum_rep): A 1 value, B and I 2 values;
+  // behind the barrier counter at part + 5 nb (host: ab_cg_resident_local)
+  double* partA = part + 8 * (size_t)nb;
+  double* partB = partA + (size_t)kRep * rep_nbp(nb);
+  double* partI = partA + (size_t)3 * kRep * rep_nbp(nb);
   unsigned nbar = 0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nsl = (nloc + 31) >> 5;
@@ -534,11 +536,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
   {
     double v[2] = {a0, a1};
     block_sum<2, kResBlock>(v, sred);
-    if (threadIdx.x == 0) { partI[blockIdx.x] = v[0]; partI[nb + blockIdx.x] = v[1]; }
+    if (threadIdx.x == 0) put_partial_rep<2>(partI, nb, v);
   }
   grid_barrier(bar, ++nbar * nb);
   double t2[2];
-  all_sum_par<2>(partI, nb, sred, bcast, t2);
+  all_sum_rep<2>(partI, nb, srep, t2);
   double rz = t2[0], rr = t2[1];
   const double bb = rr;
   double rz_old = 0.0;
@@ -599,12 +601,12 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     {
       double v[1] = {pq};
       block_sum<1, kResBlock>(v, sred);
-      if (threadIdx.x == 0) partA[blockIdx.x] = v[0];
+      if (threadIdx.x == 0) put_partial_rep<1>(partA, nb, v);
     }
     stamp(tl, it, 2);
     grid_barrier(bar, ++nbar * nb);
     double t1[1];
-    all_sum_par<1>(partA, nb, sred, bcast, t1);
+    all_sum_rep<1>(partA, nb, srep, t1);
     stamp(tl, it, 3);
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- phase B: x += alpha p, r -= alpha q, z = D^-1 r
@@ -644,11 +646,11 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_resident_local(
     {
       double v[2] = {b0, b1};
       block_sum<2, kResBlock>(v, sred);
-      if (threadIdx.x == 0) { partB[blockIdx.x] = v[0]; partB[nb + blockIdx.x] = v[1]; }
+      if (threadIdx.x == 0) put_partial_rep<2>(partB, nb, v);
     }
     stamp(tl, it, 4);
     grid_barrier(bar, ++nbar * nb);
-    all_sum_par<2>(partB, nb, sred, bcast, t2);
+    all_sum_rep<2>(partB, nb, srep, t2);
     stamp(tl, it, 5);
     rz_old = rz;
     rz = t2[0];

@@ -281,7 +281,9 @@ class PCG:
         n_cta = C.c_int32(0)
         rb = C.c_int64(0)
         fits = lib().ab_cg_resident_fits(n, C.byref(rb), C.byref(n_cta))
-        self.part = torch.zeros(max(2 * (nb + ng), 12 * n_cta.value + 1) + 8, dtype=torch.float64, device=dev)
+        # (+ 5 replicated [4][nb] partial tables of the resident solver, all_sum_rep)
+        self.part = torch.zeros(max(2 * (nb + ng), 12 * n_cta.value + 1, 8 * n_cta.value + 20 * ((n_cta.value + 3) // 4 * 4)) + 8,
+                                dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
         self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)

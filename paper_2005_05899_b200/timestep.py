@@ -121,6 +121,7 @@ class FlowSolver:
         if halo is not None and (fused_cg is True or (fused_cg is None and self._nccl(halo))):
             self.ddcg = self._fused_solver(dm, pf, fused_cg)
         self.graph = None
+        self._side = None  # step_host: G p^n while u uploads
         self.graph_key = None
         self.last_cg_iters = 0
         self.timeline = None  # list of (name, start, end) CUDA events when profiling
@@ -286,13 +287,20 @@ class FlowSolver:
     def step_host(self, u_host: torch.Tensor, p_host: torch.Tensor, dt: float, cg_iters: int = 50,
                   graph: bool = True):
         """End-to-end call with HOST buffers (pinned for async copies): upload
-        (u, p), advance one step, download (u, p) in place."""
-        self.U0[:, :3].copy_(u_host, non_blocking=True)
+        (u, p), advance one step, download (u, p) in place.  p goes first and
+        G p^n is assembled on a side stream while u is still uploading."""
+        main = torch.cuda.current_stream()
+        if self._side is None:
+            self._side = torch.cuda.Stream()
         self.P.copy_(p_host, non_blocking=True)
-        self.GP.zero_()
-        self._grad(self.P, self.GP)
-        if self.halo is not None:
-            self.halo.sum_(self.GP, 3, 4)
+        self._side.wait_stream(main)
+        with torch.cuda.stream(self._side):
+            self.GP.zero_()
+            self._grad(self.P, self.GP)
+            if self.halo is not None:
+                self.halo.sum_(self.GP, 3, 4)
+        self.U0[:, :3].copy_(u_host, non_blocking=True)
+        main.wait_stream(self._side)
         self.step(dt, cg_iters, graph=graph)
         u_host.copy_(self.U0[:, :3], non_blocking=True)
         p_host.copy_(self.P, non_blocking=True)

@@ -296,3 +296,29 @@ def test_halo_pack_unpack_kernels():
     want = f.copy()
     np.add.at(want[:, :3], idx, f[idx, :3])
     assert np.allclose(ft.cpu().numpy(), want, rtol=0, atol=1e-15)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_step_host_matches_oracle(graph):
+    """The end-to-end entry point (pinned host u, p in; step; host u, p out;
+    G p^n assembled on a side stream while u uploads) against the oracle over
+    3 steps, with the host state perturbed between steps so the uploaded p
+    differs from the device's."""
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+    m = meshgen.box_tets(7, 6, 5, jitter=0.2, seed=5)
+    u, p = _field(m, seed=4)
+    bc = dict(p_fixed=meshgen.boundary_nodes(m))
+    params = dict(rho=1.0, mu=1e-2, c_vreman=0.07)
+    ora = fem.FlowOracle(m, **params, **bc)
+    fs = FlowSolver(m, FlowParams(**params), **bc)
+    fs.set_state(u, p)
+    u_h = torch.from_numpy(np.ascontiguousarray(u)).pin_memory()
+    p_h = torch.from_numpy(np.ascontiguousarray(p)).pin_memory()
+    for k in range(3):
+        st = ora.init_state(u_h.numpy().copy(), p_h.numpy().copy())
+        st = ora.step(st, 1e-3, cg_iters=30)
+        fs.step_host(u_h, p_h, 1e-3, cg_iters=30, graph=graph)
+        torch.cuda.synchronize()
+        assert rel_l2(u_h.numpy(), st["u"]) <= TOL_STATE, k
+        assert rel_l2(p_h.numpy(), st["p"]) <= TOL_STATE, k
+        p_h += 0.01 * (k + 1)  # the next upload is not the device's p
