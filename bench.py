@@ -435,6 +435,12 @@ def run_native(args):
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             result["cpu_baseline"] = cpu_baseline_sample()
+            # the paper's co-execution model with this box's measured rates (context only: no CPU path runs)
+            from paper_2005_05899_b200 import coexec
+            cb = result["cpu_baseline"]
+            rep = coexec.report(coexec.measured_params(result["value"], cb["value"], n_core=cb.get("nproc") or 1))
+            result["coexec_model"] = {k: (round(v, 6) if isinstance(v, float) else v) for k, v in rep.items()}
+            result["coexec_model"]["inputs"] = "speedup = value / cpu_baseline.value (one core); ratio = 1 GPU / nproc"
         except Exception as exc:  # pragma: no cover
             result["cpu_baseline"] = {"error": repr(exc)}
     if rank == 0:

@@ -111,6 +111,16 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
                    const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, const int32_t* desc,
                    int32_t wmax);
 
+/* ---- Partition file I/O (host; reference sfc.py:385-417 `part 1` body) ----
+ * ab_format_partition: lines "i parts[i]\n" for i = first .. first+n-1 into
+ * buf (capacity cap); returns bytes written or < 0.  ab_parse_partition:
+ * parts[id] = subdomain for every "id subdomain" line of buf (the file after
+ * its header line); every id in [0, n) exactly once (seen: n bytes scratch);
+ * returns lines parsed or < 0 (malformed, out of range, duplicate).  Replace
+ * the per-element Python loops of store_partition / load_partition. */
+int64_t ab_format_partition(const int32_t* parts, int64_t first, int64_t n, char* buf, int64_t cap);
+int64_t ab_parse_partition(const char* buf, int64_t len, int32_t* parts, int64_t n, uint8_t* seen);
+
 /* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
  * New entry point; rhs4 accumulated. */
 int ab_momentum_rhs(const ab_mesh* mesh, const ab_phys* phys, const double* u4, double* rhs4,

@@ -29,7 +29,7 @@ def __getattr__(name):
                      "lumped_mass"),
         "partition": ("BinSequence", "Partition", "SfcConfig", "hilbert_decode", "hilbert_key",
                       "hilbert_keys_batch", "partition_chunked", "project_to_bins", "split_1d", "store_partition",
-                      "load_partition", "sfc_partition"),
+                      "load_partition", "sfc_partition", "store_partition_parts", "load_partition_parts"),
         "balance": ("BalanceMetrics", "Phase", "TimingSample", "compute_metrics", "gpu_timer",
                     "throughput_coefficients", "distributed_timer", "RegressionMode", "CorrectionState",
                     "RegressionFit", "IterationRecord", "BalanceReport", "observe", "fit", "update_coefficients",
@@ -37,6 +37,7 @@ def __getattr__(name):
         "solver": ("SellMatrix", "assemble_laplacian", "pcg_solve"),
         "timestep": ("FlowParams", "FlowSolver", "time_step", "run"),
         "ops": ("assemble_momentum", "assemble_divergence", "assemble_gradient"),
+        "coexec": ("EfficiencyParams", "eff_gpu", "eff_core", "eff_coex1", "eff_coex2", "predicted_time_reduction"),
     }
     import importlib
     for mod, names in lazy.items():

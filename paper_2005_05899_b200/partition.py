@@ -391,3 +391,61 @@ def sfc_partition(arrays, n_parts: int, coeffs=None, level: int = 8):
 def _minmax_points(cent: torch.Tensor) -> np.ndarray:
     """Two points carrying the exact per-axis min and max (box computation)."""
     return torch.stack([cent.min(dim=0).values, cent.max(dim=0).values]).cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# Array-native `part 1` I/O (SURVEY.md §8(f) row f-2): the same files as
+# store_partition / load_partition (reference sfc.py:385-417) from / into a
+# dense per-element subdomain array, formatted and parsed by the native
+# library (ab_format_partition / ab_parse_partition), for decompositions too
+# large for an assignment dict.
+# ---------------------------------------------------------------------------
+
+def _host_io(name, *args) -> int:
+    from ._lib import lib
+    rc = int(getattr(lib(), name)(*args))
+    if rc < 0:
+        raise ValueError(f"{name}: {lib().ab_last_error().decode(errors='replace')}")
+    return rc
+
+
+def store_partition_parts(parts, n_parts: int, cut_bins, subdomain_weights, path, chunk: int = 1 << 22) -> None:
+    """``parts[i]`` = subdomain (1..P) of element i (the output of
+    :func:`sfc_partition`); writes byte-identical files to
+    ``store_partition(Partition(...))``."""
+    a = np.ascontiguousarray(np.asarray(parts), dtype=np.int32)
+    if a.ndim != 1:
+        raise ValueError("parts must be a 1D array")
+    if a.size and (int(a.min()) < 1 or int(a.max()) > n_parts):
+        raise ValueError(f"subdomain ids must lie in 1..{n_parts}")
+    buf = np.empty(chunk * 24 + 64, dtype=np.uint8)
+    with open(path, "wb") as f:
+        f.write(f"part 1 {n_parts} {a.size}\n".encode())
+        for s in range(0, a.size, chunk):
+            n = min(chunk, a.size - s)
+            w = _host_io("ab_format_partition", a[s:].ctypes.data, s, n, buf.ctypes.data, buf.size)
+            f.write(buf[:w].tobytes())
+    side = {"cut_bins": [int(c) for c in cut_bins], "subdomain_weights": [float(x) for x in subdomain_weights]}
+    Path(str(path) + ".json").write_text(json.dumps(side), encoding="utf-8")
+
+
+def load_partition_parts(path):
+    """(parts int32 [E], n_parts, cut_bins, subdomain_weights) of a `part 1`
+    file whose element ids are 0..E-1; the same validation as
+    :func:`load_partition` (header, count, no duplicates)."""
+    raw = Path(path).read_bytes()
+    nl = raw.find(b"\n")
+    head = (raw if nl < 0 else raw[:nl]).decode("utf-8").split()
+    if len(head) != 4 or head[0] != "part" or head[1] != "1":
+        raise ValueError(f"{path}:1: bad partition header {head!r}")
+    n_parts, n_elem = int(head[2]), int(head[3])
+    body = np.frombuffer(raw, dtype=np.uint8, offset=nl + 1 if nl >= 0 else len(raw))
+    parts = np.zeros(n_elem, dtype=np.int32)
+    seen = np.empty(max(n_elem, 1), dtype=np.uint8)
+    got = _host_io("ab_parse_partition", body.ctypes.data if body.size else None, body.size, parts.ctypes.data,
+                   n_elem, seen.ctypes.data)
+    if got != n_elem:
+        raise ValueError(f"{path}: expected {n_elem} assignments, got {got}")
+    side = json.loads(Path(str(path) + ".json").read_text(encoding="utf-8"))
+    return (parts, n_parts, np.array(side["cut_bins"], dtype=np.int64),
+            np.array(side["subdomain_weights"], dtype=np.float64))

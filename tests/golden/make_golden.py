@@ -20,7 +20,11 @@ Fixtures:
                        t_k = W_k / theta_k + c_k (the reference's own
                        simulate_times for noise_sigma = 0, coexec.py:69-98)
 
-    python tests/golden/make_golden.py dlb   # only reference_dlb.json
+  reference_coexec.json  closed-form co-execution efficiencies (reference
+                       coexec.py:258-323)
+
+    python tests/golden/make_golden.py dlb      # only reference_dlb.json
+    python tests/golden/make_golden.py coexec   # only reference_coexec.json
 """
 
 from __future__ import annotations
@@ -207,7 +211,30 @@ def dlb_fixture():
     return {"reference_version": coexbal.__version__, "level": 8, "cases": cases}
 
 
+def coexec_fixture():
+    import warnings
+    from coexbal import coexec as rc
+    rows = []
+    for s_, nc, ng in ((20.0, 40, 4), (1.5, 16, 2), (2.0, 8, 1), (350.0, 16, 1), (1e4, 112, 8), (3.0, 1, 0)):
+        p = rc.EfficiencyParams.from_counts(nc, ng, s_)
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            row = {"speedup": s_, "n_core": nc, "n_gpu": ng, "eff_core": rc.eff_core(p), "eff_gpu": rc.eff_gpu(p),
+                   "eff_coex1": rc.eff_coex1(p), "eff_coex2": rc.eff_coex2(p)}
+            for c in (1, 2):
+                try:
+                    row[f"red{c}"] = rc.predicted_time_reduction(p, c)
+                except ValueError:
+                    row[f"red{c}"] = None
+        rows.append(row)
+    return {"reference_version": coexbal.__version__, "rows": rows}
+
+
 def main():
+    if sys.argv[1:] == ["coexec"]:
+        (HERE / "reference_coexec.json").write_text(json.dumps(coexec_fixture(), indent=1))
+        print("wrote", HERE / "reference_coexec.json")
+        return
     if sys.argv[1:] == ["dlb"]:
         (HERE / "reference_dlb.json").write_text(json.dumps(dlb_fixture()))
         print("wrote", HERE / "reference_dlb.json")
@@ -222,6 +249,7 @@ def main():
     (HERE / "reference_balance.json").write_text(json.dumps(
         {"reference_version": coexbal.__version__, "examples": balance_fixture()}, indent=1))
     (HERE / "reference_dlb.json").write_text(json.dumps(dlb_fixture()))
+    (HERE / "reference_coexec.json").write_text(json.dumps(coexec_fixture(), indent=1))
     print("wrote fixtures to", HERE)
 
 

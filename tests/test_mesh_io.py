@@ -117,3 +117,37 @@ def test_boundary_layer_mesh_is_conforming():
 def test_c2_sizes():
     m = meshgen.box_tets(88, 88, 88)
     assert m.n_elements == 4_088_832 and m.n_nodes == 704_969
+
+
+def test_partition_array_io_matches_dict_io(tmp_path):
+    """store_partition_parts / load_partition_parts (native formatter and
+    parser) write and read the same `part 1` files as the dict-based
+    store_partition / load_partition (reference sfc.py:385-417)."""
+    from paper_2005_05899_b200.partition import (Partition, load_partition, load_partition_parts,
+                                                 store_partition, store_partition_parts)
+    rng = np.random.default_rng(7)
+    parts = rng.integers(1, 6, size=12345).astype(np.int32)
+    cuts = np.array([10, 20, 30, 40], dtype=np.int64)
+    sub = np.array([1.5, 2.0, 2.5, 3.0, 4.0])
+    ref = Partition(n_parts=5, cut_bins=cuts, assignment={i: int(p) for i, p in enumerate(parts)},
+                    subdomain_weights=sub)
+    store_partition(ref, tmp_path / "a.part")
+    store_partition_parts(parts, 5, cuts, sub, tmp_path / "b.part", chunk=1000)
+    assert (tmp_path / "a.part").read_bytes() == (tmp_path / "b.part").read_bytes()
+    assert (tmp_path / "a.part.json").read_text() == (tmp_path / "b.part.json").read_text()
+    got, n_parts, c2, s2 = load_partition_parts(tmp_path / "a.part")
+    assert n_parts == 5 and np.array_equal(got, parts) and np.array_equal(c2, cuts) and np.array_equal(s2, sub)
+    assert load_partition(tmp_path / "b.part") == ref
+    # malformed / inconsistent files are rejected like the dict reader does
+    (tmp_path / "c.part").write_text("part 1 2 3\n0 1\n1 2\n1 2\n")
+    (tmp_path / "c.part.json").write_text('{"cut_bins": [0], "subdomain_weights": [1.0, 1.0]}')
+    with pytest.raises(ValueError, match="duplicate"):
+        load_partition_parts(tmp_path / "c.part")
+    (tmp_path / "c.part").write_text("part 1 2 3\n0 1\n1 2\n")
+    with pytest.raises(ValueError, match="expected 3"):
+        load_partition_parts(tmp_path / "c.part")
+    (tmp_path / "c.part").write_text("part 2 2 3\n")
+    with pytest.raises(ValueError, match="header"):
+        load_partition_parts(tmp_path / "c.part")
+    with pytest.raises(ValueError):
+        store_partition_parts(np.array([0, 1]), 2, [0], [1.0, 1.0], tmp_path / "d.part")
