@@ -121,6 +121,14 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
 int64_t ab_format_partition(const int32_t* parts, int64_t first, int64_t n, char* buf, int64_t cap);
 int64_t ab_parse_partition(const char* buf, int64_t len, int32_t* parts, int64_t n, uint8_t* seen);
 
+/* Vreman filter width of category k: delta2[e] = V_e^(2/3) (device, E_k
+ * doubles; geometry only, computed once).  ab_set_filter_width registers it
+ * for the category with connectivity `conn` and n_elem elements (delta2 NULL
+ * clears); K2 then reads it
+ * instead of evaluating the cube root per element and stage (same values). */
+int ab_filter_width(const ab_mesh* m, int32_t k, double* delta2, void* stream);
+int ab_set_filter_width(const int32_t* conn, int64_t n_elem, const double* delta2);
+
 /* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
  * New entry point; rhs4 accumulated. */
 int ab_momentum_rhs(const ab_mesh* mesh, const ab_phys* phys, const double* u4, double* rhs4,

@@ -29,6 +29,9 @@ struct CatP {
   int64_t n;
   double L0, L1, L2;  // periods (0 = none)
   int periodic;
+  // Vreman filter width squared per element, Delta^2 = V_e^(2/3) (geometry
+  // only: computed once by k_filter_width, ab_set_filter_width); nullable
+  const double* __restrict__ delta2;
 };
 
 // Node windows of a category (windowed scatter), see DESIGN.md §4.2.
@@ -395,9 +398,10 @@ __global__ void k_mass(CatP c, double* __restrict__ ae, double* __restrict__ jde
 // ---------------------------------------------------------------------------
 // K2: momentum RHS  R_a -= int rho N_a [2 eps(u) u + div(u) u] + 2 (mu+mu_t) eps : grad N_a
 // ---------------------------------------------------------------------------
+// d2: the element's precomputed Delta^2 (< 0: computed here from V_e)
 template <int R, int NN, class Emit>
 __device__ __forceinline__ void momentum_element(const ab_phys ph, const double (&x)[NN][3], const double (&u)[NN][3],
-                                                 Emit emit) {
+                                                 double d2, Emit emit) {
   constexpr int NG = RuleT<R>::NG;
   if constexpr (RuleT<R>::TET) {
     // Affine element: geometry, grad u and mu_t are constant, and the
@@ -424,8 +428,11 @@ __device__ __forceinline__ void momentum_element(const ab_phys ph, const double 
     const double div = G[0][0] + G[1][1] + G[2][2];
     double mu_eff = ph.mu;
     if (ph.c_vreman > 0.0) {
-      const double d = cbrt(vol);
-      mu_eff += vreman(G, d * d, ph.rho, ph.c_vreman);
+      if (d2 < 0.0) {
+        const double d = cbrt(vol);
+        d2 = d * d;
+      }
+      mu_eff += vreman(G, d2, ph.rho, ph.c_vreman);
     }
     // Symmetric A' = rho |J| (G + G^T + div I) and sigma = 2 mu_eff eps V,
     // 6 unique entries each (index k: 00 11 22 01 02 12).
@@ -474,8 +481,8 @@ __device__ __forceinline__ void momentum_element(const ab_phys ph, const double 
     double r[NN][3];
 #pragma unroll
     for (int a = 0; a < NN; ++a) r[a][0] = r[a][1] = r[a][2] = 0.0;
-    double delta2 = 0.0;
-    if (ph.c_vreman > 0.0) {
+    double delta2 = d2;
+    if (ph.c_vreman > 0.0 && d2 < 0.0) {
       double vol = 0.0;
 #pragma unroll
       for (int g = 0; g < NG; ++g) vol += abs_det<R, NN>(x, g) * c_w[R][g];
@@ -545,7 +552,7 @@ __global__ void __launch_bounds__(BLOCK) k_momentum(CatP c, ab_phys ph, const do
     if constexpr (WIN) {
       win_element<NN, 6>(w, cx, sm, x, u);
       unwrap<NN>(c, x);
-      momentum_element<R, NN>(ph, x, u, [&](int a, const double (&v)[3]) {
+      momentum_element<R, NN>(ph, x, u, c.delta2 ? __ldg(c.delta2 + e) : -1.0, [&](int a, const double (&v)[3]) {
         r[a][0] = v[0]; r[a][1] = v[1]; r[a][2] = v[2];
       });
     } else {
@@ -553,7 +560,7 @@ __global__ void __launch_bounds__(BLOCK) k_momentum(CatP c, ab_phys ph, const do
       load_conn<NN>(c.conn, e, nd);
       load_coords<NN>(c, nd, x);
       load_vec<NN>(u4, nd, u);
-      momentum_element<R, NN>(ph, x, u, [&](int a, const double (&v)[3]) {
+      momentum_element<R, NN>(ph, x, u, c.delta2 ? __ldg(c.delta2 + e) : -1.0, [&](int a, const double (&v)[3]) {
 #pragma unroll
         for (int i = 0; i < 3; ++i) red_add(rhs4 + 4 * (int64_t)nd[a] + i, v[i]);
       });
@@ -901,6 +908,12 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     double* nodes_nxt = nodes0 + (size_t)((it + 1) & 1) * NV * wmax;
     const int64_t b2 = b + 2 * stride, b3 = b + 3 * stride;
     const int4 d3 = b3 < n_blocks ? __ldg(w.desc + b3) : d0;  // lands during this block
+    // precomputed filter width of this thread's element: in flight across the waits below
+    double d2e = -1.0;
+    if constexpr (OP == OP_MOMENTUM) {
+      const int64_t ee = b * BLOCK + threadIdx.x;
+      if (c.delta2 && ee < c.n) d2e = __ldg(c.delta2 + ee);
+    }
     // A: node data of the next block
     if (b + stride < n_blocks) {
       mbar_wait_parity(&bars[mq1], (uint32_t)(((it + 1) / 3) & 1));
@@ -945,7 +958,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       }
       unwrap<NN>(c, x);
       if constexpr (OP == OP_MOMENTUM) {
-        momentum_element<R, NN>(ph, x, fv, [&](int a, const double (&v)[3]) {
+        momentum_element<R, NN>(ph, x, fv, d2e, [&](int a, const double (&v)[3]) {
 #pragma unroll
           for (int k = 0; k < 3; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = v[k];
         });
@@ -1032,6 +1045,37 @@ static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double s
   kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w, ph, scale, f, out, n_blocks);
   return check_launch("k_pipe");
 }
+// ---------------------------------------------------------------------------
+// Vreman filter width Delta^2 = V_e^(2/3) per element (setup): the same
+// operations as momentum_element's on-the-fly value, so K2 gives identical
+// results with or without it, and K2 skips the fp64 cbrt.
+// ---------------------------------------------------------------------------
+template <int R>
+__global__ void k_filter_width(CatP c, double* __restrict__ out) {
+  constexpr int NN = RuleT<R>::NN, NG = RuleT<R>::NG;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= c.n) return;
+  int nd[NN];
+  load_conn<NN>(c.conn, e, nd);
+  double x[NN][3];
+  load_coords<NN>(c, nd, x);
+  unwrap<NN>(c, x);
+  double vol = 0.0;
+  if constexpr (RuleT<R>::TET) {
+    double dNdx[NN][3];
+    const double adet = fabs(shape_grads<R, NN>(x, 0, dNdx));
+    double wsum = 0.0;
+#pragma unroll
+    for (int g = 0; g < NG; ++g) wsum += c_w[R][g];
+    vol = adet * wsum;
+  } else {
+#pragma unroll
+    for (int g = 0; g < NG; ++g) vol += abs_det<R, NN>(x, g) * c_w[R][g];
+  }
+  const double d = cbrt(vol);
+  out[e] = d * d;
+}
+
 // ---------------------------------------------------------------------------
 // Laplacian values into a CSR pattern (setup)
 // ---------------------------------------------------------------------------
@@ -1162,6 +1206,16 @@ __global__ void k_centroids(CatP c, double* __restrict__ out) {
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
+struct D2Entry { const int32_t* conn; const double* d2; int64_t n; };
+static D2Entry g_d2[64];
+static int g_nd2 = 0;
+
+static const double* find_d2(const int32_t* conn, int64_t n) {
+  for (int i = 0; i < g_nd2; ++i)
+    if (g_d2[i].conn == conn && g_d2[i].n == n) return g_d2[i].d2;
+  return nullptr;
+}
+
 static CatP cat_params(const ab_mesh* m, int k) {
   CatP c;
   c.coords = m->coords;
@@ -1171,6 +1225,7 @@ static CatP cat_params(const ab_mesh* m, int k) {
   c.L1 = m->period[1];
   c.L2 = m->period[2];
   c.periodic = (c.L0 > 0.0 || c.L1 > 0.0 || c.L2 > 0.0) ? 1 : 0;
+  c.delta2 = find_d2(c.conn, c.n);
   return c;
 }
 
@@ -1243,6 +1298,34 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
   if (!wnode || !wptr || !wslot || !loc) return fail("ab_set_windows: null window array");
   if (g_nwin >= 64) return fail("ab_set_windows: registry full");
   g_win[g_nwin++] = WinEntry{conn, wp};
+  return AB_OK;
+}
+
+int ab_filter_width(const ab_mesh* m, int32_t k, double* delta2, void* stream) {
+  if (int rc = valid_mesh(m)) return rc;
+  if (k < 0 || k >= m->n_cat) return fail("ab_filter_width: category out of range");
+  if (!delta2) return fail("ab_filter_width: null output");
+  CatP c = cat_params(m, k);
+  c.delta2 = nullptr;
+  if (c.n == 0) return AB_OK;
+  return dispatch_rule(m->cat[k].rule, [&](auto r) {
+    k_filter_width<decltype(r)::value><<<grid_for(c.n, 256), 256, 0, S(stream)>>>(c, delta2);
+    return check_launch("ab_filter_width");
+  });
+}
+
+int ab_set_filter_width(const int32_t* conn, int64_t n_elem, const double* delta2) {
+  for (int i = 0; i < g_nd2; ++i)
+    if (g_d2[i].conn == conn) {
+      if (!delta2) { g_d2[i] = g_d2[--g_nd2]; return AB_OK; }
+      g_d2[i].d2 = delta2;
+      g_d2[i].n = n_elem;
+      return AB_OK;
+    }
+  if (!delta2) return AB_OK;
+  if (!conn || n_elem < 1) return fail("ab_set_filter_width: null connectivity");
+  if (g_nd2 >= 64) return fail("ab_set_filter_width: registry full");
+  g_d2[g_nd2++] = D2Entry{conn, delta2, n_elem};
   return AB_OK;
 }
 

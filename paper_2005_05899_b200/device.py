@@ -12,6 +12,8 @@
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -46,6 +48,9 @@ class DeviceMesh:
             self.reorder_sfc()
         if windows:
             self.build_windows()
+        self._d2 = []
+        if os.environ.get("AB_NO_FILTER_WIDTH", "0") != "1":
+            self.build_filter_width()
 
     # -- C struct -------------------------------------------------------------
     def _build_struct(self):
@@ -87,6 +92,8 @@ class DeviceMesh:
         """Sort the elements of each category by the Hilbert key of their
         centroid (stable, so ties keep generator order)."""
         self.clear_windows()
+        had_d2 = bool(getattr(self, "_d2", []))
+        self.clear_filter_width()
         cents = [self.centroids(k) for k in range(len(self.rules))]
         allc = torch.cat(cents)
         lo = allc.min(dim=0).values
@@ -99,6 +106,8 @@ class DeviceMesh:
             self.conn[k] = self.conn[k][order].contiguous()
             self.ids[k] = self.ids[k][order].contiguous()
         self._build_struct()
+        if had_d2:
+            self.build_filter_width()
 
     def node_order(self, level: int = 10) -> torch.Tensor:
         """Node ids sorted by the Hilbert key of their coordinates (stable):
@@ -158,6 +167,23 @@ class DeviceMesh:
                  ptr(desc) if self.pipelined else None, wmax)
         self.windows = True
 
+    def build_filter_width(self):
+        """Vreman filter width Delta^2 = V_e^(2/3) of every element (geometry
+        only), registered for K2 (ab_set_filter_width)."""
+        self.clear_filter_width()
+        for k, conn in enumerate(self.conn):
+            d2 = torch.empty(conn.shape[0], dtype=torch.float64, device=self.device)
+            if conn.shape[0]:
+                call("ab_filter_width", C_ref(self.struct), k, ptr(d2), stream_handle())
+                call("ab_set_filter_width", ptr(conn), conn.shape[0], ptr(d2))
+            self._d2.append(d2)
+
+    def clear_filter_width(self):
+        for conn, d2 in zip(self.conn, getattr(self, "_d2", [])):
+            if d2.numel():
+                call("ab_set_filter_width", ptr(conn), 0, None)
+        self._d2 = []
+
     def window_stats(self):
         out = {}
         for rule, conn, w in zip(self.rules, self.conn, self._win):
@@ -177,6 +203,7 @@ class DeviceMesh:
     def __del__(self):
         try:
             self.clear_windows()
+            self.clear_filter_width()
         except Exception:
             pass
 
