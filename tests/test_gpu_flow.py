@@ -322,3 +322,20 @@ def test_step_host_matches_oracle(graph):
         assert rel_l2(u_h.numpy(), st["u"]) <= TOL_STATE, k
         assert rel_l2(p_h.numpy(), st["p"]) <= TOL_STATE, k
         p_h += 0.01 * (k + 1)  # the next upload is not the device's p
+
+
+@pytest.mark.parametrize("name", ["tet", "mixed", "hex_periodic"])
+def test_precomputed_filter_width_is_exact(name):
+    """K2 with the per-element Vreman filter width computed once at setup
+    (ab_filter_width) equals K2 evaluating V_e^(2/3) itself, bit for bit."""
+    from paper_2005_05899_b200.ops import assemble_momentum
+    from paper_2005_05899_b200.timestep import FlowParams
+    m = MESHES[name]
+    u, _ = _field(m, seed=2)
+    dm = _dm(m, "pipelined")
+    ph = FlowParams(rho=1.1, mu=0.02, c_vreman=0.1)
+    assert all(d.numel() == c.shape[0] for d, c in zip(dm._d2, dm.conn))
+    a = assemble_momentum(dm, u, ph).cpu().numpy()
+    dm.clear_filter_width()
+    b = assemble_momentum(dm, u, ph).cpu().numpy()
+    assert np.array_equal(a, b)
