@@ -202,8 +202,9 @@ __device__ __forceinline__ double vreman(const double (&G)[3][3], double delta2,
   }
   const double aa = S[0] + S[1] + S[2];
   double Bm = S[0] * S[1] - S[3] * S[3] + S[0] * S[2] - S[4] * S[4] + S[1] * S[2] - S[5] * S[5];
-  Bm = fmax(Bm, 0.0);
-  return aa > 1e-30 ? rho * c * delta2 * sqrt(Bm / aa) : 0.0;
+  // sqrt(B / a:a) as B * rsqrt(B * a:a): one reciprocal square root instead
+  // of an fp64 division and a square root (a few ulps from the quotient form)
+  return (aa > 1e-30 && Bm > 0.0) ? rho * c * delta2 * (Bm * rsqrt(Bm * aa)) : 0.0;
 }
 
 // ---------------------------------------------------------------------------

@@ -325,9 +325,11 @@ def test_step_host_matches_oracle(graph):
 
 
 @pytest.mark.parametrize("name", ["tet", "mixed", "hex_periodic"])
-def test_precomputed_filter_width_is_exact(name):
+def test_precomputed_filter_width(name):
     """K2 with the per-element Vreman filter width computed once at setup
-    (ab_filter_width) equals K2 evaluating V_e^(2/3) itself, bit for bit."""
+    (ab_filter_width) equals K2 evaluating V_e^(2/3) itself (to the rounding
+    of the unordered fp64 reductions of the scatter), and the widths equal
+    the oracle's cbrt(V_e)^2."""
     from paper_2005_05899_b200.ops import assemble_momentum
     from paper_2005_05899_b200.timestep import FlowParams
     m = MESHES[name]
@@ -335,7 +337,11 @@ def test_precomputed_filter_width_is_exact(name):
     dm = _dm(m, "pipelined")
     ph = FlowParams(rho=1.1, mu=0.02, c_vreman=0.1)
     assert all(d.numel() == c.shape[0] for d, c in zip(dm._d2, dm.conn))
+    for k, rule in enumerate(dm.rules):
+        X = fem.element_coords(m.coords, dm.conn[k].cpu().numpy(), m.period)
+        vol = (fem.jacobian_dets(X, rule) * fem.rule_points_weights(rule)[1][None, :]).sum(axis=1)
+        assert rel_l2(dm._d2[k].cpu().numpy(), np.cbrt(vol) ** 2) <= 1e-14
     a = assemble_momentum(dm, u, ph).cpu().numpy()
     dm.clear_filter_width()
     b = assemble_momentum(dm, u, ph).cpu().numpy()
-    assert np.array_equal(a, b)
+    assert rel_l2(a, b) <= 1e-14
