@@ -98,8 +98,8 @@ int ab_mass(const ab_mesh* mesh, int32_t cat, double* ae, double* jdet, double* 
  * `conn` (windowed gather/scatter); blk_ptr == NULL clears
  * them.  Elements are taken in blocks of `block` (must be 128): block b's
  * unique nodes are wnode[blk_ptr[b] .. blk_ptr[b+1]); window node k
- * collects the element slots wslot[wptr[k] .. wptr[k+1]) (slot = local
- * element * nnode + a); loc[e][a] is the window index of element e's node
+ * collects the element slots wslot[wptr[k] .. wptr[k+1]) (slot offset
+ * a * block + local element); loc[e][a] is the window index of element e's node
  * a; desc[b] = {blk_ptr[b], blk_ptr[b+1], wptr[blk_ptr[b]],
  * wptr[blk_ptr[b+1]]} (int32 x 4, nullable); wmax = largest window.  Every
  * K2/K4/K6 launch on that connectivity then gathers node data through the

@@ -39,7 +39,7 @@ struct WinP {
   const int64_t* __restrict__ blk_ptr;   // [n_blocks+1] offsets into wnode
   const int32_t* __restrict__ wnode;     // window node ids
   const int32_t* __restrict__ wptr;      // [n_win+1] offsets into wslot
-  const uint16_t* __restrict__ wslot;    // slot = local_elem*NN + a
+  const uint16_t* __restrict__ wslot;    // slot offset a*block + local_elem into the [NC][NN][block] slots
   const uint16_t* __restrict__ loc;      // [E][NN] window-local node index of each element node
   const int4* __restrict__ desc;         // per block {b0, b1, wptr[b0], wptr[b1]} (pipelined kernels)
   int block;                             // elements per block (== blockDim.x)
@@ -282,16 +282,14 @@ __device__ __forceinline__ void win_scatter(double* __restrict__ out, const WinP
       for (int u = 0; u < 4; ++u) sl[u] = __ldg(w.wslot + s + u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int a = sl[u] % NN, e = sl[u] / NN;
 #pragma unroll
-        for (int c = 0; c < NC; ++c) acc[c] += slots[(c * NN + a) * BLOCK + e];
+        for (int c = 0; c < NC; ++c) acc[c] += slots[c * NN * BLOCK + sl[u]];
       }
     }
     for (; s < s1; ++s) {
       const int sl = __ldg(w.wslot + s);
-      const int a = sl % NN, e = sl / NN;
 #pragma unroll
-      for (int c = 0; c < NC; ++c) acc[c] += slots[(c * NN + a) * BLOCK + e];
+      for (int c = 0; c < NC; ++c) acc[c] += slots[c * NN * BLOCK + sl];
     }
 #pragma unroll
     for (int c = 0; c < NC; ++c) red_add(out + (int64_t)node * STRIDE + c, acc[c]);
@@ -1000,10 +998,9 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
         double vq[8][NC];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-          const int slot = sl[u] < 0 ? 0 : sl[u];
-          const int a = slot % NN, el = slot / NN;
+          const double* sp = slots + (sl[u] < 0 ? 0 : sl[u]);
 #pragma unroll
-          for (int q = 0; q < NC; ++q) vq[u][q] = slots[(q * NN + a) * BLOCK + el];
+          for (int q = 0; q < NC; ++q) vq[u][q] = sp[q * NN * BLOCK];
         }
 #pragma unroll
         for (int u = 0; u < 8; ++u)

@@ -133,7 +133,8 @@ class DeviceMesh:
                 continue
             e = torch.arange(E, device=self.device, dtype=torch.int64)
             blk = (e // B).repeat_interleave(nn)
-            slot = ((e % B) * nn).repeat_interleave(nn) + torch.arange(nn, device=self.device).repeat(E)
+            # shared-memory slot offset a * B + (e % B) of every (element, node) reference
+            slot = (e % B).repeat_interleave(nn) + B * torch.arange(nn, device=self.device).repeat(E)
             node = conn.reshape(-1).to(torch.int64)
             key = blk * N + node
             order = torch.sort(key, stable=True).indices
