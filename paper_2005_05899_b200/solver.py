@@ -264,7 +264,8 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1,
-                 tmem: bool = False, group: int = 0, single_reduction: bool = False, force_mode: int = 0):
+                 tmem: bool = False, group: int = 0, single_reduction: bool = False, force_mode: int = 0,
+                 reorder_two_kernel: bool = True):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -325,6 +326,14 @@ class PCG:
                 m["fixed"] = (self.fixed[pl].contiguous() if (pl is not None and self.fixed is not None)
                               else self.fixed)
                 self.local = m
+        # two-kernel single-domain solves in the ``order`` row numbering (P A P^T;
+        # on C3 an SFC order cuts the SELL padding 4.7% and the iteration 7%)
+        self.perm2 = None
+        if not self.resident and halo is None and order is not None and reorder_two_kernel:
+            pl = order.to(device=dev, dtype=torch.int64).contiguous()
+            self.perm2 = dict(A=permute_matrix(A, pl), perm=pl, dinv=dinv[pl].contiguous(),
+                              fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
+                              b=z(), x=z())
 
     def _m(self, name):
         import contextlib
@@ -351,6 +360,8 @@ class PCG:
                      ptr(self.part), s)
             it = int(self.red[3].item()) if tol > 0 else maxit
             return self.x, it
+        if self.perm2 is not None:
+            return self._solve_permuted(b, maxit, tol, check_every, zero_b)
         call("ab_cg_init", self.n, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
              ptr(self.x), ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.own), ptr(self.red),
              ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
@@ -386,6 +397,35 @@ class PCG:
                     self.halo.allreduce_(self.red[0:2])
             it += 1
         return self.x, it
+
+    def _solve_permuted(self, b: torch.Tensor, maxit: int, tol: float, check_every: int, zero_b: bool):
+        """Two kernels per iteration on P A P^T; b in and x out through the
+        row permutation (one gather and one scatter per solve)."""
+        s = stream_handle()
+        pm = self.perm2
+        A = ctypes.byref(pm["A"].struct)
+        torch.index_select(b, 0, pm["perm"], out=pm["b"])
+        if zero_b:
+            b.zero_()
+        call("ab_cg_init", self.n, ptr(pm["b"]), None, ptr(pm["fixed"]), ptr(pm["dinv"]), ptr(self.x),
+             ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), None, ptr(self.red), ptr(self.sc), ptr(self.part),
+             ptr(self.cnt), s)
+        call("ab_cg_set_bb", ptr(self.red), ptr(self.sc), s)
+        it = 0
+        while it < maxit:
+            if tol > 0 and it % check_every == 0:
+                rr, bb = float(self.red[1].item()), float(self.sc[1].item())
+                if bb == 0.0 or math.sqrt(rr / bb) <= tol:
+                    break
+            with self._m("K5_cg_spmv"):
+                call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
+                     ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+            with self._m("K5_cg_update"):
+                call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(pm["dinv"]), ptr(self.x), ptr(self.r),
+                     ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+            it += 1
+        pm["x"].index_copy_(0, pm["perm"], self.x)
+        return pm["x"], it
 
     def residual(self) -> float:
         rr, bb = float(self.red[1].item()), float(self.sc[1].item())

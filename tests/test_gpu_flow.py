@@ -147,6 +147,7 @@ CG_VARIANTS = {
     "local": dict(),                        # local column map, node order
     "resident": dict(local=False),          # k_cg_resident (L2 gathers)
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
+    "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on P A P^T (SFC row order)
 }
 
 
@@ -169,7 +170,8 @@ def test_pcg_fixed_iterations_and_convergence(name, variant):
         kw["order"] = dm.node_order()
     # fixed iteration count: same iterate as the oracle
     pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed), **kw)
-    assert pcg.resident == (variant != "two-kernel")
+    assert pcg.resident == (not variant.startswith("two-kernel"))
+    assert (pcg.perm2 is not None) == (variant == "two-kernel-sfc")
     if variant in ("local-sfc", "tmem", "local", "cg1"):
         assert pcg.local is not None and pcg.local["tmem"] == (variant == "tmem")
     bt = torch.from_numpy(b).cuda()
