@@ -851,7 +851,7 @@ template <int R> struct OpT<R, OP_DIVERGENCE> { static constexpr int NV = 6, NC 
 template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 3, STRIDE = 4; };
 
 #ifndef PIPE_OCC_K2
-#define PIPE_OCC_K2 5  // 90 registers, measured 192 us vs 197 us at 106 (C2 K2)
+#define PIPE_OCC_K2 4  // C2 K2 graph-timed: 180.0 us at 4 CTAs/SM vs 184.5 at 5 and 182.8 at 6 (session 3)
 #endif
 // minimum resident CTAs per SM requested from the register allocator
 template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
