@@ -110,6 +110,13 @@ int ab_mass(const ab_mesh* mesh, int32_t cat, double* ae, double* jdet, double* 
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
                    const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, const int32_t* desc,
                    int32_t wmax);
+/* The pipelined kernels (desc != NULL) also need, per 128-element block b,
+ * the block's 128 * nnode element-node references sorted by window node:
+ * wref[b * 128 * nnode + j] = slot offset | (window index << 16), the last
+ * block padded with 0xffff0000.  Thread t of the block then reduces
+ * references t*nnode .. t*nnode+nnode-1 (one fp64 reduction per window node
+ * it touches). */
+int ab_set_window_refs(const int32_t* conn, const uint32_t* wref);
 
 /* ---- Partition file I/O (host; reference sfc.py:385-417 `part 1` body) ----
  * ab_format_partition: lines "i parts[i]\n" for i = first .. first+n-1 into

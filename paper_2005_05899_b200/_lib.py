@@ -60,6 +60,7 @@ _SIGS = {
     "ab_last_error": ([], C.c_char_p),
     "ab_launch_count": ([], i64),
     "ab_set_windows": ([vp, i32, vp, vp, vp, vp, vp, vp, i32], C.c_int),
+    "ab_set_window_refs": ([vp, vp], C.c_int),
     "ab_format_partition": ([vp, i64, i64, vp, i64], C.c_int64),
     "ab_filter_width": ([P(AbMesh), i32, vp, vp], C.c_int),
     "ab_set_filter_width": ([vp, i64, vp], C.c_int),

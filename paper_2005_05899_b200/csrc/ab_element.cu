@@ -42,6 +42,9 @@ struct WinP {
   const uint16_t* __restrict__ wslot;    // slot offset a*block + local_elem into the [NC][NN][block] slots
   const uint16_t* __restrict__ loc;      // [E][NN] window-local node index of each element node
   const int4* __restrict__ desc;         // per block {b0, b1, wptr[b0], wptr[b1]} (pipelined kernels)
+  // pipelined kernels: the block's block*NN element-node references sorted by
+  // window node, (slot offset | window index << 16); padding 0xffff0000
+  const uint32_t* __restrict__ wref;
   int block;                             // elements per block (== blockDim.x)
   int wmax;                              // largest window (nodes) of any block
 };
@@ -746,12 +749,13 @@ __device__ __forceinline__ Chunk chunk16(const void* base, int64_t lo_elem, int6
   return Chunk{reinterpret_cast<const char*>(a), (uint32_t)(b - a), (uint32_t)((lo - a) / es)};
 }
 
-// Shared-memory layout: 3 metadata stages, 2 node-data stages, 1 slot buffer.
+// Shared-memory layout: 3 metadata stages (window node ids, sorted
+// references, element window indices), 2 node-data stages, 1 slot buffer.
 template <int NN, int NV, int BLOCK>
 struct PipeSmem {
   static __host__ __device__ size_t wcap(int wmax) { return ((size_t)wmax + 8 + 3) & ~(size_t)3; }
   static __host__ __device__ size_t meta_bytes(int wmax) {
-    return wcap(wmax) * 4 + (wcap(wmax) + 4) * 4 + (size_t)BLOCK * NN * 2 + ((size_t)BLOCK * NN + 16) * 2;
+    return wcap(wmax) * 4 + (size_t)BLOCK * NN * 4 + ((size_t)BLOCK * NN + 16) * 2;
   }
   static __host__ __device__ size_t node_bytes(int wmax) { return (size_t)NV * wmax * 8; }
   static __host__ __device__ size_t slot_bytes() { return sizeof(double) * 3 * NN * BLOCK; }
@@ -762,35 +766,30 @@ struct PipeSmem {
 
 struct MetaPtr {
   int32_t* wnode;
-  int32_t* wptr;
+  uint32_t* wref;
   uint16_t* loc;
-  uint16_t* wslot;
 };
 
 template <int NN, int NV, int BLOCK>
 __device__ __forceinline__ MetaPtr meta_ptr(unsigned char* smem, int wmax, int q) {
   using L = PipeSmem<NN, NV, BLOCK>;
   unsigned char* base = smem + (size_t)q * L::meta_bytes(wmax);
-  const size_t wn = L::wcap(wmax) * 4, wp = (L::wcap(wmax) + 4) * 4, lc = (size_t)BLOCK * NN * 2;
+  const size_t wn = L::wcap(wmax) * 4, wr = (size_t)BLOCK * NN * 4;
   MetaPtr m;
   m.wnode = reinterpret_cast<int32_t*>(base);
-  m.wptr = reinterpret_cast<int32_t*>(base + wn);
-  m.loc = reinterpret_cast<uint16_t*>(base + wn + wp);
-  m.wslot = reinterpret_cast<uint16_t*>(base + wn + wp + lc);
+  m.wref = reinterpret_cast<uint32_t*>(base + wn);
+  m.loc = reinterpret_cast<uint16_t*>(base + wn + wr);
   return m;
 }
 
 // Offsets of a block's data inside its (16-byte widened) metadata chunks.
 struct BlockView {
-  int nw, s_lo, skip_wnode, skip_wptr, skip_wslot;
+  int nw, skip_wnode;
 };
 __device__ __forceinline__ BlockView block_view(const WinP& w, int4 d) {
   BlockView v;
   v.nw = d.y - d.x;
-  v.s_lo = d.z;
   v.skip_wnode = (int)((((uint64_t)w.wnode + (uint64_t)d.x * 4) & 15) / 4);
-  v.skip_wptr = (int)((((uint64_t)w.wptr + (uint64_t)d.x * 4) & 15) / 4);
-  v.skip_wslot = (int)((((uint64_t)w.wslot + (uint64_t)d.z * 2) & 15) / 2);
   return v;
 }
 
@@ -801,13 +800,11 @@ __device__ __forceinline__ void issue_meta(const WinP& w, int64_t n_elem, int64_
   const int64_t e0 = b * w.block;
   const int64_t e1 = e0 + w.block < n_elem ? e0 + w.block : n_elem;
   const Chunk cw = chunk16(w.wnode, d.x, d.y, 4);
-  const Chunk cp = chunk16(w.wptr, d.x, (int64_t)d.y + 1, 4);
-  const Chunk cs = chunk16(w.wslot, d.z, d.w, 2);
+  const Chunk cr = chunk16(w.wref, e0 * NN, (e0 + w.block) * NN, 4);  // padded to whole blocks
   const Chunk cl = chunk16(w.loc, e0 * NN, e1 * NN, 2);
-  mbar_arrive_tx(bar, cw.bytes + cp.bytes + cs.bytes + cl.bytes);
+  mbar_arrive_tx(bar, cw.bytes + cr.bytes + cl.bytes);
   bulk_copy(m.wnode, cw.src, cw.bytes, bar);
-  bulk_copy(m.wptr, cp.src, cp.bytes, bar);
-  bulk_copy(m.wslot, cs.src, cs.bytes, bar);
+  bulk_copy(m.wref, cr.src, cr.bytes, bar);
   bulk_copy(m.loc, cl.src, cl.bytes, bar);
 }
 
@@ -981,35 +978,54 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
         for (int k = 0; k < NC; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = 0.0;
     }
     __syncthreads();
-    // D: ordered per-window-node sums, one fp64 reduction per component
-    for (int k = threadIdx.x; k < vc.nw; k += BLOCK) {
-      const int node = mc.wnode[vc.skip_wnode + k];
-      const int s0 = mc.wptr[vc.skip_wptr + k] - vc.s_lo, s1 = mc.wptr[vc.skip_wptr + k + 1] - vc.s_lo;
+    // D: thread t sums the block's sorted references t*NN .. t*NN+NN-1 (the
+    // block*NN element-node references ordered by window node), one fp64
+    // reduction per (thread, window node) piece: every thread busy, no
+    // variable-length list walks.
+    {
+      uint32_t rr[NN];
+      const uint32_t* wr = mc.wref + threadIdx.x * NN;
+      if constexpr (NN == 4) {
+        const uint4 v = *reinterpret_cast<const uint4*>(wr);
+        rr[0] = v.x; rr[1] = v.y; rr[2] = v.z; rr[3] = v.w;
+      } else if constexpr (NN == 8) {
+        const uint4 v = *reinterpret_cast<const uint4*>(wr), u = *reinterpret_cast<const uint4*>(wr + 4);
+        rr[0] = v.x; rr[1] = v.y; rr[2] = v.z; rr[3] = v.w; rr[4] = u.x; rr[5] = u.y; rr[6] = u.z; rr[7] = u.w;
+      } else {
+#pragma unroll
+        for (int k = 0; k < NN; ++k) rr[k] = wr[k];
+      }
+      double vq[NN][NC];
+#pragma unroll
+      for (int k = 0; k < NN; ++k)
+#pragma unroll
+        for (int q = 0; q < NC; ++q) vq[k][q] = slots[q * NN * BLOCK + (rr[k] & 0xffffu)];
       double acc[NC];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) acc[q] = 0.0;
-      // batches of 8 list entries: all slot ids, then all slot values, then
-      // the adds in list order (two shared-memory round trips per batch
-      // instead of two per entry)
-      for (int t0 = s0; t0 < s1; t0 += 8) {
-        int sl[8];
+      for (int q = 0; q < NC; ++q) acc[q] = vq[0][q];
+      uint32_t cur = rr[0] >> 16;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) sl[u] = t0 + u < s1 ? (int)mc.wslot[vc.skip_wslot + t0 + u] : -1;
-        double vq[8][NC];
+      for (int k = 1; k < NN; ++k) {
+        const uint32_t lw = rr[k] >> 16;
+        if (lw != cur) {
+          if (cur != 0xffffu) {
+            const int node = mc.wnode[vc.skip_wnode + cur];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const double* sp = slots + (sl[u] < 0 ? 0 : sl[u]);
+            for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+          }
 #pragma unroll
-          for (int q = 0; q < NC; ++q) vq[u][q] = sp[q * NN * BLOCK];
+          for (int q = 0; q < NC; ++q) acc[q] = vq[k][q];
+          cur = lw;
+        } else {
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] += vq[k][q];
         }
-#pragma unroll
-        for (int u = 0; u < 8; ++u)
-          if (sl[u] >= 0)
-#pragma unroll
-            for (int q = 0; q < NC; ++q) acc[q] += vq[u][q];
       }
+      if (cur != 0xffffu) {
+        const int node = mc.wnode[vc.skip_wnode + cur];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+        for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+      }
     }
     d0 = d1;
     d1 = d2;
@@ -1023,6 +1039,7 @@ static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double s
   constexpr int NN = RuleT<R>::NN;
   constexpr int NV = OpT<R, OP>::NV;
   using L = PipeSmem<NN, NV, BLOCK>;
+  if (!w.wref) return fail("pipelined element kernel: sorted window references not registered (ab_set_window_refs)");
   const size_t smem = L::total(w.wmax);
   auto kern = k_pipe<R, OP, BLOCK>;
   if (smem > 48 * 1024 &&
@@ -1283,7 +1300,7 @@ extern "C" {
 int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, const int32_t* wnode,
                    const int32_t* wptr, const uint16_t* wslot, const uint16_t* loc, const int32_t* desc,
                    int32_t wmax) {
-  const WinP wp{blk_ptr, wnode, wptr, wslot, loc, reinterpret_cast<const int4*>(desc), block, wmax};
+  const WinP wp{blk_ptr, wnode, wptr, wslot, loc, reinterpret_cast<const int4*>(desc), nullptr, block, wmax};
   for (int i = 0; i < g_nwin; ++i)
     if (g_win[i].conn == conn) {
       if (!blk_ptr) { g_win[i] = g_win[--g_nwin]; return AB_OK; }
@@ -1297,6 +1314,16 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
   if (g_nwin >= 64) return fail("ab_set_windows: registry full");
   g_win[g_nwin++] = WinEntry{conn, wp};
   return AB_OK;
+}
+
+// Sorted element-node references of a category's windows (pipelined kernels).
+int ab_set_window_refs(const int32_t* conn, const uint32_t* wref) {
+  for (int i = 0; i < g_nwin; ++i)
+    if (g_win[i].conn == conn) {
+      g_win[i].w.wref = wref;
+      return AB_OK;
+    }
+  return fail("ab_set_window_refs: no windows registered for this connectivity");
 }
 
 int ab_filter_width(const ab_mesh* m, int32_t k, double* delta2, void* stream) {

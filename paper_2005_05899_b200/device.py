@@ -155,6 +155,11 @@ class DeviceMesh:
             loc = torch.empty_like(local)
             loc[order] = local
             loc = loc.to(torch.int16).reshape(E, nn).contiguous()
+            # sorted references of every block (slot offset | window index << 16), padded to whole blocks
+            nblk_ = (E + B - 1) // B
+            wref = torch.full((nblk_ * B * nn,), 0xFFFF << 16, dtype=torch.int64, device=self.device)
+            wref[:E * nn] = slot[order] | (local << 16)
+            wref = torch.where(wref >= 1 << 31, wref - (1 << 32), wref).to(torch.int32).contiguous()
             wmax = int((blk_ptr[1:] - blk_ptr[:-1]).max().item())
             # per-block descriptors for the pipelined kernels
             b0, b1 = blk_ptr[:-1], blk_ptr[1:]
@@ -162,10 +167,11 @@ class DeviceMesh:
             desc = desc.to(torch.int32).contiguous()
             # bulk copies read whole 16-byte granules: pad every array
             wnode, wptr, wslot, loc = (_padded(t) for t in (wnode, wptr, wslot, loc))
-            w = (blk_ptr, wnode, wptr, wslot, loc, wmax, desc)
+            w = (blk_ptr, wnode, wptr, wslot, loc, wmax, desc, wref)
             self._win.append(w)
             call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot), ptr(loc),
                  ptr(desc) if self.pipelined else None, wmax)
+            call("ab_set_window_refs", ptr(conn), ptr(wref))
         self.windows = True
 
     def build_filter_width(self):
