@@ -1000,19 +1000,32 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       for (int k = 0; k < NN; ++k)
 #pragma unroll
         for (int q = 0; q < NC; ++q) vq[k][q] = slots[q * NN * BLOCK + (rr[k] & 0xffffu)];
-      double acc[NC];
+      // pieces: maximal runs of equal window index.  Middle pieces are
+      // reduced at once; the first (H) and last (T) may continue in the
+      // neighbouring lanes: a lane with >= 2 pieces hands H to the lane
+      // before it when that lane's last piece is the same window node (one
+      // shuffle level; longer chains keep one reduction per lane).
+      auto red_node = [&](uint32_t lw, const double (&v)[NC]) {
+        const int node = mc.wnode[vc.skip_wnode + lw];
 #pragma unroll
-      for (int q = 0; q < NC; ++q) acc[q] = vq[0][q];
+        for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, v[q]);
+      };
+      double acc[NC], H[NC];
+#pragma unroll
+      for (int q = 0; q < NC; ++q) acc[q] = H[q] = vq[0][q];
       uint32_t cur = rr[0] >> 16;
+      int np = 1;
 #pragma unroll
       for (int k = 1; k < NN; ++k) {
         const uint32_t lw = rr[k] >> 16;
         if (lw != cur) {
-          if (cur != 0xffffu) {
-            const int node = mc.wnode[vc.skip_wnode + cur];
+          if (np == 1) {
 #pragma unroll
-            for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+            for (int q = 0; q < NC; ++q) H[q] = acc[q];
+          } else if (cur != 0xffffu) {
+            red_node(cur, acc);
           }
+          ++np;
 #pragma unroll
           for (int q = 0; q < NC; ++q) acc[q] = vq[k][q];
           cur = lw;
@@ -1021,10 +1034,23 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
           for (int q = 0; q < NC; ++q) acc[q] += vq[k][q];
         }
       }
-      if (cur != 0xffffu) {
-        const int node = mc.wnode[vc.skip_wnode + cur];
+      const uint32_t f = rr[0] >> 16, l = cur;
+      const int lane = threadIdx.x & 31;
+      const uint32_t mine = f | (np >= 2 ? 0x80000000u : 0u);
+      const uint32_t nxt = __shfl_down_sync(0xffffffffu, mine, 1);
+      const uint32_t prv = __shfl_up_sync(0xffffffffu, l, 1);
+      double hn[NC];
 #pragma unroll
-        for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, acc[q]);
+      for (int q = 0; q < NC; ++q) hn[q] = __shfl_down_sync(0xffffffffu, H[q], 1);
+      const bool recv = lane != 31 && (nxt >> 31) && (nxt & 0xffffu) == l && l != 0xffffu;
+      const bool give = lane != 0 && np >= 2 && prv == f && f != 0xffffu;
+      if (np >= 2 && !give && f != 0xffffu) red_node(f, H);
+      if (l != 0xffffu) {
+        if (recv) {
+#pragma unroll
+          for (int q = 0; q < NC; ++q) acc[q] += hn[q];
+        }
+        red_node(l, acc);
       }
     }
     d0 = d1;
