@@ -170,7 +170,7 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
 
 
 # flops per element of K2 as written in the kernel (DESIGN.md §4.1 counts)
-FLOPS_K2 = {"tet4": 432.5}  # ncu (current K2): 138 DFMA + 66 DMUL + 90.5 DADD thread-instructions per tet4 element
+FLOPS_K2 = {"tet4": 417.8}  # ncu (current K2): 138 DFMA + 66 DMUL + 75.8 DADD thread-instructions per tet4 element
 
 
 def load_peaks():
@@ -392,7 +392,7 @@ def run_native(args):
         ach = kern["K2_momentum"]["gflops"] / 1e3
         roof_k2 = {"kernel": "K2_momentum", "bound": "fp64", "achieved": round(ach, 3), "peak": fp_peak,
                    "unit": "TFLOP/s", "frac": round(ach / fp_peak, 4), "peak_source": fp_src,
-                   "flops_definition": "tet4: 432.5 fp64 flops per element = 2 x 138 DFMA + 66 DMUL + 90.5 DADD "
+                   "flops_definition": "tet4: 417.8 fp64 flops per element = 2 x 138 DFMA + 66 DMUL + 75.8 DADD "
                                        "(ncu-counted thread instructions of the current K2), DESIGN.md §4"}
     if dom == "K5_cg_resident":
         # what this design must move at minimum per iteration: the stored SELL
