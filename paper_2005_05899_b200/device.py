@@ -124,7 +124,7 @@ class DeviceMesh:
         return torch.sort(keys, stable=True).indices.to(torch.int32)
 
     # -- node windows ---------------------------------------------------------
-    def tune_tet_node_order(self, block: int = WINDOW_BLOCK):
+    def tune_tet_node_order(self, block: int = WINDOW_BLOCK, chunk: int = 1 << 22):
         """Permute the 4 nodes of every tetrahedron (all tet kernels use |det J|
         and are symmetric in the node order, so results change only by
         rounding) so that the window gathers of K2 — instruction a reads node a
@@ -132,43 +132,47 @@ class DeviceMesh:
         words — hit distinct banks: greedy per group of 8 elements, choosing
         for each element the permutation with the fewest same-bank, different-
         address partners among the group's earlier elements.  Window-local
-        indices do not depend on the node order, so they are computed first."""
+        indices do not depend on the node order, so they are computed first.
+        Processed in chunks of whole blocks (``chunk`` elements) to bound the
+        memory on 250M-element meshes."""
         import itertools
         perms = torch.tensor(list(itertools.permutations(range(4))), dtype=torch.int64, device=self.device)
         N = self.n_nodes
+        chunk = max(block, chunk // block * block)
         for k, (rule, conn) in enumerate(zip(self.rules, self.conn)):
             E = conn.shape[0]
             if not rule.startswith("tet") or E < 8:
                 continue
             E8 = E // 8 * 8
-            e = torch.arange(E, device=self.device, dtype=torch.int64)
-            key = (e // block).repeat_interleave(4) * N + conn.reshape(-1).to(torch.int64)
-            _, inv = torch.unique(key, return_inverse=True)  # ascending (block, node): window order
-            first = torch.zeros_like(inv)
-            blk = (e // block).repeat_interleave(4)
-            first.scatter_reduce_(0, blk, inv, reduce="amin", include_self=False)
-            loc = (inv - first[blk]).view(E, 4)[:E8].view(-1, 8, 4)  # (G, 8, 4) window indices
-            G = loc.shape[0]
-            chosen = torch.full((G, 8, 4), -1, dtype=torch.int64, device=self.device)
-            best_all = torch.zeros((G, 8), dtype=torch.int64, device=self.device)
-            for j in range(8):
-                cand = loc[:, j, :][:, perms]  # (G, 24, 4): value placed in slot a
-                prev = chosen[:, :j, :]        # (G, j, 4)
-                if j == 0:
-                    cost = torch.zeros((G, 24), dtype=torch.int64, device=self.device)
-                else:
-                    c = cand[:, :, None, :]            # (G, 24, 1, 4)
-                    pv = prev[:, None, :, :]           # (G, 1, j, 4)
-                    clash = ((c % 8) == (pv % 8)) & (c != pv)
-                    cost = clash.sum(dim=(2, 3))
-                best = torch.argmin(cost, dim=1)       # first minimum
-                best_all[:, j] = best
-                chosen[:, j, :] = cand[torch.arange(G, device=self.device), best]
-            pidx = perms[best_all.view(-1)]            # (E8, 4)
-            c8 = conn[:E8].to(torch.int64)
-            newc = torch.gather(c8, 1, pidx).to(torch.int32)
             conn = conn.clone()
-            conn[:E8] = newc
+            for e0 in range(0, E8, chunk):
+                e1 = min(E8, e0 + chunk)
+                n = e1 - e0
+                c = conn[e0:e1].to(torch.int64)
+                blk = (torch.arange(n, device=self.device, dtype=torch.int64) // block).repeat_interleave(4)
+                _, inv = torch.unique(blk * N + c.reshape(-1), return_inverse=True)  # (block, node) ascending
+                first = torch.zeros(int(blk[-1].item()) + 1, dtype=inv.dtype, device=self.device)
+                first.scatter_reduce_(0, blk, inv, reduce="amin", include_self=False)
+                loc = (inv - first[blk]).view(-1, 8, 4)  # (G, 8, 4) window indices
+                del inv, blk
+                G = loc.shape[0]
+                rows = torch.arange(G, device=self.device)
+                chosen = torch.empty((G, 8, 4), dtype=torch.int64, device=self.device)
+                best_all = torch.empty((G, 8), dtype=torch.int64, device=self.device)
+                for j in range(8):
+                    cand = loc[:, j, :][:, perms]  # (G, 24, 4): the value placed in slot a
+                    if j == 0:
+                        best = torch.zeros(G, dtype=torch.int64, device=self.device)
+                    else:
+                        cv = cand[:, :, None, :]
+                        pv = chosen[:, None, :j, :]
+                        cost = (((cv - pv) % 8 == 0) & (cv != pv)).sum(dim=(2, 3))
+                        best = torch.argmin(cost, dim=1)  # first minimum
+                    best_all[:, j] = best
+                    chosen[:, j, :] = cand[rows, best]
+                pidx = perms[best_all.view(-1)]
+                conn[e0:e1] = torch.gather(c, 1, pidx).to(torch.int32)
+                del loc, chosen, c
             self.conn[k] = conn.contiguous()
         self._build_struct()
 
