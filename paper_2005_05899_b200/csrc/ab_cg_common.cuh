@@ -8,7 +8,10 @@
 namespace ab {
 
 constexpr int kResBlock = 1024;
-constexpr int kLocChunk = 8;
+#ifndef LOC_CHUNK
+#define LOC_CHUNK 8
+#endif
+constexpr int kLocChunk = LOC_CHUNK;
 
 // Grid barrier on a monotone arrival counter (zeroed before launch): the
 // k-th barrier completes when the counter reaches k * gridDim.x.  One
