@@ -178,53 +178,15 @@ class DeviceMesh:
 
     def build_windows(self):
         self.clear_windows()
-        B = WINDOW_BLOCK
-        N = self.n_nodes
-        for k, conn in enumerate(self.conn):
-            E, nn = conn.shape
-            if E == 0:
+        for conn in self.conn:
+            if conn.shape[0] == 0:
                 self._win.append(None)
                 continue
-            e = torch.arange(E, device=self.device, dtype=torch.int64)
-            blk = (e // B).repeat_interleave(nn)
-            # shared-memory slot offset a * B + (e % B) of every (element, node) reference
-            slot = (e % B).repeat_interleave(nn) + B * torch.arange(nn, device=self.device).repeat(E)
-            node = conn.reshape(-1).to(torch.int64)
-            key = blk * N + node
-            order = torch.sort(key, stable=True).indices
-            ks = key[order]
-            start = torch.ones_like(ks, dtype=torch.bool)
-            start[1:] = ks[1:] != ks[:-1]
-            starts = torch.nonzero(start).squeeze(1)
-            wnode = (ks[starts] % N).to(torch.int32).contiguous()
-            wblk = ks[starts] // N
-            wptr = torch.cat([starts, torch.tensor([ks.numel()], device=self.device)]).to(torch.int32).contiguous()
-            wslot = slot[order].to(torch.int16).contiguous()
-            nblk = (E + B - 1) // B
-            blk_ptr = torch.searchsorted(wblk, torch.arange(nblk + 1, device=self.device, dtype=torch.int64))
-            blk_ptr = blk_ptr.to(torch.int64).contiguous()
-            # window-local index of every (element, node) reference
-            uid = torch.cumsum(start.to(torch.int64), 0) - 1
-            local = uid - blk_ptr[blk[order]]
-            loc = torch.empty_like(local)
-            loc[order] = local
-            loc = loc.to(torch.int16).reshape(E, nn).contiguous()
-            # sorted references of every block (slot offset | window index << 16), padded to whole blocks
-            nblk_ = (E + B - 1) // B
-            wref = torch.full((nblk_ * B * nn,), 0xFFFF << 16, dtype=torch.int64, device=self.device)
-            wref[:E * nn] = slot[order] | (local << 16)
-            wref = torch.where(wref >= 1 << 31, wref - (1 << 32), wref).to(torch.int32).contiguous()
-            wmax = int((blk_ptr[1:] - blk_ptr[:-1]).max().item())
-            # per-block descriptors for the pipelined kernels
-            b0, b1 = blk_ptr[:-1], blk_ptr[1:]
-            desc = torch.stack([b0, b1, wptr[b0].to(torch.int64), wptr[b1].to(torch.int64)], dim=1)
-            desc = desc.to(torch.int32).contiguous()
-            # bulk copies read whole 16-byte granules: pad every array
-            wnode, wptr, wslot, loc = (_padded(t) for t in (wnode, wptr, wslot, loc))
-            w = (blk_ptr, wnode, wptr, wslot, loc, wmax, desc, wref)
+            w = window_arrays(conn, self.n_nodes, WINDOW_BLOCK)
+            blk_ptr, wnode, wptr, wslot, loc, wmax, desc, wref = w
             self._win.append(w)
-            call("ab_set_windows", ptr(conn), B, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot), ptr(loc),
-                 ptr(desc) if self.pipelined else None, wmax)
+            call("ab_set_windows", ptr(conn), WINDOW_BLOCK, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot),
+                 ptr(loc), ptr(desc) if self.pipelined else None, wmax)
             call("ab_set_window_refs", ptr(conn), ptr(wref))
         self.windows = True
 
@@ -267,6 +229,51 @@ class DeviceMesh:
             self.clear_filter_width()
         except Exception:
             pass
+
+
+def window_arrays(conn: torch.Tensor, N: int, B: int = WINDOW_BLOCK):
+    """Node windows of one category (any device): returns (blk_ptr, wnode,
+    wptr, wslot, loc, wmax, desc, wref) as registered by ab_set_windows /
+    ab_set_window_refs (include/alyab200.h).  Window indices ascend with the
+    node id inside each block."""
+    dev = conn.device
+    E, nn = conn.shape
+    e = torch.arange(E, device=dev, dtype=torch.int64)
+    blk = (e // B).repeat_interleave(nn)
+    # shared-memory slot offset a * B + (e % B) of every (element, node) reference
+    slot = (e % B).repeat_interleave(nn) + B * torch.arange(nn, device=dev).repeat(E)
+    node = conn.reshape(-1).to(torch.int64)
+    key = blk * N + node
+    order = torch.sort(key, stable=True).indices
+    ks = key[order]
+    start = torch.ones_like(ks, dtype=torch.bool)
+    start[1:] = ks[1:] != ks[:-1]
+    starts = torch.nonzero(start).squeeze(1)
+    wnode = (ks[starts] % N).to(torch.int32).contiguous()
+    wblk = ks[starts] // N
+    wptr = torch.cat([starts, torch.tensor([ks.numel()], device=dev)]).to(torch.int32).contiguous()
+    wslot = slot[order].to(torch.int16).contiguous()
+    nblk = (E + B - 1) // B
+    blk_ptr = torch.searchsorted(wblk, torch.arange(nblk + 1, device=dev, dtype=torch.int64))
+    blk_ptr = blk_ptr.to(torch.int64).contiguous()
+    # window-local index of every (element, node) reference
+    uid = torch.cumsum(start.to(torch.int64), 0) - 1
+    local = uid - blk_ptr[blk[order]]
+    loc = torch.empty_like(local)
+    loc[order] = local
+    loc = loc.to(torch.int16).reshape(E, nn).contiguous()
+    # sorted references of every block (slot offset | window index << 16), padded to whole blocks
+    wref = torch.full((nblk * B * nn,), 0xFFFF << 16, dtype=torch.int64, device=dev)
+    wref[:E * nn] = slot[order] | (local << 16)
+    wref = torch.where(wref >= 1 << 31, wref - (1 << 32), wref).to(torch.int32).contiguous()
+    wmax = int((blk_ptr[1:] - blk_ptr[:-1]).max().item())
+    # per-block descriptors for the pipelined kernels
+    b0, b1 = blk_ptr[:-1], blk_ptr[1:]
+    desc = torch.stack([b0, b1, wptr[b0].to(torch.int64), wptr[b1].to(torch.int64)], dim=1)
+    desc = desc.to(torch.int32).contiguous()
+    # bulk copies read whole 16-byte granules: pad every array
+    wnode, wptr, wslot, loc = (_padded(t) for t in (wnode, wptr, wslot, loc))
+    return (blk_ptr, wnode, wptr, wslot, loc, wmax, desc, wref)
 
 
 def _padded(t: torch.Tensor) -> torch.Tensor:
