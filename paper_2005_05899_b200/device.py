@@ -139,11 +139,12 @@ class DeviceMesh:
         perms = torch.tensor(list(itertools.permutations(range(4))), dtype=torch.int64, device=self.device)
         N = self.n_nodes
         chunk = max(block, chunk // block * block)
+        gs = int(os.environ.get("AB_TET_TUNE_GROUP", "8"))  # lanes per modelled shared-memory phase
         for k, (rule, conn) in enumerate(zip(self.rules, self.conn)):
             E = conn.shape[0]
-            if not rule.startswith("tet") or E < 8:
+            if not rule.startswith("tet") or E < gs:
                 continue
-            E8 = E // 8 * 8
+            E8 = E // gs * gs
             conn = conn.clone()
             for e0 in range(0, E8, chunk):
                 e1 = min(E8, e0 + chunk)
@@ -153,13 +154,13 @@ class DeviceMesh:
                 _, inv = torch.unique(blk * N + c.reshape(-1), return_inverse=True)  # (block, node) ascending
                 first = torch.zeros(int(blk[-1].item()) + 1, dtype=inv.dtype, device=self.device)
                 first.scatter_reduce_(0, blk, inv, reduce="amin", include_self=False)
-                loc = (inv - first[blk]).view(-1, 8, 4)  # (G, 8, 4) window indices
+                loc = (inv - first[blk]).view(-1, gs, 4)  # (G, gs, 4) window indices
                 del inv, blk
                 G = loc.shape[0]
                 rows = torch.arange(G, device=self.device)
-                chosen = torch.empty((G, 8, 4), dtype=torch.int64, device=self.device)
-                best_all = torch.empty((G, 8), dtype=torch.int64, device=self.device)
-                for j in range(8):
+                chosen = torch.empty((G, gs, 4), dtype=torch.int64, device=self.device)
+                best_all = torch.empty((G, gs), dtype=torch.int64, device=self.device)
+                for j in range(gs):
                     cand = loc[:, j, :][:, perms]  # (G, 24, 4): the value placed in slot a
                     if j == 0:
                         best = torch.zeros(G, dtype=torch.int64, device=self.device)
@@ -170,6 +171,21 @@ class DeviceMesh:
                         best = torch.argmin(cost, dim=1)  # first minimum
                     best_all[:, j] = best
                     chosen[:, j, :] = cand[rows, best]
+                # refinement sweeps: re-choose each element against all the
+                # others of its group (never worse than the current choice,
+                # which is candidate best_all[:, j] with the same cost model)
+                for _ in range(int(os.environ.get("AB_TET_TUNE_SWEEPS", "1"))):
+                    for j in range(gs):
+                        cand = loc[:, j, :][:, perms]
+                        others = torch.cat([chosen[:, :j, :], chosen[:, j + 1:, :]], dim=1)
+                        cv = cand[:, :, None, :]
+                        pv = others[:, None, :, :]
+                        cost = (((cv - pv) % 8 == 0) & (cv != pv)).sum(dim=(2, 3))
+                        cur = cost[rows, best_all[:, j]]
+                        best = torch.argmin(cost, dim=1)
+                        best = torch.where(cost[rows, best] < cur, best, best_all[:, j])
+                        best_all[:, j] = best
+                        chosen[:, j, :] = cand[rows, best]
                 pidx = perms[best_all.view(-1)]
                 conn[e0:e1] = torch.gather(c, 1, pidx).to(torch.int32)
                 del loc, chosen, c
