@@ -198,7 +198,8 @@ class DeviceMesh:
             if conn.shape[0] == 0:
                 self._win.append(None)
                 continue
-            w = window_arrays(conn, self.n_nodes, WINDOW_BLOCK)
+            w = window_arrays(conn, self.n_nodes, WINDOW_BLOCK,
+                              spread=self.pipelined and os.environ.get("AB_NO_SLOT_SPREAD", "0") != "1")
             blk_ptr, wnode, wptr, wslot, loc, wmax, desc, wref = w
             self._win.append(w)
             call("ab_set_windows", ptr(conn), WINDOW_BLOCK, ptr(blk_ptr), ptr(wnode), ptr(wptr), ptr(wslot),
@@ -247,7 +248,56 @@ class DeviceMesh:
             pass
 
 
-def window_arrays(conn: torch.Tensor, N: int, B: int = WINDOW_BLOCK):
+def _spread_slot_banks(order, starts, slot, E, nn, B, chunk_blocks: int = 1 << 17):
+    """Reorder the references inside every window node's run (sum order only)
+    so that the phase-D slot loads — lane t of a block reads sorted positions
+    t*nn .. t*nn+nn-1, instruction k position t*nn+k, 16 lanes per shared-
+    memory phase of 8-byte words, bank = slot offset mod 16 — meet few
+    same-bank partners: position by position, the run's remaining reference
+    with the fewest already placed same-bank references in that phase."""
+    dev = order.device
+    R = order.numel()
+    RB = B * nn
+    nblk_full = R // RB
+    if nblk_full == 0:
+        return order
+    run_end = torch.empty(R, dtype=torch.int64, device=dev)
+    ends = torch.cat([starts[1:], torch.tensor([R], device=dev)])
+    run_end[starts] = ends
+    run_end = torch.cummax(torch.where(torch.zeros(R, dtype=torch.bool, device=dev).index_fill_(0, starts, True),
+                                       run_end, torch.zeros_like(run_end)), 0).values
+    out = order.clone()
+    bank_all = slot % 16
+    maxrun = int((ends - starts).max().item())
+    n_ph = (B // 16) * nn
+    for b0 in range(0, nblk_full, chunk_blocks):
+        b1 = min(nblk_full, b0 + chunk_blocks)
+        nb = b1 - b0
+        base = torch.arange(b0, b1, device=dev) * RB
+        o = out[b0 * RB:b1 * RB].view(nb, RB).clone()
+        re = (run_end[b0 * RB:b1 * RB].view(nb, RB) - base[:, None])  # run end (block-relative) of each position
+        cnt = torch.zeros((nb, n_ph, 16), dtype=torch.int32, device=dev)
+        rows = torch.arange(nb, device=dev)
+        jj = torch.arange(maxrun, device=dev)
+        for p_ in range(RB):
+            t, k = divmod(p_, nn)
+            ph = (t // 16) * nn + k
+            cand = p_ + jj[None, :]                                   # (nb, maxrun) positions
+            ok = cand < re[:, p_:p_ + 1]
+            cand = torch.where(ok, cand, torch.full_like(cand, p_))
+            bk = bank_all[o.gather(1, cand)]                          # banks of the candidates
+            cost = cnt[rows, ph].gather(1, bk).to(torch.int64) * 4096 + jj[None, :]
+            cost = torch.where(ok, cost, torch.full_like(cost, 1 << 40))
+            pick = cand[rows, torch.argmin(cost, dim=1)]
+            a_ = o[rows, p_].clone()
+            o[rows, p_] = o[rows, pick]
+            o[rows, pick] = a_
+            cnt[rows, ph, bank_all[o[rows, p_]]] += 1
+        out[b0 * RB:b1 * RB] = o.view(-1)
+    return out
+
+
+def window_arrays(conn: torch.Tensor, N: int, B: int = WINDOW_BLOCK, spread: bool = True):
     """Node windows of one category (any device): returns (blk_ptr, wnode,
     wptr, wslot, loc, wmax, desc, wref) as registered by ab_set_windows /
     ab_set_window_refs (include/alyab200.h).  Window indices ascend with the
@@ -272,6 +322,8 @@ def window_arrays(conn: torch.Tensor, N: int, B: int = WINDOW_BLOCK):
     nblk = (E + B - 1) // B
     blk_ptr = torch.searchsorted(wblk, torch.arange(nblk + 1, device=dev, dtype=torch.int64))
     blk_ptr = blk_ptr.to(torch.int64).contiguous()
+    if spread and nn * B <= 4096:
+        order = _spread_slot_banks(order, starts, slot, E, nn, B)
     # window-local index of every (element, node) reference
     uid = torch.cumsum(start.to(torch.int64), 0) - 1
     local = uid - blk_ptr[blk[order]]
