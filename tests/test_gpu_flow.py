@@ -347,3 +347,22 @@ def test_precomputed_filter_width(name):
     dm.clear_filter_width()
     b = assemble_momentum(dm, u, ph).cpu().numpy()
     assert rel_l2(a, b) <= 1e-14
+
+
+@pytest.mark.parametrize("name", ["tet", "mixed"])
+def test_window_tuning_changes_only_rounding(name, monkeypatch):
+    """The bank-aware tet node order (tune_tet_node_order) and the bank-spread
+    reference order inside window runs (_spread_slot_banks) only reorder
+    floating-point sums: K2 with and without them agrees to rounding."""
+    from paper_2005_05899_b200.device import DeviceMesh
+    from paper_2005_05899_b200.ops import assemble_momentum
+    from paper_2005_05899_b200.timestep import FlowParams
+    m = MESHES[name]
+    u, _ = _field(m, seed=6)
+    ph = FlowParams(rho=1.0, mu=0.01, c_vreman=0.07)
+    tuned = assemble_momentum(DeviceMesh(m, reorder="sfc", windows=True), u, ph).cpu().numpy()
+    monkeypatch.setenv("AB_NO_TET_TUNE", "1")
+    monkeypatch.setenv("AB_NO_SLOT_SPREAD", "1")
+    plain = assemble_momentum(DeviceMesh(m, reorder="sfc", windows=True), u, ph).cpu().numpy()
+    assert rel_l2(tuned, plain) <= 1e-13
+    assert rel_l2(tuned, fem.momentum_rhs(m, u, rho=1.0, mu=0.01, c_vreman=0.07)) <= TOL_RHS
