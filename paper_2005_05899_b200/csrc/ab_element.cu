@@ -848,7 +848,7 @@ template <int R> struct OpT<R, OP_DIVERGENCE> { static constexpr int NV = 6, NC 
 template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 3, STRIDE = 4; };
 
 #ifndef PIPE_OCC_K2
-#define PIPE_OCC_K2 4  // C2 K2 graph-timed: 180.0 us at 4 CTAs/SM vs 184.5 at 5 and 182.8 at 6 (session 3)
+#define PIPE_OCC_K2 3  // register cap of the tet4 K2 (launch_bounds min CTAs); the compiler then uses 96 registers and 5 CTAs/SM are resident. C2 bench: 157.3 us vs 159.1 with the cap for 4 (94 regs)
 #endif
 // minimum resident CTAs per SM requested from the register allocator
 template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
