@@ -199,6 +199,7 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 #define AB_RED_RR 1
 #define AB_RED_PQ 2
 #define AB_RED_ITERS 3
+#define AB_RED_FAIL 5  /* sticky failure flag of the decomposed solvers (1.0 = a peer wait timed out) */
 #define AB_SC_RZ 0
 #define AB_SC_BB 1
 int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
@@ -212,18 +213,10 @@ int ab_cg_dot(int64_t n, const double* z, const double* t, double* p, double* q,
 int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r, double* z,
                  const double* own, double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
 
-/* Resident CG: init + up to `maxit` iterations (stop when ||r||/||b|| <=
- * tol, tested on the device; tol = 0 runs exactly maxit) in one cooperative
- * kernel with one CTA per SM; each CTA keeps x, r, z, p, q of its rows in
- * shared memory.  Same iterates as the kernels above.
- * Outputs: x, z (scratch); red[RZN], red[RR], red[ITERS]; sc[BB].  `part`
- * >= 5 * n_cta + 1 doubles (partials + the grid-barrier counter).  ab_cg_resident_fits() returns 1 when n rows fit
- * (and reports the launch shape); ab_cg_resident fails with AB_EINVAL
- * otherwise. */
+/* Launch shape of the resident CG (one cooperative CTA per SM, each owning a
+ * contiguous, slice-aligned row range): returns 1 when the per-CTA rows fit
+ * the shared-memory vectors (x, r, z, p, q), and reports rows_per_cta/n_cta. */
 int ab_cg_resident_fits(int64_t n, int64_t* rows_per_cta, int32_t* n_cta);
-int ab_cg_resident(const ab_sell* a, const double* b_in, double* b_zero, const uint8_t* fixed, const double* dinv,
-                   double* x, double* z, int32_t maxit, double tol, double* red, double* sc, double* part,
-                   void* stream);
 
 /* CTA-local column map of a SELL matrix for the resident CG (DESIGN.md
  * §4.3): CTA b owns rows [b*rows_per_cta, (b+1)*rows_per_cta) (the launch
@@ -246,17 +239,14 @@ typedef struct ab_cg_local {
   const int32_t* ghost;
   const int32_t* perm;       /* [n_rows] or NULL */
   int32_t prefetch_depth;
-  int32_t variant;           /* 0: vectors in shared memory; 1: tensor-memory solver (k_cg_tmem);
-                                2: single-reduction (Chronopoulos-Gear) form (k_cg_cg1) */
-  /* variant 1: the CTA's slices in chunks of `group` slices, each chunk's
-   * values then local columns contiguous: chunk [E0, E1) of entries at byte
-   * 10*E0, values (8 B) first, then columns (2 B). */
-  const unsigned char* packed;
-  int32_t group;
+  int32_t variant;           /* must be 0 (the tensor-memory and single-reduction variants
+                                measured slower and live in tools/lab/cg_rejected_variants.cu) */
+  const unsigned char* packed;  /* reserved (NULL) */
+  int32_t group;                /* reserved (0) */
   int32_t force_mode;        /* variant 0: 0 = best shared-memory plan; 1..4 = the plan of
                                 ab_cg_resident_local_fits (testing: every plan is exercised) */
-  /* variant 2 (single-reduction form, k_cg_cg1): the CTAs owning each CTA's
-   * ghost rows, nbr[nbr_ptr[b] .. nbr_ptr[b+1]) */
+  /* the CTAs owning each CTA's ghost rows, nbr[nbr_ptr[b] .. nbr_ptr[b+1])
+   * (informational; NULL allowed) */
   const int32_t* nbr_ptr;
   const int32_t* nbr;
 } ab_cg_local;
@@ -268,15 +258,15 @@ int ab_debug_timeline(int64_t* buf);
 /* 0: does not fit; otherwise 1 + (x kept in shared memory) + 2 * (the CTA's
  * slice pointers and ghost ids copied to shared memory) */
 int ab_cg_resident_local_fits(int64_t rows_per_cta, int32_t max_ghost);
-/* ab_cg_resident with the z gathers served from shared memory: each CTA
- * fetches its ghost z values once per iteration, the SpMV reads z through
- * the 16-bit local columns.  Same iterates as ab_cg_resident.  `part` >=
+/* Resident Jacobi-PCG: init + up to `maxit` iterations (stop when
+ * ||r||/||b|| <= tol, tested on the device; tol = 0 runs exactly maxit) in
+ * one cooperative kernel, one CTA per SM; each CTA keeps its rows' vectors
+ * on chip (x in tensor memory, r, p, q, z in shared memory), fetches its
+ * ghost z values once per iteration, and the SpMV reads z through the
+ * 16-bit local columns.  Same iterates as the two-kernel form above.
+ * Outputs: x, z (scratch); red[RZN], red[RR], red[ITERS]; sc[BB].  `part` >=
  * 8 * n_cta + 20 * ceil4(n_cta) doubles (grid-barrier counter at 5 * n_cta,
  * replicated partial tables from 8 * n_cta). */
-/* > 0 (ring slots) when the tensor-memory solver (variant 1) fits: vectors
- * x, r, p, q, D^-1 in TMEM, matrix slices streamed by a producer warp into
- * a shared-memory ring with bulk asynchronous copies. */
-int ab_cg_tmem_fits(int64_t rows_per_cta, int32_t max_ghost, int64_t max_width, int32_t group);
 int ab_cg_resident_local(const ab_sell* a, const ab_cg_local* m, const double* b_in, double* b_zero,
                          const uint8_t* fixed, const double* dinv, double* x, double* z, int32_t maxit, double tol,
                          double* red, double* sc, double* part, void* stream);
@@ -341,7 +331,7 @@ typedef struct ab_cg_dd_rank {
   double* red;                        /* RZN, RR, -, ITERS (-1: peer timeout) */
   double* sc;                         /* BB */
   double* part;                       /* >= 6 * n_cta */
-  unsigned* bar;                      /* zeroed before every solve */
+  unsigned* bar;                      /* [2] zeroed before every solve: grid barrier, failure flag */
   /* interface: rows whose partial products are exchanged */
   const uint32_t* ifmask;             /* bit per row */
   const int32_t* send_ptr;            /* [n_rows + 1] per row into send_peer/send_off (interface rows only) */
@@ -355,7 +345,8 @@ typedef struct ab_cg_dd_rank {
   unsigned long long* cnt_in;         /* [n_ranks]: CTAs of rank q done sending (monotone) */
   double* red_in;                     /* [3][n_ranks][2][2]: {value, epoch} records per set, rank, value */
   unsigned long long* evbase;         /* [2]: halo events, reduction epochs completed before this solve */
-  int32_t n_peers, pad1_;
+  int32_t n_peers;
+  int32_t recv_stride;                /* M: recv slot q * M + k holds rank q's k-th value */
   int32_t peer_rank[AB_DD_MAX_PEERS];
   int32_t peer_ncta[AB_DD_MAX_PEERS];
   double* peer_recv[AB_DD_MAX_PEERS];

@@ -80,10 +80,8 @@ _SIGS = {
     "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_resident_fits": ([i64, vp, vp], C.c_int),
-    "ab_cg_resident": ([P(AbSell), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp], C.c_int),
     "ab_cg_resident_local_fits": ([i64, i32], C.c_int),
     "ab_debug_timeline": ([vp], C.c_int),
-    "ab_cg_tmem_fits": ([i64, i32, i64, i32], C.c_int),
     "ab_cg_resident_local": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, i32, f64, vp, vp, vp, vp],
                              C.c_int),
     "ab_gradop_csr": ([P(AbMesh), vp, vp, vp, vp, vp, vp], C.c_int),

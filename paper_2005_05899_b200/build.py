@@ -32,14 +32,38 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """Compile every source to an object in parallel (nvcc per file), then
+    link the shared object."""
     if not force and not _stale():
         return LIB
-    cmd = [NVCC, *FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB)] + [str(CSRC / s) for s in SOURCES]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = res.stdout + res.stderr
+    from concurrent.futures import ThreadPoolExecutor
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    cflags = [f for f in FLAGS if f != "-shared"]
+
+    def compile_one(src: str):
+        obj = objdir / (Path(src).stem + ".o")
+        cmd = [NVCC, *cflags, "-c", "-I", str(ROOT / "include"), "-o", str(obj), str(CSRC / src)]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return obj, r.returncode, r.stdout + r.stderr
+
+    with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, SOURCES))
+    log = "".join(f"== {s}\n{out}" for s, (_o, _rc, out) in zip(SOURCES, results))
+    bad = [s for s, (_o, rc, _out) in zip(SOURCES, results) if rc != 0]
+    if not bad:
+        tmp = LIB.with_suffix(".so.tmp")
+        cmd = [NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp)] + [
+            str(o) for o, _rc, _out in results]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        log += "== link\n" + r.stdout + r.stderr
+        if r.returncode != 0:
+            bad = ["link"]
+        else:
+            os.replace(tmp, LIB)
     (PKG / "build.log").write_text(log)
-    if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{log[-4000:]}")
+    if bad:
+        raise RuntimeError(f"nvcc failed ({bad}):\n{log[-4000:]}")
     if verbose:
         print(log)
     return LIB

@@ -43,11 +43,52 @@ __device__ __forceinline__ unsigned long long ld_acq_sys_u64(const unsigned long
 __device__ __forceinline__ void red_rel_sys_u64(unsigned long long* p, unsigned long long v) {
   asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
+// {value, epoch} record: the value is stored first (relaxed), then the
+// epoch word with release semantics; a reader acquires the epoch and only
+// then loads the value, so a matching epoch always comes with its value (a
+// 16-byte vector access is not single-copy atomic).  A slot is rewritten
+// only after every rank has consumed it (the next write of a set needs the
+// other set's records of every rank, published after their collection).
 __device__ __forceinline__ void st_rec_sys(double* p, double v, double e) {
-  asm volatile("st.relaxed.sys.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v), "d"(e) : "memory");
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+  asm volatile("st.release.sys.global.f64 [%0], %1;" ::"l"(p + 1), "d"(e) : "memory");
 }
-__device__ __forceinline__ void ld_rec_sys(const double* p, double& v, double& e) {
-  asm volatile("ld.relaxed.sys.global.v2.f64 {%0, %1}, [%2];" : "=d"(v), "=d"(e) : "l"(p) : "memory");
+__device__ __forceinline__ double ld_rec_epoch(const double* p) {
+  double e;
+  asm volatile("ld.acquire.sys.global.f64 %0, [%1];" : "=d"(e) : "l"(p + 1) : "memory");
+  return e;
+}
+__device__ __forceinline__ double ld_rec_value(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// Rank-wide failure flag (bar[1], zeroed per solve): a CTA whose peer wait
+// times out raises it; grid barriers give up when it is set and every CTA
+// leaves the iteration loop after the next barrier, so no CTA is left
+// spinning in a barrier its siblings will never reach.
+__device__ __forceinline__ void raise_failure(unsigned* bar) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+}
+__device__ __forceinline__ unsigned failure_flag(unsigned* bar) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar + 1) : "memory");
+  return v;
+}
+__device__ __forceinline__ void dd_grid_barrier(unsigned* bar, unsigned target, int* s_failed) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    unsigned v;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+      if (v >= target) break;
+      if (failure_flag(bar)) { *s_failed = 1; break; }
+    }
+    if (failure_flag(bar)) *s_failed = 1;
+  }
+  __syncthreads();
 }
 
 struct DdCtx {
@@ -69,7 +110,7 @@ __device__ __forceinline__ void dd_publish(const DdCtx& c, double (&v)[NV], int 
   if (threadIdx.x == 0)
 #pragma unroll
     for (int k = 0; k < NV; ++k) part[(size_t)k * c.nb + c.lcta] = v[k];
-  grid_barrier(g.bar, ++nbar * (unsigned)c.nb);
+  dd_grid_barrier(g.bar, ++nbar * (unsigned)c.nb, c.failed);
   all_sum_par<NV>(part, c.nb, sred, bcast, loc);
   const int P = g.n_ranks;
   if (P > 1 && c.lcta == 0 && threadIdx.x == 0) {
@@ -86,7 +127,7 @@ __device__ __forceinline__ void dd_publish(const DdCtx& c, double (&v)[NV], int 
 // totals are summed in rank order (identical on every rank).
 template <int NV>
 __device__ __forceinline__ void dd_collect(const DdCtx& c, int set, double ep, double* bcast, const double (&loc)[NV],
-                                           double (&out)[NV], long long t0) {
+                                           double (&out)[NV]) {
   const ab_cg_dd_rank& g = *c.g;
   const int P = g.n_ranks;
   if (P == 1) {
@@ -101,11 +142,15 @@ __device__ __forceinline__ void dd_collect(const DdCtx& c, int set, double ep, d
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       const double* rec = g.red_in + (((size_t)set * P + threadIdx.x) * 2 + k) * 2;
-      double val, e;
+      double val = 0.0;
+      const long long tw = gtime();  // timeout per wait
       for (;;) {
-        ld_rec_sys(rec, val, e);
-        if (e == ep) break;
-        if (gtime() - t0 > kDdTimeoutNs) { *c.failed = 1; val = 0.0; break; }
+        if (ld_rec_epoch(rec) == ep) { val = ld_rec_value(rec); break; }
+        if (*c.failed || gtime() - tw > kDdTimeoutNs) {
+          *c.failed = 1;
+          raise_failure(g.bar);
+          break;
+        }
       }
       w[k] = val;
     }
@@ -146,7 +191,6 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
   const int lcta = (int)blockIdx.x - g.cta0;
   if (threadIdx.x == 0) s_failed = 0;
   DdCtx c{&g, lcta, g.n_cta, &s_failed};
-  const long long t0 = gtime();
   const int64_t n = g.n_rows;
   const int64_t RB = g.rows_per_cta;
   const int64_t r0 = (int64_t)lcta * RB;
@@ -219,7 +263,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
     block_sum<2, kResBlock>(v, sred);
     ep += 1.0;
     dd_publish<2>(c, v, 0, ep, nbar, sred, bcast, l2);
-    dd_collect<2>(c, 0, ep, bcast, l2, t2, t0);
+    dd_collect<2>(c, 0, ep, bcast, l2, t2);
   }
   double rz = t2[0], rr = t2[1];
   const double bb = rr;
@@ -233,6 +277,9 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
   double epB = 0.0;
   unsigned long long hev = 0;  // halo events of this solve
   for (; it < maxit; ++it) {
+    if (s_failed) break;
+    if (threadIdx.x == 0 && failure_flag(g.bar)) s_failed = 1;
+    __syncthreads();
     if (s_failed) break;
     if (!pending && tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) break;
     for (int k = threadIdx.x; k < ng; k += kResBlock) sz[RB + k] = __ldcg(g.zg + tg[k]);
@@ -258,7 +305,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
       }
     }
     if (pending) {  // reduction B of the previous iteration
-      dd_collect<2>(c, 2, epB, bcast, l2, t2, t0);
+      dd_collect<2>(c, 2, epB, bcast, l2, t2);
       rz_old = rz;
       rz = t2[0];
       rr = t2[1];
@@ -270,8 +317,13 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
       if ((int)threadIdx.x < g.n_peers) {
         const int q = g.peer_rank[threadIdx.x];
         const unsigned long long want = (hbase + hev) * (unsigned long long)g.peer_ncta[threadIdx.x];
+        const long long tw = gtime();
         while (ld_acq_sys_u64(g.cnt_in + q) < want) {
-          if (gtime() - t0 > kDdTimeoutNs) { s_failed = 1; break; }
+          if (s_failed || gtime() - tw > kDdTimeoutNs) {
+            s_failed = 1;
+            raise_failure(g.bar);
+            break;
+          }
         }
       }
     }
@@ -289,7 +341,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
       const int l = sl * 32 + lane;
       if (l < nloc) {
         const double p = fma(beta, spp[l], sz[l]);
-        double q = fma(beta, sq[l], az);
+        double q;
         if ((smask[sl] >> lane) & 1u) {
           const int64_t i = r0 + l;
           // rrow is ascending: find this row's receive range
@@ -298,9 +350,21 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
             const int mid = (lo_k + hi_k) >> 1;
             if (g.rrow[mid] < i) lo_k = mid + 1; else hi_k = mid;
           }
-          for (int e = g.recv_ptr[lo_k]; e < g.recv_ptr[lo_k + 1]; ++e) q += __ldcg(g.recv + g.recv_off[e]);
+          // (A z)_i = sum of the sharing ranks' partials in global rank
+          // order, this rank's at its position: every rank forms the same
+          // bits, so duplicated interface values stay identical
+          double t = 0.0;
+          bool own_added = false;
+          for (int e = g.recv_ptr[lo_k]; e < g.recv_ptr[lo_k + 1]; ++e) {
+            const int off = g.recv_off[e];
+            if (!own_added && off / g.recv_stride > g.rank) { t += az; own_added = true; }
+            t += __ldcg(g.recv + off);
+          }
+          if (!own_added) t += az;
+          q = fma(beta, sq[l], t);
           if ((sown[sl] >> lane) & 1u) pq += p * q;
         } else {
+          q = fma(beta, sq[l], az);
           pq += p * q;  // non-interface rows are owned
         }
         spp[l] = p;
@@ -320,7 +384,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
       block_sum<1, kResBlock>(v, sred);
       ep += 1.0;
       dd_publish<1>(c, v, 1, ep, nbar, sred, bcast, l1);
-      dd_collect<1>(c, 1, ep, bcast, l1, t1, t0);
+      dd_collect<1>(c, 1, ep, bcast, l1, t1);
     }
     const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
     // ---- x += alpha p, r -= alpha q, z = D^-1 r
@@ -356,7 +420,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
     }
   }
   if (pending) {
-    dd_collect<2>(c, 2, epB, bcast, l2, t2, t0);
+    dd_collect<2>(c, 2, epB, bcast, l2, t2);
     rz_old = rz;
     rz = t2[0];
     rr = t2[1];
@@ -376,6 +440,7 @@ __global__ void __launch_bounds__(kResBlock, 1) k_cg_dd(const ab_cg_dd_rank* __r
     g.red[AB_RED_RZN] = rz;
     g.red[AB_RED_RR] = rr;
     g.red[AB_RED_ITERS] = s_failed ? -1.0 : (double)it;
+    if (s_failed) g.red[AB_RED_FAIL] = 1.0;  // sticky until the host clears it
     g.sc[AB_SC_BB] = bb;
     g.evbase[0] = hbase + hev;
     g.evbase[1] = (unsigned long long)ep;

@@ -39,7 +39,7 @@ class AbCgDdRank(C.Structure):
                                       "own", "b_in", "b_zero", "x_out", "zg", "red", "sc", "part", "bar",
                                       "ifmask", "send_ptr", "send_peer", "send_off", "rrow_ptr", "rrow", "recv_ptr",
                                       "recv_off", "recv", "cnt_in", "red_in", "evbase")]
-                + [("n_peers", i32), ("pad1_", i32), ("peer_rank", i32 * MAX_PEERS), ("peer_ncta", i32 * MAX_PEERS),
+                + [("n_peers", i32), ("recv_stride", i32), ("peer_rank", i32 * MAX_PEERS), ("peer_ncta", i32 * MAX_PEERS),
                    ("peer_recv", vp * MAX_PEERS), ("peer_cnt", vp * MAX_PEERS), ("peer_red", vp * MAX_PEERS)])
 
 
@@ -165,6 +165,7 @@ class DDRank:
         s.recv, s.cnt_in, s.red_in, s.evbase = ptr(self.recv), ptr(self.cnt_in), ptr(self.red_in), ptr(self.evbase)
         s.pad0_ = 1 if getattr(self, "same_device", False) else 0
         s.n_peers = len(self.peers)
+        s.recv_stride = max(1, self.M)
         for k, q in enumerate(self.peers):
             s.peer_rank[k] = q
             s.peer_ncta[k] = self.peer_ncta_[q]
@@ -255,10 +256,26 @@ class FusedDDSolver:
         return self.rank.x
 
     def solve(self, b: torch.Tensor, maxit: int, tol: float = 0.0):
+        """With tol > 0 the iteration count is read back (host sync) and a
+        failed solve raises at once; with tol == 0 nothing synchronises and a
+        failure stays recorded in the sticky device flag (see check())."""
         assert b.data_ptr() == self.b.data_ptr(), "the fused solver is bound to its right-hand side buffer"
         self.launch.run(maxit, tol)
-        it = self.rank.iterations if tol > 0 else maxit
-        return self.rank.x, it
+        if tol > 0:
+            it = self.rank.iterations
+            if it < 0:
+                self.check()
+            return self.rank.x, it
+        return self.rank.x, maxit
+
+    def check(self):
+        """Raise if any solve since the last check timed out waiting for a
+        peer (red[AB_RED_FAIL], set by the kernel).  The iterate of such a
+        solve is meaningless, and the cross-rank counters are out of step, so
+        the fused solver cannot be used again."""
+        if float(self.rank.red[5].item()) != 0.0:
+            raise RuntimeError("fused decomposed CG: a peer wait timed out (ranks out of step); "
+                               "the pressure increment of that step is invalid")
 
 
 def virtual_ranks(ranks: list):

@@ -152,15 +152,13 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
     if rows_per_cta + max_ghost > 65536:
         return None
     lcols = torch.where(lc >= 32768, lc - 65536, lc).to(torch.int16).contiguous()
-    # CTAs owning each CTA's ghost rows (single-reduction solver's z flags)
+    # CTAs owning each CTA's ghost rows (informational)
     owner = (uk % n) // rows_per_cta
     pair = torch.unique(g_cta * n_cta + owner)
     nbr = (pair % n_cta).to(torch.int32).contiguous()
     nbr_ptr = torch.zeros(n_cta + 1, dtype=torch.int64, device=dev)
     nbr_ptr[1:] = torch.cumsum(torch.bincount(pair // n_cta, minlength=n_cta), 0)
     nbr_ptr = nbr_ptr.to(torch.int32).contiguous()
-    if int((nbr_ptr[1:] - nbr_ptr[:-1]).max().item()) > 1024:
-        return None
     ghost_ptr = ghost_ptr.to(torch.int32).contiguous()
     if ghost.numel() == 0:  # no remote columns at all: keep a valid (unused) array
         ghost = torch.zeros(1, dtype=torch.int32, device=dev)
@@ -170,33 +168,6 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
                        ghost_ptr=ptr(ghost_ptr), ghost=ptr(ghost), nbr_ptr=ptr(nbr_ptr), nbr=ptr(nbr))
     return dict(cols=lcols, ghost_ptr=ghost_ptr, ghost=ghost, max_ghost=max_ghost, struct=struct, nbr=nbr,
                 nbr_ptr=nbr_ptr)
-
-
-def pack_chunks(A: SellMatrix, lcols: torch.Tensor, rows_per_cta: int, group: int) -> torch.Tensor:
-    """Packed matrix stream of the tensor-memory solver (ab_cg_local.packed):
-    the slices of every CTA in chunks of ``group``; chunk [E0, E1) of entries
-    occupies bytes [10 E0, 10 E1): its values, then its 16-bit columns."""
-    sp = A.slice_ptr
-    dev = A.vals.device
-    total = int(sp[-1].item())
-    n_sl = sp.numel() - 1
-    spc = rows_per_cta // 32
-    s = torch.arange(n_sl, device=dev)
-    b = s // spc
-    c_end = torch.minimum(torch.minimum(b * spc + (s - b * spc) // group * group + group, (b + 1) * spc),
-                          torch.full_like(s, n_sl))
-    c_beg = b * spc + (s - b * spc) // group * group
-    counts = sp[1:] - sp[:-1]
-    e = torch.arange(total, device=dev)
-    slice_of = torch.repeat_interleave(s, counts)
-    E0 = sp[c_beg][slice_of]
-    E1 = sp[c_end][slice_of]
-    packed = torch.zeros(total * 10, dtype=torch.uint8, device=dev)
-    pv = packed.view(torch.float64)
-    pc = packed.view(torch.int16)
-    pv[(E0 // 32) * 40 + (e - E0)] = A.vals
-    pc[5 * E0 + 4 * (E1 - E0) + (e - E0)] = lcols
-    return packed
 
 
 def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
@@ -262,9 +233,8 @@ class PCG:
     """
 
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
-                 own: torch.Tensor | None = None, halo=None, resident: bool = True, local: bool = True,
-                 order: torch.Tensor | None = None, prefetch_depth: int = 1,
-                 tmem: bool = False, group: int = 0, single_reduction: bool = False, force_mode: int = 0,
+                 own: torch.Tensor | None = None, halo=None, resident: bool = True,
+                 order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
                  reorder_two_kernel: bool = True):
         self.A = A
         n = A.n_rows
@@ -290,15 +260,14 @@ class PCG:
         self.cnt = torch.zeros(ng + 2, dtype=torch.int32, device=dev)
         self.launches_per_iter = 2 if halo is None else 3
         self.mark = None  # optional event recorder (FlowSolver._mark)
-        # single-domain solves run as one cooperative kernel when the rows fit
-        # in shared memory (ab_cg_resident); otherwise two kernels/iteration
-        self.resident = bool(resident and halo is None and fits)
-        # ... with the z gathers served from shared memory (ab_cg_resident_local)
+        # single-domain solves run as ONE cooperative kernel when every CTA's
+        # rows and ghost rows fit on chip (ab_cg_resident_local, z gathers
+        # served from shared memory); otherwise two kernels per iteration.
         # ``order`` (node id per solver row, e.g. an SFC order of the nodes)
         # renumbers the system P A P^T so every CTA's rows are compact and its
         # ghost set small; b and x stay in node order.
         self.local = None
-        if self.resident and local:
+        if resident and halo is None and fits:
             Ap, perm = A, None
             if order is not None:
                 perm = order.to(device=dev, dtype=torch.int32).contiguous()
@@ -310,22 +279,12 @@ class PCG:
                 m["struct"].perm = ptr(perm)
                 m["struct"].prefetch_depth = int(prefetch_depth)
                 m["struct"].force_mode = int(force_mode)
-                # tensor-memory solver when it fits (ab_cg_tmem_fits)
-                group = int(group) if group else max(1, -(-16384 // max(1, Ap.max_width * 256)))
-                m["tmem"] = bool(tmem and lib().ab_cg_tmem_fits(rb.value, m["max_ghost"], Ap.max_width, group) > 0)
-                m["struct"].variant = 1 if m["tmem"] else 0
-                m["cg1"] = bool(single_reduction and not m["tmem"])
-                if m["cg1"]:
-                    m["struct"].variant = 2
-                if m["tmem"]:
-                    m["packed"] = pack_chunks(Ap, m["cols"], rb.value, group)
-                    m["struct"].packed = ptr(m["packed"])
-                    m["struct"].group = group
                 pl = perm.to(torch.int64) if perm is not None else None
                 m["dinv"] = dinv[pl].contiguous() if pl is not None else dinv
                 m["fixed"] = (self.fixed[pl].contiguous() if (pl is not None and self.fixed is not None)
                               else self.fixed)
                 self.local = m
+        self.resident = self.local is not None
         # two-kernel single-domain solves in the ``order`` row numbering (P A P^T;
         # on C3 an SFC order cuts the SELL padding 4.7% and the iteration 7%)
         self.perm2 = None
@@ -351,13 +310,6 @@ class PCG:
                 call("ab_cg_resident_local", ctypes.byref(lm["A"].struct), ctypes.byref(lm["struct"]), ptr(b),
                      ptr(b) if zero_b else None, ptr(lm["fixed"]), ptr(lm["dinv"]), ptr(self.x), ptr(self.z),
                      int(maxit), float(tol), ptr(self.red), ptr(self.sc), ptr(self.part), s)
-            it = int(self.red[3].item()) if tol > 0 else maxit
-            return self.x, it
-        if self.resident:
-            with self._m("K5_cg_resident"):
-                call("ab_cg_resident", A, ptr(b), ptr(b) if zero_b else None, ptr(self.fixed), ptr(self.dinv),
-                     ptr(self.x), ptr(self.z), int(maxit), float(tol), ptr(self.red), ptr(self.sc),
-                     ptr(self.part), s)
             it = int(self.red[3].item()) if tol > 0 else maxit
             return self.x, it
         if self.perm2 is not None:

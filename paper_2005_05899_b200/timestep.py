@@ -288,7 +288,8 @@ class FlowSolver:
                   graph: bool = True):
         """End-to-end call with HOST buffers (pinned for async copies): upload
         (u, p), advance one step, download (u, p) in place.  p goes first and
-        G p^n is assembled on a side stream while u is still uploading."""
+        G p^n is assembled on a side stream while u is still uploading.
+        Returns after the download has completed (u_host, p_host are valid)."""
         main = torch.cuda.current_stream()
         if self._side is None:
             self._side = torch.cuda.Stream()
@@ -304,6 +305,16 @@ class FlowSolver:
         self.step(dt, cg_iters, graph=graph)
         u_host.copy_(self.U0[:, :3], non_blocking=True)
         p_host.copy_(self.P, non_blocking=True)
+        # the host buffers are read by the caller on return
+        main.synchronize()
+        self.check_health()
+
+    def check_health(self):
+        """Raise if a fused decomposed pressure solve failed since the last
+        check (device-side sticky flag; a host read, so call it outside
+        timed loops or where the step synchronises anyway)."""
+        if self.ddcg is not None:
+            self.ddcg.check()
 
     def step(self, dt: float, cg_iters: int = 50, cg_tol: float = 0.0, graph: bool = False):
         """Advance one step.  ``graph=True`` (fixed iterations, no halo)

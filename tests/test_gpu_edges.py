@@ -67,7 +67,7 @@ def test_empty_mesh_packs():
 
 
 @pytest.mark.parametrize("cells", [(1, 1, 1), (3, 2, 5), (2, 7, 3)])
-@pytest.mark.parametrize("variant", ["local", "resident", "two-kernel"])
+@pytest.mark.parametrize("variant", ["local", "local-node-order", "two-kernel"])
 def test_ragged_small_systems(cells, variant):
     """Row counts below 148 CTAs / not a multiple of the slice height."""
     from paper_2005_05899_b200.device import DeviceMesh
@@ -84,7 +84,7 @@ def test_ragged_small_systems(cells, variant):
     b[fixed] = 0.0
     dm = DeviceMesh(m)
     A = assemble_laplacian(dm, torch.from_numpy(fixed))
-    kw = {"local": dict(order=dm.node_order()), "resident": dict(local=False), "two-kernel": dict(resident=False)}
+    kw = {"local": dict(order=dm.node_order()), "local-node-order": dict(), "two-kernel": dict(resident=False)}
     pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), **kw[variant])
     x, it = pcg.solve(torch.from_numpy(b).cuda(), 5, zero_b=False)
     xr, _, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 5)

@@ -142,10 +142,7 @@ def test_laplacian_and_spmv(name):
 
 CG_VARIANTS = {
     "local-sfc": dict(order=True),          # ab_cg_resident_local, SFC row order, z gathers from shared memory
-    "tmem": dict(order=True, tmem=True),    # tensor-memory vectors + bulk-copy matrix stream (k_cg_tmem)
-    "cg1": dict(order=True, single_reduction=True),  # Chronopoulos-Gear single-reduction form (k_cg_cg1)
     "local": dict(),                        # local column map, node order
-    "resident": dict(local=False),          # k_cg_resident (L2 gathers)
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
     "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on P A P^T (SFC row order)
 }
@@ -172,8 +169,8 @@ def test_pcg_fixed_iterations_and_convergence(name, variant):
     pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed), **kw)
     assert pcg.resident == (not variant.startswith("two-kernel"))
     assert (pcg.perm2 is not None) == (variant == "two-kernel-sfc")
-    if variant in ("local-sfc", "tmem", "local", "cg1"):
-        assert pcg.local is not None and pcg.local["tmem"] == (variant == "tmem")
+    if variant in ("local-sfc", "local"):
+        assert pcg.local is not None
     bt = torch.from_numpy(b).cuda()
     x, it = pcg.solve(bt.clone(), 7)
     xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 7)

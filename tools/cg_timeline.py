@@ -17,7 +17,7 @@ fixed = torch.from_numpy(meshgen.boundary_nodes(m))
 dm = DeviceMesh(m)
 A = assemble_laplacian(dm, fixed)
 depth = int(sys.argv[2]) if len(sys.argv) > 2 else 1
-pcg = PCG(A, 1.0 / A.diag, fixed=fixed, order=dm.node_order(), tmem=False, prefetch_depth=depth)
+pcg = PCG(A, 1.0 / A.diag, fixed=fixed, order=dm.node_order(), prefetch_depth=depth)
 b = torch.randn(A.n_rows, dtype=torch.float64, device="cuda")
 b[fixed.cuda()] = 0
 tl = torch.zeros(148 * 8, dtype=torch.int64, device="cuda")

@@ -16,7 +16,7 @@ m = meshgen.box_tets(n, n, n, jitter=0.2, seed=20200131)
 fixed = torch.from_numpy(meshgen.boundary_nodes(m))
 dm = DeviceMesh(m)
 A = assemble_laplacian(dm, fixed)
-kw = {"local": dict(order=dm.node_order()), "resident": dict(local=False), "two": dict(resident=False)}[kind]
+kw = {"local": dict(order=dm.node_order()), "two": dict(resident=False)}[kind]
 pcg = PCG(A, 1.0 / A.diag, fixed=fixed, **kw)
 b = torch.randn(A.n_rows, dtype=torch.float64, device="cuda")
 b[fixed.cuda()] = 0

@@ -24,12 +24,9 @@ flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 order = dm.node_order()
 depths = [int(k) for k in sys.argv[2].split(",")] if len(sys.argv) > 2 else []
 variants = {
-    "cg1": dict(order=order, single_reduction=True),
-    "tmem": dict(order=order, tmem=True),
-    "local+sfc": dict(order=order, tmem=False),
-    **{f"depth{k}": dict(order=order, prefetch_depth=k, tmem=False) for k in depths},
+    "local+sfc": dict(order=order),
+    **{f"depth{k}": dict(order=order, prefetch_depth=k) for k in depths},
     "local": dict(),
-    "resident": dict(local=False),
     "two-kernel": dict(resident=False),
 }
 ref = None
@@ -37,7 +34,7 @@ for name, kw in variants.items():
     pcg = PCG(A, dinv, fixed=fixed, **kw)
     info = ""
     if pcg.local is not None:
-        info = f"cg1={pcg.local.get('cg1')} tmem={pcg.local['tmem']} group={pcg.local['struct'].group} max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
+        info = f"max_ghost={pcg.local['max_ghost']} stored={pcg.local['A'].nnz_stored}"
     pcg.solve(b.clone(), its, zero_b=False)
     torch.cuda.synchronize()
     g = torch.cuda.CUDAGraph()
