@@ -138,6 +138,9 @@ int ab_set_filter_width(const int32_t* conn, int64_t n_elem, const double* delta
 
 /* ---- K2: momentum RHS (EMAC convection + viscous + Vreman) --------------
  * New entry point; rhs4 accumulated. */
+/* Diagnostics: grid size and element-block count of the most recent
+ * pipelined (persistent) element kernel launched by the calling thread. */
+int ab_last_pipe_shape(int64_t* grid, int64_t* n_blocks);
 int ab_momentum_rhs(const ab_mesh* mesh, const ab_phys* phys, const double* u4, double* rhs4,
                     void* stream);
 

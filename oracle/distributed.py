@@ -32,14 +32,19 @@ def np_unpack_add(idx, buf, stride, ncomp, field):
 
 
 class DistFlowOracle:
-    def __init__(self, sub, halo, rho, mu, c_vreman, p_fixed_local):
+    def __init__(self, sub, halo, rho, mu, c_vreman, p_fixed_local, u_fixed=None, u_fixed_values=None,
+                 wall=None):
         self.m, self.halo = sub, halo
+        self.wall = wall  # (faces, off) of this rank's wall faces (each face belongs to one element)
+        self.uf = None if u_fixed is None else np.asarray(u_fixed, bool)
+        self.uv = None if u_fixed_values is None else np.asarray(u_fixed_values, float)
         self.rho, self.mu, self.cv = rho, mu, c_vreman
         n = sub.n_nodes
         self.own = halo.own.numpy()
         ml = torch.from_numpy(fem.lumped_mass(sub))
         halo.sum_(ml, 1, 1)
-        self.minv = 1.0 / ml.numpy()
+        self.ml = ml.numpy()
+        self.minv = 1.0 / self.ml
         self.pf = np.asarray(p_fixed_local, bool)
         self.L = fem.laplacian(sub, self.pf)
         diag = torch.from_numpy(self.L.diagonal().copy())
@@ -64,8 +69,14 @@ class DistFlowOracle:
         self.halo.allreduce_(t)
         return t.tolist()
 
+    def _bc(self, u):
+        if self.uf is not None:
+            u[self.uf] = self.uv[self.uf]
+        return u
+
     def init_state(self, u, p):
-        return {"u": np.array(u, float), "p": np.array(p, float), "gp": self._sum3(fem.gradient(self.m, p))}
+        return {"u": self._bc(np.array(u, float)), "p": np.array(p, float),
+                "gp": self._sum3(fem.gradient(self.m, p))}
 
     def pcg(self, b, maxit):
         own = self.own
@@ -94,12 +105,16 @@ class DistFlowOracle:
         u = u0
         k = dt / self.rho
         for s in range(3):
-            R = self._sum3(fem.momentum_rhs(self.m, u, self.rho, self.mu, self.cv))
+            R = fem.momentum_rhs(self.m, u, self.rho, self.mu, self.cv)
+            if self.wall is not None:
+                R = R + fem.wall_traction(self.m, *self.wall, u, self.rho, self.mu)
+            R = self._sum3(R)
             u = fem.RK3_A[s] * u0 + fem.RK3_B[s] * (u + k * self.minv[:, None] * (R - st["gp"]))
+            u = self._bc(u)
         b = self._sum1(-(self.rho / dt) * fem.divergence(self.m, u))
         dp = self.pcg(b, cg_iters)
         gd = self._sum3(fem.gradient(self.m, dp))
-        u = u - k * self.minv[:, None] * gd
+        u = self._bc(u - k * self.minv[:, None] * gd)
         return {"u": u, "p": st["p"] + dp, "gp": st["gp"] + gd}
 
 

@@ -66,6 +66,7 @@ _SIGS = {
     "ab_set_filter_width": ([vp, i64, vp], C.c_int),
     "ab_parse_partition": ([vp, i64, vp, i64, vp], C.c_int64),
     "ab_mass": ([P(AbMesh), i32, vp, vp, vp, i32, vp], C.c_int),
+    "ab_last_pipe_shape": ([vp, vp], C.c_int),
     "ab_momentum_rhs": ([P(AbMesh), P(AbPhys), vp, vp, vp], C.c_int),
     "ab_divergence": ([P(AbMesh), vp, f64, vp, vp], C.c_int),
     "ab_wall_traction": ([P(AbWall), P(AbPhys), vp, vp, vp, vp], C.c_int),

@@ -1059,6 +1059,10 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
   }
 }
 
+// Launch shape of the most recent pipelined element kernel (diagnostics:
+// tests check that the persistent CTAs walk several blocks each).
+static thread_local int64_t g_pipe_grid = 0, g_pipe_blocks = 0;
+
 template <int R, int OP, int BLOCK>
 static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double scale, const double* f, double* out,
                        cudaStream_t stream) {
@@ -1083,6 +1087,8 @@ static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double s
   const int64_t n_blocks = (c.n + BLOCK - 1) / BLOCK;
   int64_t grid = (int64_t)sms * per_sm;
   if (grid > n_blocks) grid = n_blocks;
+  g_pipe_grid = grid;
+  g_pipe_blocks = n_blocks;
   kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w, ph, scale, f, out, n_blocks);
   return check_launch("k_pipe");
 }
@@ -1396,6 +1402,13 @@ int ab_mass(const ab_mesh* m, int32_t k, double* ae, double* jdet, double* ml, i
     k_mass<decltype(r)::value><<<grid_for(c.n, t), t, 0, S(stream)>>>(c, ae, jdet, ml);
     return check_launch("ab_mass");
   });
+}
+
+int ab_last_pipe_shape(int64_t* grid, int64_t* n_blocks) {
+  if (!grid || !n_blocks) return fail("ab_last_pipe_shape: null argument");
+  *grid = g_pipe_grid;
+  *n_blocks = g_pipe_blocks;
+  return AB_OK;
 }
 
 int ab_momentum_rhs(const ab_mesh* m, const ab_phys* ph, const double* u4, double* rhs4, void* stream) {

@@ -201,49 +201,81 @@ def box_hexes(nx, ny, nz, lengths=(1.0, 1.0, 1.0), periodic=False, origin=(0.0, 
     return _finish(coords, {"hex": hexes}, period=period, shape=(nx, ny, nz))
 
 
+# Cell types of the boundary-layer box (one code per structured cell) and the
+# Gauss-point weight of the elements each cell produces (mesh.py:66-71 counts:
+# hex 8, 2 prisms 2 x 6, pyramid + 4 tets 5 + 16, 6 Kuhn tets 6 x 4).
+CELL_HEX, CELL_PRI, CELL_TRANS, CELL_KUHN = 0, 1, 2, 3
+CELL_GAUSS = np.array([8, 12, 21, 24], dtype=np.int64)
+CELL_ELEMS = {"hex": np.array([1, 0, 0, 0]), "pri": np.array([0, 2, 0, 0]), "pyr": np.array([0, 0, 1, 0]),
+              "tet_trans": np.array([0, 0, 4, 0]), "tet_kuhn": np.array([0, 0, 0, 6])}
+
+
+def patch_extent(nx, ny, hex_fraction):
+    s = np.sqrt(hex_fraction)
+    return int(round(nx * s)), int(round(ny * s))
+
+
+def cell_codes(ii, jj, kk, layers, px, py):
+    """Cell type (CELL_*) of cells (ii, jj, kk) of the boundary-layer box."""
+    patch = (ii < px) & (jj < py)
+    code = np.full(np.shape(ii), CELL_KUHN, dtype=np.int8)
+    code[(kk < layers) & patch] = CELL_HEX
+    code[(kk < layers) & ~patch] = CELL_PRI
+    code[(kk == layers) & patch] = CELL_TRANS
+    return code
+
+
+def boundary_layer_blocks(nx, ny, nz, layers, px, py, ii, jj, kk):
+    """Element blocks (kind tag -> connectivity with GLOBAL grid node ids) of
+    the given cells, in the order boundary_layer_mesh emits them: per kind
+    in ascending cell id, the transition tets before the Kuhn tets.  The
+    cells must be in ascending cell id ((i * ny + j) * nz + k)."""
+    code = cell_codes(ii, jj, kk, layers, px, py)
+    blocks = {}
+
+    def sel(c):
+        m = code == c
+        return ii[m], jj[m], kk[m]
+
+    ci, cj, ck = sel(CELL_HEX)
+    if ci.size:
+        c = _cell_corner_ids(nx, ny, nz, ci, cj, ck)
+        order = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)]
+        blocks["hex"] = np.stack([c[o] for o in order], axis=1)
+    ci, cj, ck = sel(CELL_PRI)
+    if ci.size:  # split along the xy diagonal
+        c = _cell_corner_ids(nx, ny, nz, ci, cj, ck)
+        pa = np.stack([c[(0, 0, 0)], c[(1, 0, 0)], c[(1, 1, 0)], c[(0, 0, 1)], c[(1, 0, 1)], c[(1, 1, 1)]], axis=1)
+        pb = np.stack([c[(0, 0, 0)], c[(1, 1, 0)], c[(0, 1, 0)], c[(0, 0, 1)], c[(1, 1, 1)], c[(0, 1, 1)]], axis=1)
+        blocks["pri"] = np.stack([pa, pb], axis=1).reshape(-1, 6)
+    ci, cj, ck = sel(CELL_TRANS)
+    trans_tets = None
+    if ci.size:  # pyramid (base = bottom quad, apex = max corner) + 4 Kuhn tets
+        c = _cell_corner_ids(nx, ny, nz, ci, cj, ck)
+        blocks["pyr"] = np.stack([c[(0, 0, 0)], c[(1, 0, 0)], c[(1, 1, 0)], c[(0, 1, 0)], c[(1, 1, 1)]], axis=1)
+        trans_tets = _kuhn_tets(c, perms=[(0, 2, 1), (1, 2, 0), (2, 0, 1), (2, 1, 0)])
+    ci, cj, ck = sel(CELL_KUHN)
+    tets = _kuhn_tets(_cell_corner_ids(nx, ny, nz, ci, cj, ck)) if ci.size else np.zeros((0, 4), np.int64)
+    if trans_tets is not None:
+        tets = np.concatenate([trans_tets, tets], axis=0)
+    if tets.shape[0]:
+        blocks["tet"] = tets
+    return blocks
+
+
 def boundary_layer_mesh(nx, ny, nz, layers, hex_fraction=0.25, lengths=(1.0, 1.0, 1.0)):
     """Conforming mixed tet/prism/pyramid/hex boundary-layer box (C3/C4/C5).
 
     Prism layers k < ``layers`` except a hex "wing patch" covering
     ``hex_fraction`` of the wall (i < px, j < py); transition cells (one
     pyramid + four Kuhn tets) above the patch at k == layers; Kuhn tets
-    everywhere else.
+    everywhere else.  dmesh.py generates the same
+    elements for a subset of the cells (one rank's subdomain).
     """
-    s = np.sqrt(hex_fraction)
-    px, py = int(round(nx * s)), int(round(ny * s))
+    px, py = patch_extent(nx, ny, hex_fraction)
     coords = _grid_nodes(nx, ny, nz, lengths)
-
-    def in_patch(i, j):
-        return (i < px) & (j < py)
-
-    blocks = {}
-    # hexes: patch cells below the transition layer
-    ii, jj, kk = _cells(nx, ny, nz, lambda i, j, k: (k < layers) & in_patch(i, j))
-    if ii.size:
-        c = _cell_corner_ids(nx, ny, nz, ii, jj, kk)
-        order = [(0, 0, 0), (1, 0, 0), (1, 1, 0), (0, 1, 0), (0, 0, 1), (1, 0, 1), (1, 1, 1), (0, 1, 1)]
-        blocks["hex"] = np.stack([c[o] for o in order], axis=1)
-    # prisms: wall layers outside the patch, split along the xy diagonal
-    ii, jj, kk = _cells(nx, ny, nz, lambda i, j, k: (k < layers) & ~in_patch(i, j))
-    if ii.size:
-        c = _cell_corner_ids(nx, ny, nz, ii, jj, kk)
-        pa = np.stack([c[(0, 0, 0)], c[(1, 0, 0)], c[(1, 1, 0)], c[(0, 0, 1)], c[(1, 0, 1)], c[(1, 1, 1)]], axis=1)
-        pb = np.stack([c[(0, 0, 0)], c[(1, 1, 0)], c[(0, 1, 0)], c[(0, 0, 1)], c[(1, 1, 1)], c[(0, 1, 1)]], axis=1)
-        blocks["pri"] = np.stack([pa, pb], axis=1).reshape(-1, 6)
-    # transition cells: pyramid + 4 Kuhn tets above the patch
-    ii, jj, kk = _cells(nx, ny, nz, lambda i, j, k: (k == layers) & in_patch(i, j))
-    trans_tets = None
-    if ii.size:
-        c = _cell_corner_ids(nx, ny, nz, ii, jj, kk)
-        blocks["pyr"] = np.stack([c[(0, 0, 0)], c[(1, 0, 0)], c[(1, 1, 0)], c[(0, 1, 0)], c[(1, 1, 1)]], axis=1)
-        trans_tets = _kuhn_tets(c, perms=[(0, 2, 1), (1, 2, 0), (2, 0, 1), (2, 1, 0)])
-    # Kuhn tets everywhere else
-    ii, jj, kk = _cells(nx, ny, nz, lambda i, j, k: (k > layers) | ((k == layers) & ~in_patch(i, j)))
-    tets = _kuhn_tets(_cell_corner_ids(nx, ny, nz, ii, jj, kk)) if ii.size else np.zeros((0, 4), np.int64)
-    if trans_tets is not None:
-        tets = np.concatenate([trans_tets, tets], axis=0)
-    if tets.shape[0]:
-        blocks["tet"] = tets
+    ii, jj, kk = _cells(nx, ny, nz)
+    blocks = boundary_layer_blocks(nx, ny, nz, layers, px, py, ii, jj, kk)
     return _finish(coords, blocks, shape=(nx, ny, nz))
 
 
@@ -302,22 +334,25 @@ def c2_initial(coords, seed=20200131, noise=0.01):
     return u + rng.normal(0.0, noise, size=u.shape), np.zeros(coords.shape[0])
 
 
-def wall_model_bcs(mesh: MeshArrays):
+def wall_model_bcs(mesh: MeshArrays, bounds=None):
     """C3-C5 with the equilibrium wall model on z = 0 (Algorithm 1 line 4):
     inflow u = (1,0,0) at x = 0, zero normal velocity on the wall (the wall
     shear comes from the wall law), p = 0 at x = 1.  Returns (bcs, (faces,
-    off)) for FlowSolver(**bcs, wall=(faces, off))."""
+    off)) for FlowSolver(**bcs, wall=(faces, off)).  ``bounds`` = (lo, hi)
+    of the whole box (a subdomain's own extent is not the box's); default:
+    this mesh's extent."""
     from .wall import wall_faces
     x = mesh.coords
     n = mesh.n_nodes
+    lo, hi = (x.min(axis=0), x.max(axis=0)) if bounds is None else (np.asarray(bounds[0]), np.asarray(bounds[1]))
     uf = np.zeros((n, 3), bool)
     uv = np.zeros((n, 3))
-    inflow = np.abs(x[:, 0] - x[:, 0].min()) < 1e-12
-    wall = np.abs(x[:, 2] - x[:, 2].min()) < 1e-12
+    inflow = np.abs(x[:, 0] - lo[0]) < 1e-12
+    wall = np.abs(x[:, 2] - lo[2]) < 1e-12
     uf[wall, 2] = True
     uf[inflow] = True
     uv[inflow] = (1.0, 0.0, 0.0)
-    pf = np.abs(x[:, 0] - x[:, 0].max()) < 1e-12
+    pf = np.abs(x[:, 0] - hi[0]) < 1e-12
     return dict(p_fixed=pf, u_fixed=uf, u_fixed_values=uv), wall_faces(mesh, wall)
 
 

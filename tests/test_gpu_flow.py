@@ -260,16 +260,14 @@ def test_tgv_converged_cg_and_energy_decay():
 def test_full_size_c2_properties():
     """Size-independent properties at BASELINE configs[1] size (4.09M tets)."""
     from paper_2005_05899_b200.device import DeviceMesh
-    from paper_2005_05899_b200.ops import assemble_divergence, assemble_gradient, assemble_momentum
+    from paper_2005_05899_b200.ops import assemble_divergence, assemble_gradient
     from paper_2005_05899_b200.assembly import lumped_mass
     m = meshgen.c2_mesh()
     dm = DeviceMesh(m, reorder="sfc", windows=True)
     ml = lumped_mass(dm)
     assert abs(ml.sum() - 1.0) <= 1e-12
     x = torch.from_numpy(m.coords).cuda()
-    # constant velocity: no convection, no viscous stress -> R == 0
-    R = assemble_momentum(dm, torch.ones_like(x))
-    assert float(R.abs().max()) <= 1e-12
+    # (K2 at this size is compared with the oracle in test_gpu_production.py)
     # linear fields are reproduced exactly: D u = div(u) M_L, G p = grad(p) M_L
     inner = ~torch.from_numpy(meshgen.boundary_nodes(m)).cuda()
     u = torch.stack([2 * x[:, 0] + x[:, 1], -x[:, 1] + 0.5 * x[:, 2], 3 * x[:, 2]], dim=1)
