@@ -1,13 +1,22 @@
 """Benchmark of the time-step hot path (BASELINE.json metric: M element-steps/s).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2|c3] [--impl native|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c4|c5|c3|c2] [--weak]
+                    [--impl native|reference]
 
-A "step" is one full fractional time step (3 x K2+K3, K4, PCG with a fixed
-50 iterations, K6, K7) over the whole mesh; the unit of work is one element
-through one step.  N = 1 runs BASELINE configs[1] (C2: jittered Kuhn TET04
-box, 88^3 cells = 4,088,832 elements).  N > 1 (torchrun, one rank per GPU,
-NCCL) runs weak scaling: an (88 N) x 88 x 88 box split by the SFC partitioner
-into N subdomains of ~4.09M elements with NCCL interface sums.
+A "step" is one full fractional time step (Algorithm 1: 3 x (K2 + K8 wall
+model + K3), K4, PCG with a fixed 50 iterations, K6 + K7) over the whole
+mesh; the unit of work is one element through one step.
+
+Default workload: C4 (BASELINE configs[3], the config the metric's 1/2/4/8
+quotes): the ~249M-element mixed tet/prism/pyramid/hex boundary-layer box.
+N = 1 runs it on one GPU (68 GB of HBM); N > 1 (torchrun, one rank per GPU)
+runs STRONG scaling: the cells are split along a Hilbert curve
+(dmesh.partition_cells, the reference's split_1d rule on cell bins) and every
+rank generates only its own subdomain; after one calibration the split is
+re-done with lambda_i = P theta_i / sum(theta) from the measured K2
+throughput (the paper's DLB analog).  ``--weak`` runs C5 (BASELINE
+configs[4]: 150 x 150 x (237 P + 21) cells, ~32M elements per GPU).
+``--workload c2`` keeps round 1's C2 line (4.09M jittered tets).
 
 Timing: W untimed warm-up steps; K timed steps, each bracketed by CUDA events
 on the launching stream, with a 512 MB L2 flush (untimed) between steps;
@@ -42,7 +51,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--workload", default="c2", choices=["c2", "c3", "c4"])
+    ap.add_argument("--workload", default="c4", choices=["c2", "c3", "c4", "c5"])
+    ap.add_argument("--weak", action="store_true", help="weak scaling: C5 (32M elements per GPU)")
+    ap.add_argument("--no-c2", action="store_true", help="N=1: skip the extra C2 reference point")
     ap.add_argument("--cg-iters", type=int, default=CG_ITERS)
     ap.add_argument("--no-graph", action="store_true")
     ap.add_argument("--no-windows", action="store_true")
@@ -59,38 +70,58 @@ def dist_env():
     return ws, rank, local
 
 
-def build_workload(name: str, n_ranks: int):
-    from paper_2005_05899_b200 import meshgen
+PHYS = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
+
+
+def workload_spec(name: str, n_ranks: int):
+    """(BoxSpec, description, scaling) of a boundary-layer workload."""
+    from paper_2005_05899_b200 import dmesh
+    if name == "c4":
+        return (dmesh.c4_spec(), "C4: ~250M-element mixed tet/prism/pyramid/hex boundary-layer box "
+                                 "(BASELINE configs[3]), strong scaling", "strong")
+    if name == "c5":
+        return (dmesh.c5_spec(n_ranks), "C5: ~32M mixed elements per GPU, throughput-weighted repartitioning "
+                                        "(BASELINE configs[4]), weak scaling", "weak")
+    return (dmesh.c3_spec(n_ranks ** (1.0 / 3.0)),
+            "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2]), scaled by P^(1/3)", "weak")
+
+
+def build_rank_workload(name: str, ws: int, rank: int, coeffs=None, device="cuda"):
+    """This rank's subdomain and inputs.  Boundary-layer workloads (C3/C4/C5):
+    the rank generates only its own cells (dmesh.local_mesh); C2: the global
+    jittered box, decomposed by decompose.py (weak scaling, round-1 path)."""
+    from paper_2005_05899_b200 import dmesh, meshgen
     if name == "c2":
         n = 88
-        mesh = meshgen.box_tets(n * n_ranks, n, n, lengths=(float(n_ranks), 1.0, 1.0), jitter=0.2, seed=20200131)
+        mesh = meshgen.box_tets(n * ws, n, n, lengths=(float(ws), 1.0, 1.0), jitter=0.2, seed=20200131)
         u, p = meshgen.c2_initial(mesh.coords)
         bc = dict(p_fixed=meshgen.boundary_nodes(mesh))
-        wall_nodes = None
-        params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
-        desc = {"workload": "C2: jittered Kuhn TET04 box (BASELINE configs[1])", "cells": [n * n_ranks, n, n],
-                "elements": mesh.n_elements, "nodes": mesh.n_nodes, "kinds": {"tet4": mesh.n_elements}}
-    else:
-        if name == "c4":  # BASELINE configs[3] at N = 1: 300 x 300 x 490 cells, 40 prism layers (~249M elements)
-            mesh = meshgen.c4_mesh()
-        else:
-            mesh = meshgen.c3_mesh(n_ranks ** (1.0 / 3.0))
-        u = np.zeros((mesh.n_nodes, 3))
-        u[:, 0] = 1.0
-        p = np.zeros(mesh.n_nodes)
-        # full Algorithm 1 step: element + boundary assembly (equilibrium wall
-        # model on z = 0, zero normal velocity there)
-        bc, _faces = meshgen.wall_model_bcs(mesh)
-        wall_nodes = np.abs(mesh.coords[:, 2] - mesh.coords[:, 2].min()) < 1e-12
-        params = dict(rho=1.0, mu=1e-3, c_vreman=0.07)
-        desc = {"workload": ("C4: ~250M-element mixed boundary-layer box on one GPU (BASELINE configs[3], N = 1)"
-                             if name == "c4" else
-                             "C3: mixed tet/prism/pyramid/hex boundary-layer box (BASELINE configs[2])"),
-                "elements": mesh.n_elements, "nodes": mesh.n_nodes,
-                "kinds": {r: int(c.shape[0]) for r, c in mesh.conn.items()}}
-    if wall_nodes is not None:
-        desc["wall"] = "equilibrium wall model (Reichardt) on z = 0, K8 per RK stage"
-    return mesh, u, p, bc, params, desc, wall_nodes
+        desc = {"workload": "C2: jittered Kuhn TET04 box (BASELINE configs[1])", "cells": [n * ws, n, n],
+                "nodes": mesh.n_nodes}
+        w = dict(sub=mesh, u=u, p=p, bc=bc, wall=None, desc=desc, plan=None, scaling="weak", weights=None)
+        if ws > 1:
+            from paper_2005_05899_b200.decompose import decompose
+            from paper_2005_05899_b200.partition import sfc_partition
+            parts, _cuts, subw = sfc_partition(mesh, ws, coeffs=coeffs, level=8)
+            sub, plan = decompose(mesh, parts, ws, rank)
+            l2g = plan.l2g
+            w.update(sub=sub, u=u[l2g], p=p[l2g], bc={k: np.asarray(v)[l2g] for k, v in bc.items()}, plan=plan,
+                     weights=subw)
+        return w
+    spec, text, scaling = workload_spec(name, ws)
+    part = dmesh.partition_cells(spec, ws, coeffs=coeffs, device=device)
+    sub, plan = dmesh.local_mesh(spec, part, rank)
+    weights = part.weights
+    del part
+    bc, wall = dmesh.wall_model_bcs_local(sub, spec)
+    u = np.zeros((sub.n_nodes, 3))
+    u[:, 0] = 1.0
+    desc = {"workload": text, "cells": [spec.nx, spec.ny, spec.nz], "prism_layers": spec.layers,
+            "nodes": spec.n_nodes,
+            "wall": "equilibrium wall model (Reichardt) on z = 0, K8 per RK stage",
+            "decomposition": ("per-rank generation of Hilbert-ordered cell ranges (dmesh.py)" if ws > 1 else None)}
+    return dict(sub=sub, u=u, p=np.zeros(sub.n_nodes), bc=bc, wall=wall, desc=desc,
+                plan=plan if ws > 1 else None, scaling=scaling, weights=weights)
 
 
 class ClockSampler:
@@ -233,6 +264,22 @@ def cpu_baseline_sample(steps: int = 2):
                       f"{steps} full steps (CG {CG_ITERS} it), numpy single thread", **host_cpu()}
 
 
+KINDS = ("hex8", "pri6", "pyr5", "tet4")
+
+
+def _kind_counts(solver) -> dict:
+    c = solver.dm.element_counts()
+    return {k: c.get(k, 0) for k in KINDS}
+
+
+def _max_over_ranks(v: float, backend: str) -> float:
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(v)], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_native(args):
     import torch
     import torch.distributed as dist
@@ -253,52 +300,53 @@ def run_native(args):
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group(backend)
-    mesh, u_g, p_g, bc_g, params, desc, wall_g = build_workload(args.workload, ws)
-    n_elem_total = mesh.n_elements
+    name = "c5" if args.weak else args.workload
+    params = PHYS
     rebalance = None
 
-    def make_solver(parts=None):
-        if ws == 1:
-            from paper_2005_05899_b200.wall import wall_faces
-            wall = wall_faces(mesh, wall_g) if wall_g is not None else None
-            s_ = FlowSolver(mesh, FlowParams(**params), **bc_g, windows=not args.no_windows, reorder="sfc",
-                            wall=wall)
-            s_.set_state(u_g, p_g)
-            return s_, mesh.n_elements
-        from paper_2005_05899_b200.decompose import decompose
-        from paper_2005_05899_b200.halo import HaloExchanger
-        sub, plan = decompose(mesh, parts, ws, rank)
-        l2g = plan.l2g
-        halo = HaloExchanger(plan, "cuda")
-        from paper_2005_05899_b200.wall import wall_faces
-        wall = wall_faces(sub, wall_g[l2g]) if wall_g is not None else None
+    def make_solver(coeffs=None):
+        w = build_rank_workload(name, ws, rank, coeffs=coeffs)
+        halo = None
+        if w["plan"] is not None:
+            if os.environ.get("AB_PEER", "1") == "1":
+                # interface sums over peer memory (CUDA IPC over NVLink), graph-capturable
+                from paper_2005_05899_b200.peer import PeerHalo
+                halo = PeerHalo.connect(w["plan"], "cuda")
+            else:  # AB_PEER=0: NCCL grouped send/recv (host-driven)
+                from paper_2005_05899_b200.halo import HaloExchanger
+                halo = HaloExchanger(w["plan"], "cuda")
         # AB_FUSED_CG=1 forces the fused decomposed CG also on gloo (ranks sharing one GPU)
-        fused = True if os.environ.get("AB_FUSED_CG") == "1" else None
-        s_ = FlowSolver(sub, FlowParams(**params), **{k: np.asarray(v)[l2g] for k, v in bc_g.items()},
-                        windows=not args.no_windows, reorder="sfc", halo=halo, own=halo.own, wall=wall,
-                        fused_cg=fused)
-        s_.set_state(u_g[l2g], p_g[l2g])
-        return s_, sub.n_elements
+        fused = True if (halo is not None and os.environ.get("AB_FUSED_CG") == "1") else None
+        s_ = FlowSolver(w["sub"], FlowParams(**params), **w["bc"], windows=not args.no_windows, reorder="sfc",
+                        wall=w["wall"], halo=halo, own=halo.own if halo is not None else None, fused_cg=fused)
+        s_.set_state(w["u"], w["p"])
+        return s_, w
 
-    if ws == 1:
-        solver, n_local = make_solver()
-    else:
+    solver, wl = make_solver()
+    if ws > 1 and not args.no_rebalance:
         from paper_2005_05899_b200.balance import distributed_timer, throughput_coefficients
-        from paper_2005_05899_b200.partition import sfc_partition
-        parts, _cuts, subw = sfc_partition(mesh, ws, level=8)
-        solver, n_local = make_solver(parts)
-        if not args.no_rebalance:
-            # DLB analog: lambda_i = P theta_i / sum(theta) from
-            # each rank's measured K2 throughput, one re-split, rebuild
-            sample = distributed_timer(solver)
-            lam = throughput_coefficients(sample.times, subw)
-            parts, _cuts, subw2 = sfc_partition(mesh, ws, coeffs=lam, level=8)
-            del solver
-            torch.cuda.synchronize()
-            solver, n_local = make_solver(parts)
-            rebalance = {"k2_seconds_before": [float(t) for t in sample.times], "lambda": [float(x) for x in lam],
-                         "weights_before": [float(x) for x in subw], "weights_after": [float(x) for x in subw2]}
-    graph = (not args.no_graph) and ws == 1
+        # DLB analog: lambda_i = P theta_i / sum(theta) from
+        # each rank's measured K2 throughput, one re-split, rebuild
+        sample = distributed_timer(solver)
+        subw = wl["weights"]
+        lam = throughput_coefficients(sample.times, subw)
+        del solver
+        torch.cuda.synchronize()
+        solver, wl = make_solver(coeffs=lam)
+        rebalance = {"k2_seconds_before": [float(t) for t in sample.times], "lambda": [float(x) for x in lam],
+                     "weights_before": [float(x) for x in subw], "weights_after": [float(x) for x in wl["weights"]]}
+    desc = dict(wl["desc"])
+    n_local = solver.dm.n_elements
+    counts_t = torch.tensor([n_local] + [c for c in _kind_counts(solver).values()], dtype=torch.float64,
+                            device="cuda" if backend == "nccl" else "cpu")
+    if ws > 1:
+        dist.all_reduce(counts_t)
+    n_elem_total = int(counts_t[0].item())
+    desc["elements"] = n_elem_total
+    desc["kinds"] = {k: int(v) for k, v in zip(_kind_counts(solver).keys(), counts_t[1:].tolist())}
+    if ws > 1:
+        desc["elements_per_rank_max"] = _max_over_ranks(n_local, backend)
+    graph = (not args.no_graph) and solver.graph_safe
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device="cuda")
 
     for _ in range(args.warmup):
@@ -412,9 +460,9 @@ def run_native(args):
         "metric": "M element-steps/s per time step (assembly + CG)", "value": round(value, 3),
         "unit": "M element-steps/s", "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_per_step, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": wl["scaling"], "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": dict(desc, step=("3x(K2+%sK3) + K4 + PCG(%d it, Jacobi) + K6 + K7"
-                                   % ("K8+" if wall_g is not None else "", args.cg_iters)),
+                                   % ("K8+" if solver.wall is not None else "", args.cg_iters)),
                        cg_iters=args.cg_iters, dt=DT, physics=params, cuda_graph=graph,
                        scatter="windowed" if not args.no_windows else "atomics",
                        l2="flushed (512 MB write) between timed steps", parallelism=f"dd{ws}"),
@@ -430,6 +478,11 @@ def run_native(args):
     }
     if rebalance is not None:
         result["rebalance"] = rebalance
+    if ws == 1 and not args.no_c2 and name != "c2":
+        del solver
+        torch.cuda.synchronize()
+        torch.cuda.empty_cache()
+        result["c2_point"] = c2_point(args, flush)
     if backend != "nccl":
         result["note"] = f"{ws} ranks on one GPU over {backend}: functional check, not a performance number"
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -448,6 +501,32 @@ def run_native(args):
     if ws > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def c2_point(args, flush) -> dict:
+    """Round 1's headline config as an extra key: C2 (4.09M jittered tets,
+    BASELINE configs[1]), same step, graph replay, L2 flushed per step."""
+    import torch
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+    w = build_rank_workload("c2", 1, 0)
+    s_ = FlowSolver(w["sub"], FlowParams(**PHYS), **w["bc"], windows=True, reorder="sfc")
+    s_.set_state(w["u"], w["p"])
+    for _ in range(3):
+        s_.step(DT, args.cg_iters, graph=True)
+    torch.cuda.synchronize()
+    ms = []
+    for _ in range(10):
+        flush.fill_(1.0)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        s_.step(DT, args.cg_iters, graph=True)
+        b.record()
+        b.synchronize()
+        ms.append(a.elapsed_time(b))
+    e = s_.dm.n_elements
+    return {"workload": "C2: jittered Kuhn TET04 88^3 (BASELINE configs[1])", "elements": e,
+            "value": round(e * len(ms) / (sum(ms) / 1e3) / 1e6, 3), "ms_per_step": round(float(np.mean(ms)), 4),
+            "steps": len(ms), "warmup": 3}
 
 
 def _ref_worker(args):

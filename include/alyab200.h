@@ -367,6 +367,131 @@ int ab_ipc_get_handle(const void* dev_ptr, unsigned char* handle64, int64_t* off
 int ab_ipc_open_handle(const unsigned char* handle64, void** dev_ptr);
 int ab_ipc_close(void* dev_ptr);
 
+/* ---- Peer-memory interface exchange and decomposed CG for large subdomains
+ * (DESIGN.md §5).  One process (rank) per GPU; the buffers a rank's peers
+ * write into (recv, cnt_in, rec) are mapped into every peer with CUDA IPC
+ * (ab_ipc_*), or are plain device pointers when several ranks share one GPU
+ * in one process ("virtual ranks", tests).  All progress state (exchange
+ * counts, record epochs, iteration counter, scalars) lives in device memory,
+ * so every entry point below is asynchronous on the caller's stream and a
+ * whole multi-rank time step can be captured in one CUDA graph.  Waits
+ * poll with acquire loads and never time out silently: after 10 s they set
+ * the sticky failure word (state[AB_PS_FAIL] / scal[AB_D2_FAIL]) and return.
+ *
+ * Interface sum (element operators): node i of
+ * this rank shared with ranks S_i gets  sum_{q in S_i + {rank}} f_q(i)  added
+ * in ascending global rank order, so every copy of the node holds the same
+ * bits on every rank.  Two launches: put (this rank's partials into the
+ * sharers' receive slots + one release-add per CTA on their arrival
+ * counters) and add (acquire-wait for the neighbours, rank-ordered sum).
+ * The receive area is double-buffered by exchange parity, which is all a
+ * neighbour can run ahead (its next put needs this rank's next put). */
+#define AB_PEER_MAX 8
+#define AB_PS_EV 0      /* exchanges completed (u64 words of `state`) */
+#define AB_PS_TICK 1    /* arrival ticket of the add kernel */
+#define AB_PS_FAIL 2    /* sticky failure flag */
+typedef struct ab_peer_halo {
+  int32_t rank, n_ranks;
+  int32_t n_if;                       /* interface nodes of this rank */
+  int32_t n_cta;                      /* CTAs of this rank's put kernel (a neighbour waits for that many) */
+  int32_t max_shared;                 /* M: longest shared-node list of any rank pair (all ranks agree) */
+  int32_t n_nbr;
+  const int32_t* if_node;             /* [n_if] local node ids, ascending */
+  const int32_t* if_ptr;              /* [n_if + 1] into if_rank / if_slot */
+  const int32_t* if_rank;             /* sharing rank of each copy (ascending per node, this rank excluded) */
+  const int32_t* if_slot;             /* index k of the node in the (this rank, that rank) shared list */
+  double* recv;                       /* [2][n_ranks][M][3] written by the neighbours */
+  unsigned long long* cnt_in;         /* [n_ranks] put-CTA arrivals from rank q (monotone) */
+  unsigned long long* state;          /* [4] AB_PS_* */
+  int32_t nbr_rank[AB_PEER_MAX];
+  int32_t nbr_ncta[AB_PEER_MAX];      /* put CTAs of that neighbour */
+  double* nbr_recv[AB_PEER_MAX];      /* the neighbour's recv (mapped) */
+  unsigned long long* nbr_cnt[AB_PEER_MAX];  /* &neighbour.cnt_in[rank] (mapped) */
+} ab_peer_halo;
+/* field[node * stride + c], c < ncomp <= 3 */
+int ab_peer_halo_put(const ab_peer_halo* h, const double* field, int32_t ncomp, int32_t stride, void* stream);
+int ab_peer_halo_add(const ab_peer_halo* h, double* field, int32_t ncomp, int32_t stride, void* stream);
+int ab_peer_halo_grid(int32_t n_if);  /* the put kernel's CTA count for n_if interface nodes */
+
+/* Decomposed Jacobi-PCG for subdomains too large to stay on chip (two
+ * kernels + one small interface kernel per iteration, PAPER.md:327-330,
+ * :449-454).  The rank's P L P^T is numbered with its interface rows FIRST
+ * ([0, n_if), SFC order) and the interior rows after (SFC order), so the
+ * blocks holding interface rows run first in the SpMV and their partial
+ * products travel to the sharers while the interior rows stream:
+ *   spmv    beta from the ranks' {r.z, r.r} records; t = (A z) per row;
+ *           interface rows: t -> tif and into every sharer's receive slot,
+ *           one release-add per signalling block; interior rows: p = z +
+ *           beta p, q = t + beta q, p.q partials (grid sum -> scal)
+ *   iface   wait for the neighbours' blocks; interface rows: (A z)_i = the
+ *           sharers' partials summed in global rank order; p, q, p.q; the
+ *           rank's p.q total -> {value, epoch} record into every rank
+ *   update  alpha from the ranks' p.q records; x += alpha p, r -= alpha q,
+ *           z = D^-1 r; {r.z, r.r} record into every rank
+ * Records: the value is stored first, then the epoch with release
+ * semantics; a reader acquires the epoch, then loads the value.  Every rank
+ * sums the P records in rank order, so alpha, beta and the stopping
+ * decision are identical everywhere.  Convergence (tol > 0) is decided on
+ * the device; once done, later launches of the solve return immediately. */
+#define AB_D2_IT 0        /* iterations completed (doubles of `scal`) */
+#define AB_D2_DONE 1
+#define AB_D2_BB 2
+#define AB_D2_RZ0 3       /* rz of even / odd iterations: 3, 4 */
+#define AB_D2_BETA 5
+#define AB_D2_PQI 6       /* interior p.q of this rank */
+#define AB_D2_EPOCH 7     /* publishes so far (monotone over the run, equal on all ranks) */
+#define AB_D2_EPA 8       /* epoch of the last p.q record */
+#define AB_D2_EPB 9       /* epoch of the last {r.z, r.r} record */
+#define AB_D2_HEV 10      /* SpMV exchanges completed */
+#define AB_D2_RR 11
+#define AB_D2_FAIL 12     /* sticky failure flag (1.0 = a peer wait timed out) */
+#define AB_D2_TOL 13
+#define AB_D2_NSCAL 16
+typedef struct ab_ddcg2_rank {
+  int64_t n_rows, n_if;
+  int32_t rank, n_ranks;
+  int32_t n_peers;                    /* every other rank (the reductions) */
+  int32_t recv_stride;                /* M: recv slot q * M + k holds rank q's k-th shared row */
+  const int64_t* slice_ptr;           /* SELL-32 of P L P^T (interface rows first) */
+  const int32_t* cols;
+  const double* vals;
+  const double* dinv;                 /* row order, D of the assembled global operator */
+  const uint8_t* fixed;               /* row order, nullable */
+  const double* own;                  /* row order: 1 on the lowest sharing rank, else 0 */
+  const int32_t* perm;                /* row -> local node */
+  double *x, *r, *z, *p, *q;          /* row order */
+  double* tif;                        /* [n_if] this rank's (A z) at the interface rows */
+  const int32_t* send_ptr;            /* [n_if + 1] into send_peer / send_off */
+  const int32_t* send_peer;           /* index into peer_* */
+  const int32_t* send_off;            /* slot in that peer's recv */
+  const int32_t* recv_ptr;            /* [n_if + 1] into recv_rank / recv_off */
+  const int32_t* recv_rank;           /* sharing rank (ascending; this rank excluded) */
+  const int32_t* recv_off;            /* slot in this rank's recv */
+  double* recv;                       /* written by the neighbours */
+  unsigned long long* cnt_in;         /* [n_ranks] signalling-block arrivals from rank q (monotone) */
+  double* rec;                        /* [2 sets][n_ranks][2 values][value, epoch] written by every rank */
+  double* part;                       /* grid partials */
+  uint32_t* cnt;                      /* grid-sum counters (zeroed once) */
+  double* scal;                       /* [AB_D2_NSCAL] */
+  int32_t nsig;                       /* blocks of this rank's SpMV holding interface rows */
+  int32_t pad_;
+  int32_t peer_rank[AB_PEER_MAX];
+  int32_t peer_nsig[AB_PEER_MAX];     /* that peer's signalling blocks (0: not a neighbour) */
+  double* peer_recv[AB_PEER_MAX];     /* mapped */
+  unsigned long long* peer_cnt[AB_PEER_MAX];  /* &peer.cnt_in[rank] (mapped) */
+  double* peer_rec[AB_PEER_MAX];      /* &peer.rec[0] (mapped) */
+} ab_ddcg2_rank;
+/* b (node order) -> r = b (fixed rows 0), z = D^-1 r, x = p = q = 0, and the
+ * {r.z, r.r} record; b_zero (nullable) is zeroed.  tol is kept for the solve. */
+int ab_ddcg2_init(const ab_ddcg2_rank* d, const double* b, double* b_zero, double tol, void* stream);
+int ab_ddcg2_spmv(const ab_ddcg2_rank* d, void* stream);
+int ab_ddcg2_iface(const ab_ddcg2_rank* d, void* stream);
+int ab_ddcg2_update(const ab_ddcg2_rank* d, void* stream);
+/* x (row order) -> x_node[perm[i]] */
+int ab_ddcg2_finish(const ab_ddcg2_rank* d, double* x_node, void* stream);
+/* doubles of `part` / uint32 of `cnt` the kernels need for n_rows */
+int64_t ab_ddcg2_part_size(int64_t n_rows);
+
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */
 int ab_rk_stage(int64_t n, double a, double b, double k, const double* u0, const double* uprev,

@@ -54,8 +54,38 @@ class AbCgLocal(C.Structure):
                 ("nbr_ptr", vp), ("nbr", vp)]
 
 
+PEER_MAX = 8
+u64p = C.c_void_p
+
+
+class AbPeerHalo(C.Structure):
+    _fields_ = ([("rank", i32), ("n_ranks", i32), ("n_if", i32), ("n_cta", i32), ("max_shared", i32), ("n_nbr", i32)]
+                + [(n, vp) for n in ("if_node", "if_ptr", "if_rank", "if_slot", "recv", "cnt_in", "state")]
+                + [("nbr_rank", i32 * PEER_MAX), ("nbr_ncta", i32 * PEER_MAX), ("nbr_recv", vp * PEER_MAX),
+                   ("nbr_cnt", vp * PEER_MAX)])
+
+
+class AbDdcg2Rank(C.Structure):
+    _fields_ = ([("n_rows", i64), ("n_if", i64), ("rank", i32), ("n_ranks", i32), ("n_peers", i32),
+                 ("recv_stride", i32)]
+                + [(n, vp) for n in ("slice_ptr", "cols", "vals", "dinv", "fixed", "own", "perm", "x", "r", "z",
+                                     "p", "q", "tif", "send_ptr", "send_peer", "send_off", "recv_ptr", "recv_rank",
+                                     "recv_off", "recv", "cnt_in", "rec", "part", "cnt", "scal")]
+                + [("nsig", i32), ("pad_", i32), ("peer_rank", i32 * PEER_MAX), ("peer_nsig", i32 * PEER_MAX),
+                   ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX)])
+
+
 P = C.POINTER
 _SIGS = {
+    "ab_peer_halo_put": ([P(AbPeerHalo), vp, i32, i32, vp], C.c_int),
+    "ab_peer_halo_add": ([P(AbPeerHalo), vp, i32, i32, vp], C.c_int),
+    "ab_peer_halo_grid": ([i32], C.c_int),
+    "ab_ddcg2_init": ([P(AbDdcg2Rank), vp, vp, f64, vp], C.c_int),
+    "ab_ddcg2_spmv": ([P(AbDdcg2Rank), vp], C.c_int),
+    "ab_ddcg2_iface": ([P(AbDdcg2Rank), vp], C.c_int),
+    "ab_ddcg2_update": ([P(AbDdcg2Rank), vp], C.c_int),
+    "ab_ddcg2_finish": ([P(AbDdcg2Rank), vp, vp], C.c_int),
+    "ab_ddcg2_part_size": ([i64], i64),
     "ab_version": ([], C.c_int),
     "ab_last_error": ([], C.c_char_p),
     "ab_launch_count": ([], i64),

@@ -64,6 +64,37 @@ __device__ __forceinline__ double sell_row_dot_smem(const int64_t* tsp, const ui
   return acc;
 }
 
+constexpr int kChunk = 16;
+
+// (A z)_i for one SELL row: all column/value loads of a 16-wide chunk first,
+// then the gathers, then the FMAs.  CG = true gathers through L2 only (z is
+// rewritten inside the resident kernel).
+template <bool CG = false>
+__device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
+                                               const double* __restrict__ sval, const double* zv, int64_t i) {
+  const int64_t s = i >> 5;
+  const int lane = (int)(i & 31);
+  const int64_t base = sp[s] + lane;
+  const int width = (int)((sp[s + 1] - sp[s]) >> 5);
+  double acc = 0.0;
+  for (int j0 = 0; j0 < width; j0 += kChunk) {
+    int c[kChunk];
+    double a[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) {
+      const bool ok = j0 + u < width;
+      c[u] = ok ? __ldcs(scol + base + (int64_t)(j0 + u) * 32) : 0;
+      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
+    }
+    double g[kChunk];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) g[u] = CG ? __ldcg(zv + c[u]) : zv[c[u]];
+#pragma unroll
+    for (int u = 0; u < kChunk; ++u) acc = fma(a[u], g[u], acc);
+  }
+  return acc;
+}
+
 // Replicated per-CTA partials (resident solvers): the NV values of CTA b are
 // written to kRep copies of a [NV][nbp] table (nbp = nb rounded up to 4),
 // and CTA b reads copy b % kRep with 16-byte loads, so each 32-byte sector is

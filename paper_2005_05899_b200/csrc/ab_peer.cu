@@ -1,0 +1,465 @@
+// Peer-memory interface exchange and the decomposed CG for subdomains too
+// large to stay on chip (include/alyab200.h).
+//
+// Every rank owns the buffers its neighbours write into (receive slots,
+// arrival counters, reduction records); the neighbours reach them through
+// CUDA IPC mappings (NVLink / NVSwitch peer stores) or, for ranks sharing one
+// GPU in one process, as plain device pointers.  Progress state lives in
+// device memory, so no launch argument changes between steps and the whole
+// multi-rank step is graph-capturable.  The interface sums add the sharers'
+// partials in ascending global rank order (this rank's own partial at its
+// position), so duplicated interface values stay bitwise identical across
+// ranks.
+#include "ab_cg_common.cuh"
+
+namespace ab {
+
+static_assert(sizeof(ab_peer_halo) == 272, "ab_peer_halo layout (mirrored by _lib.AbPeerHalo)");
+static_assert(sizeof(ab_ddcg2_rank) == 496, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
+
+constexpr int kPeerBlock = 256;
+constexpr long long kPeerTimeoutNs = 10000000000ll;
+
+__device__ __forceinline__ long long peer_time() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ unsigned long long ld_acq_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void red_rel_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.sys.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ void st_rel_f64(double* p, double v) {
+  asm volatile("st.release.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ void st_rlx_f64(double* p, double v) {
+  asm volatile("st.relaxed.sys.global.f64 [%0], %1;" ::"l"(p), "d"(v) : "memory");
+}
+__device__ __forceinline__ double ld_acq_f64(const double* p) {
+  double v;
+  asm volatile("ld.acquire.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ double ld_rlx_f64(const double* p) {
+  double v;
+  asm volatile("ld.relaxed.sys.global.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// Interface sum of an element-assembled nodal field
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kPeerBlock) k_halo_put(ab_peer_halo h, const double* __restrict__ f, int ncomp,
+                                                         int stride) {
+  const unsigned long long ev = h.state[AB_PS_EV];
+  const size_t par = (size_t)(ev & 1ull);
+  const size_t M = (size_t)h.max_shared;
+  for (int i = blockIdx.x * kPeerBlock + threadIdx.x; i < h.n_if; i += gridDim.x * kPeerBlock) {
+    const int64_t node = h.if_node[i];
+    double v[3];
+    for (int c = 0; c < ncomp; ++c) v[c] = f[node * stride + c];
+    for (int e = h.if_ptr[i]; e < h.if_ptr[i + 1]; ++e) {
+      const int q = h.if_rank[e];
+      int k = 0;
+      while (h.nbr_rank[k] != q) ++k;
+      double* dst = h.nbr_recv[k] + ((par * h.n_ranks + h.rank) * M + (size_t)h.if_slot[e]) * 3;
+      for (int c = 0; c < ncomp; ++c) dst[c] = v[c];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence_system();
+    for (int k = 0; k < h.n_nbr; ++k) red_rel_u64(h.nbr_cnt[k], 1ull);
+  }
+}
+
+__global__ void __launch_bounds__(kPeerBlock) k_halo_add(ab_peer_halo h, double* __restrict__ f, int ncomp,
+                                                         int stride) {
+  __shared__ int s_fail;
+  const unsigned long long ev = h.state[AB_PS_EV];
+  const size_t par = (size_t)(ev & 1ull);
+  const size_t M = (size_t)h.max_shared;
+  if (threadIdx.x == 0) s_fail = 0;
+  __syncthreads();
+  if ((int)threadIdx.x < h.n_nbr) {
+    const int q = h.nbr_rank[threadIdx.x];
+    const unsigned long long want = (ev + 1ull) * (unsigned long long)h.nbr_ncta[threadIdx.x];
+    const long long t0 = peer_time();
+    while (ld_acq_u64(h.cnt_in + q) < want) {
+      if (peer_time() - t0 > kPeerTimeoutNs) { s_fail = 1; break; }
+    }
+  }
+  __syncthreads();
+  if (s_fail) {
+    if (threadIdx.x == 0) h.state[AB_PS_FAIL] = 1ull;
+  } else {
+    for (int i = blockIdx.x * kPeerBlock + threadIdx.x; i < h.n_if; i += gridDim.x * kPeerBlock) {
+      const int64_t node = h.if_node[i];
+      double own[3], acc[3] = {0.0, 0.0, 0.0};
+      for (int c = 0; c < ncomp; ++c) own[c] = f[node * stride + c];
+      bool mine = false;
+      for (int e = h.if_ptr[i]; e < h.if_ptr[i + 1]; ++e) {
+        const int q = h.if_rank[e];
+        if (!mine && q > h.rank) {
+          for (int c = 0; c < ncomp; ++c) acc[c] += own[c];
+          mine = true;
+        }
+        const double* src = h.recv + ((par * h.n_ranks + q) * M + (size_t)h.if_slot[e]) * 3;
+        for (int c = 0; c < ncomp; ++c) acc[c] += __ldcg(src + c);
+      }
+      if (!mine)
+        for (int c = 0; c < ncomp; ++c) acc[c] += own[c];
+      for (int c = 0; c < ncomp; ++c) f[node * stride + c] = acc[c];
+    }
+  }
+  // the last CTA to finish advances the exchange count (next parity)
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned long long t = atomicAdd(h.state + AB_PS_TICK, 1ull);
+    if (t + 1 == (ev + 1) * (unsigned long long)gridDim.x) {
+      __threadfence();
+      h.state[AB_PS_EV] = ev + 1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decomposed CG, large subdomains
+// ---------------------------------------------------------------------------
+constexpr int kD2Block = 256;
+constexpr int kD2IfGrid = 148;
+
+// Record of `set` published by rank `src`: NV values into every rank's
+// record array (this rank's own included).
+template <int NV>
+__device__ __forceinline__ void d2_publish(const ab_ddcg2_rank& d, int set, const double (&v)[NV], double ep) {
+  const int P = d.n_ranks;
+  double* dst0 = d.rec + ((size_t)set * P + d.rank) * 4;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) st_rlx_f64(dst0 + 2 * k, v[k]);
+  for (int q = 0; q < d.n_peers; ++q) {
+    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) st_rlx_f64(dst + 2 * k, v[k]);
+  }
+  // epochs after all values (release orders the value stores before them)
+#pragma unroll
+  for (int k = 0; k < NV; ++k) st_rel_f64(dst0 + 2 * k + 1, ep);
+  for (int q = 0; q < d.n_peers; ++q) {
+    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) st_rel_f64(dst + 2 * k + 1, ep);
+  }
+}
+
+// Every rank's record of `set` at epoch `ep`, summed in rank order; the same
+// in every thread of the block.  Returns false on a timeout.
+template <int NV>
+__device__ __forceinline__ bool d2_collect(const ab_ddcg2_rank& d, int set, double ep, double (&out)[NV],
+                                           double* sbuf /* [NV * P] shared */, int* sflag) {
+  const int P = d.n_ranks;
+  if ((int)threadIdx.x < P) {
+    const double* rec = d.rec + ((size_t)set * P + threadIdx.x) * 4;
+    const long long t0 = peer_time();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double v = 0.0;
+      for (;;) {
+        if (ld_acq_f64(rec + 2 * k + 1) == ep) { v = ld_rlx_f64(rec + 2 * k); break; }
+        if (peer_time() - t0 > kPeerTimeoutNs) { *sflag = 1; break; }
+      }
+      sbuf[k * P + threadIdx.x] = v;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double acc = 0.0;
+    for (int q = 0; q < P; ++q) acc += sbuf[k * P + q];
+    out[k] = acc;
+  }
+  const bool ok = *sflag == 0;
+  __syncthreads();
+  return ok;
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_init(ab_ddcg2_rank d, const double* __restrict__ b, double* b_zero,
+                                                      double tol) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x; i < d.n_rows;
+       i += (int64_t)gridDim.x * kD2Block) {
+    const int64_t ni = d.perm[i];
+    double ri = b[ni];
+    if (d.fixed && d.fixed[i]) ri = 0.0;
+    const double zi = d.dinv[i] * ri;
+    d.r[i] = ri;
+    d.z[i] = zi;
+    d.x[i] = 0.0;
+    d.p[i] = 0.0;
+    d.q[i] = 0.0;
+    const double w = d.own[i];
+    v[0] += w * ri * zi;
+    v[1] += w * ri * ri;
+  }
+  double tot[2];
+  if (grid_sum<2, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+    const double ep = d.scal[AB_D2_EPOCH] + 1.0;
+    d.scal[AB_D2_EPOCH] = ep;
+    d.scal[AB_D2_EPB] = ep;
+    d.scal[AB_D2_IT] = 0.0;
+    d.scal[AB_D2_DONE] = 0.0;
+    d.scal[AB_D2_RZ0] = 0.0;
+    d.scal[AB_D2_RZ0 + 1] = 0.0;
+    d.scal[AB_D2_TOL] = tol;
+    d2_publish<2>(d, 1, tot, ep);
+  }
+}
+
+__global__ void k_d2_zero(int64_t n, double* b) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = 0.0;
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_spmv(ab_ddcg2_rank d) {
+  __shared__ double sbuf[2 * 32];
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  const int it = (int)d.scal[AB_D2_IT];
+  double t2[2];
+  if (!d2_collect<2>(d, 1, d.scal[AB_D2_EPB], t2, sbuf, &sflag)) {
+    if (threadIdx.x == 0) { d.scal[AB_D2_FAIL] = 1.0; d.scal[AB_D2_DONE] = 1.0; }
+    return;
+  }
+  const double rz_new = t2[0], rr = t2[1];
+  const double bb = it == 0 ? rr : d.scal[AB_D2_BB];
+  const double tol = d.scal[AB_D2_TOL];
+  if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) {  // identical decision in every block and rank
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      d.scal[AB_D2_DONE] = 1.0;
+      d.scal[AB_D2_RR] = rr;
+      if (it == 0) d.scal[AB_D2_BB] = bb;
+    }
+    return;
+  }
+  const double rz_old = d.scal[AB_D2_RZ0 + ((it + 1) & 1)];
+  const double beta = it > 0 && rz_old != 0.0 ? rz_new / rz_old : 0.0;
+  const int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x;
+  double v[1] = {0.0};
+  if (i < d.n_rows) {
+    const double az = sell_row_dot(d.slice_ptr, d.cols, d.vals, d.z, i);
+    if (i < d.n_if) {
+      d.tif[i] = az;
+      for (int e = d.send_ptr[i]; e < d.send_ptr[i + 1]; ++e) d.peer_recv[d.send_peer[e]][d.send_off[e]] = az;
+    } else {
+      const double pi = fma(beta, d.p[i], d.z[i]);
+      const double qi = fma(beta, d.q[i], az);
+      d.p[i] = pi;
+      d.q[i] = qi;
+      v[0] = d.own[i] * pi * qi;
+    }
+  }
+  if ((int64_t)blockIdx.x * kD2Block < d.n_if) {  // a signalling block: its puts are complete
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < d.n_peers; ++q)
+        if (d.peer_nsig[q] > 0) red_rel_u64(d.peer_cnt[q], 1ull);
+    }
+  }
+  double tot[1];
+  if (grid_sum<1, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+    d.scal[AB_D2_PQI] = tot[0];
+    d.scal[AB_D2_BETA] = beta;
+    d.scal[AB_D2_RZ0 + (it & 1)] = rz_new;
+    d.scal[AB_D2_RR] = rr;
+    if (it == 0) d.scal[AB_D2_BB] = bb;
+  }
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_iface(ab_ddcg2_rank d) {
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  const double hev = d.scal[AB_D2_HEV];
+  if ((int)threadIdx.x < d.n_peers && d.peer_nsig[threadIdx.x] > 0) {
+    const int q = d.peer_rank[threadIdx.x];
+    const unsigned long long want = (unsigned long long)(hev + 1.0) * (unsigned long long)d.peer_nsig[threadIdx.x];
+    const long long t0 = peer_time();
+    while (ld_acq_u64(d.cnt_in + q) < want) {
+      if (peer_time() - t0 > kPeerTimeoutNs) { sflag = 1; break; }
+    }
+  }
+  __syncthreads();
+  const bool failed = sflag != 0;
+  const double beta = d.scal[AB_D2_BETA];
+  double v[1] = {0.0};
+  if (!failed) {
+    for (int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x; i < d.n_if; i += (int64_t)gridDim.x * kD2Block) {
+      const double own_t = d.tif[i];
+      double t = 0.0;
+      bool mine = false;
+      for (int e = d.recv_ptr[i]; e < d.recv_ptr[i + 1]; ++e) {
+        if (!mine && d.recv_rank[e] > d.rank) { t += own_t; mine = true; }
+        t += __ldcg(d.recv + d.recv_off[e]);
+      }
+      if (!mine) t += own_t;
+      const double pi = fma(beta, d.p[i], d.z[i]);
+      const double qi = fma(beta, d.q[i], t);
+      d.p[i] = pi;
+      d.q[i] = qi;
+      v[0] += d.own[i] * pi * qi;
+    }
+  }
+  double tot[1];
+  // (part/cnt behind the SpMV's: ab_ddcg2_part_size)
+  const int64_t nb_spmv = (d.n_rows + kD2Block - 1) / kD2Block;
+  double* part = d.part + 2 * (nb_spmv + (nb_spmv + kGroup - 1) / kGroup) + 8;
+  uint32_t* cnt = d.cnt + 2 + (nb_spmv + kGroup - 1) / kGroup;
+  if (grid_sum<1, kD2Block>(v, part, cnt, tot) && threadIdx.x == 0) {
+    d.scal[AB_D2_HEV] = hev + 1.0;
+    if (failed) {
+      d.scal[AB_D2_FAIL] = 1.0;
+      d.scal[AB_D2_DONE] = 1.0;
+      return;
+    }
+    const double ep = d.scal[AB_D2_EPOCH] + 1.0;
+    d.scal[AB_D2_EPOCH] = ep;
+    d.scal[AB_D2_EPA] = ep;
+    const double pq[1] = {d.scal[AB_D2_PQI] + tot[0]};
+    d2_publish<1>(d, 0, pq, ep);
+  }
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_update(ab_ddcg2_rank d) {
+  __shared__ double sbuf[32];
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  double t1[1];
+  if (!d2_collect<1>(d, 0, d.scal[AB_D2_EPA], t1, sbuf, &sflag)) {
+    if (threadIdx.x == 0) { d.scal[AB_D2_FAIL] = 1.0; d.scal[AB_D2_DONE] = 1.0; }
+    return;
+  }
+  const int it = (int)d.scal[AB_D2_IT];
+  const double rz = d.scal[AB_D2_RZ0 + (it & 1)];
+  const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
+  double v[2] = {0.0, 0.0};
+  const int64_t i = 2 * ((int64_t)blockIdx.x * kD2Block + threadIdx.x);
+  for (int64_t k = i; k < i + 2 && k < d.n_rows; ++k) {
+    d.x[k] = fma(alpha, d.p[k], d.x[k]);
+    const double rk = fma(-alpha, d.q[k], d.r[k]);
+    const double zk = d.dinv[k] * rk;
+    d.r[k] = rk;
+    d.z[k] = zk;
+    const double w = d.own[k];
+    v[0] += w * rk * zk;
+    v[1] += w * rk * rk;
+  }
+  double tot[2];
+  if (grid_sum<2, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+    const double ep = d.scal[AB_D2_EPOCH] + 1.0;
+    d.scal[AB_D2_EPOCH] = ep;
+    d.scal[AB_D2_EPB] = ep;
+    d.scal[AB_D2_IT] = (double)(it + 1);
+    d2_publish<2>(d, 1, tot, ep);
+  }
+}
+
+__global__ void k_d2_finish(ab_ddcg2_rank d, double* __restrict__ x_node) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d.n_rows) x_node[d.perm[i]] = d.x[i];
+}
+
+}  // namespace ab
+
+using namespace ab;
+
+extern "C" {
+
+int ab_peer_halo_grid(int32_t n_if) {
+  const int g = (n_if + kPeerBlock - 1) / kPeerBlock;
+  return g < 1 ? 1 : (g > 64 ? 64 : g);
+}
+
+static int check_halo(const ab_peer_halo* h, int ncomp, int stride, const char* what) {
+  if (!h || !h->state || !h->recv || !h->cnt_in) return fail(what);
+  if (ncomp < 1 || ncomp > 3 || stride < ncomp) return fail("peer halo: ncomp must be 1..3 and <= stride");
+  if (h->n_nbr < 0 || h->n_nbr > AB_PEER_MAX) return fail("peer halo: too many neighbours");
+  if (h->n_cta != ab_peer_halo_grid(h->n_if)) return fail("peer halo: n_cta != ab_peer_halo_grid(n_if)");
+  return AB_OK;
+}
+
+int ab_peer_halo_put(const ab_peer_halo* h, const double* field, int32_t ncomp, int32_t stride, void* stream) {
+  if (int rc = check_halo(h, ncomp, stride, "ab_peer_halo_put: incomplete descriptor")) return rc;
+  k_halo_put<<<h->n_cta, kPeerBlock, 0, S(stream)>>>(*h, field, ncomp, stride);
+  return check_launch("ab_peer_halo_put");
+}
+
+int ab_peer_halo_add(const ab_peer_halo* h, double* field, int32_t ncomp, int32_t stride, void* stream) {
+  if (int rc = check_halo(h, ncomp, stride, "ab_peer_halo_add: incomplete descriptor")) return rc;
+  k_halo_add<<<h->n_cta, kPeerBlock, 0, S(stream)>>>(*h, field, ncomp, stride);
+  return check_launch("ab_peer_halo_add");
+}
+
+int64_t ab_ddcg2_part_size(int64_t n_rows) {
+  const int64_t nb = (n_rows + kD2Block - 1) / kD2Block + 1;
+  const int64_t ng = (nb + kGroup - 1) / kGroup + 1;
+  // SpMV/update/init grid sums (<= 2 values over <= nb blocks) + the
+  // interface kernel's (1 value over kD2IfGrid blocks) behind them
+  return 2 * (nb + ng) + 8 + 2 * (kD2IfGrid + 4) + 8;
+}
+
+static int check_d2(const ab_ddcg2_rank* d, const char* what) {
+  if (!d || !d->slice_ptr || !d->scal || !d->part || !d->cnt || !d->rec) return fail(what);
+  if (d->n_peers < 0 || d->n_peers > AB_PEER_MAX || d->n_ranks > 32) return fail("ddcg2: at most 8 peers / 32 ranks");
+  return AB_OK;
+}
+
+int ab_ddcg2_init(const ab_ddcg2_rank* d, const double* b, double* b_zero, double tol, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_init: incomplete descriptor")) return rc;
+  const unsigned g = grid_for(d->n_rows, kD2Block);
+  k_d2_init<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d, b, b_zero, tol);
+  if (int rc = check_launch("ab_ddcg2_init")) return rc;
+  if (b_zero && d->n_rows > 0) k_d2_zero<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(d->n_rows, b_zero);
+  return check_launch("ab_ddcg2_init");
+}
+
+int ab_ddcg2_spmv(const ab_ddcg2_rank* d, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_spmv: incomplete descriptor")) return rc;
+  const unsigned g = grid_for(d->n_rows, kD2Block);
+  k_d2_spmv<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d);
+  return check_launch("ab_ddcg2_spmv");
+}
+
+int ab_ddcg2_iface(const ab_ddcg2_rank* d, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_iface: incomplete descriptor")) return rc;
+  int g = (int)((d->n_if + kD2Block - 1) / kD2Block);
+  if (g < 1) g = 1;
+  if (g > kD2IfGrid) g = kD2IfGrid;
+  k_d2_iface<<<g, kD2Block, 0, S(stream)>>>(*d);
+  return check_launch("ab_ddcg2_iface");
+}
+
+int ab_ddcg2_update(const ab_ddcg2_rank* d, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_update: incomplete descriptor")) return rc;
+  const unsigned g = grid_for((d->n_rows + 1) / 2, kD2Block);
+  k_d2_update<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d);
+  return check_launch("ab_ddcg2_update");
+}
+
+int ab_ddcg2_finish(const ab_ddcg2_rank* d, double* x_node, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_finish: incomplete descriptor")) return rc;
+  if (d->n_rows > 0) k_d2_finish<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(*d, x_node);
+  return check_launch("ab_ddcg2_finish");
+}
+
+}  // extern "C"

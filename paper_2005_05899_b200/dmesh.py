@@ -128,6 +128,10 @@ def partition_cells(spec: BoxSpec, n_parts: int, coeffs=None, device="cuda", key
     if n_parts > 127:
         raise ValueError("at most 127 parts")
     dev = torch.device(device)
+    if n_parts == 1:  # one subdomain: no curve needed
+        w_all = meshgen.CELL_GAUSS[np.asarray(spec.codes(np.arange(spec.n_cells, dtype=np.int64)))]
+        return CellPartition(n_parts=1, owner=torch.zeros(spec.n_cells, dtype=torch.int8, device=dev),
+                             cuts=np.zeros(0, np.int64), weights=np.array([float(w_all.sum())]))
     keys_fn = keys_fn or cuda_cell_keys
     L = _level(spec)
     nc = spec.n_cells
@@ -198,8 +202,15 @@ def local_mesh(spec: BoxSpec, part: CellPartition, rank: int):
                 parts_.append(start["tet"] + n_trans_tets + (b[:, None] * 6 + np.arange(6)[None, :]).reshape(-1))
             ids["tet"] = np.concatenate(parts_)
         del code_all
-    used = [b.reshape(-1) for b in blocks.values()]
-    l2g = np.unique(np.concatenate(used)) if used else np.zeros(0, np.int64)
+    # local nodes = grid nodes touched by my elements, ascending global id
+    # (a mark-and-compact over the grid instead of sorting E * n_k ids)
+    used = np.zeros(spec.n_nodes, dtype=bool)
+    for b in blocks.values():
+        used[b.reshape(-1)] = True
+    l2g = np.flatnonzero(used).astype(np.int64)
+    del used
+    g2l = np.full(spec.n_nodes, -1, dtype=np.int32)
+    g2l[l2g] = np.arange(l2g.size, dtype=np.int32)
     # coordinates exactly as meshgen._grid_nodes
     nyz = (spec.ny + 1) * (spec.nz + 1)
     gi, gj, gk = l2g // nyz, (l2g // (spec.nz + 1)) % (spec.ny + 1), l2g % (spec.nz + 1)
@@ -210,10 +221,15 @@ def local_mesh(spec: BoxSpec, part: CellPartition, rank: int):
     for tag in meshgen.KIND_TAGS:
         if tag in blocks:
             rule = meshgen.DEFAULT_RULE[tag]
-            sub.conn[rule] = np.searchsorted(l2g, blocks[tag]).astype(np.int32)
+            sub.conn[rule] = np.ascontiguousarray(g2l[blocks[tag]])
             sub.elem_ids[rule] = np.asarray(ids[tag], dtype=np.int64)
+            del blocks[tag]
+    del g2l
     sub.shape = None
-    plan = interface_plan_local(spec, owner, rank, P, l2g)
+    if P == 1:
+        plan = InterfacePlan(rank=0, n_ranks=1, l2g=l2g, own=np.ones(l2g.size))
+    else:
+        plan = interface_plan_local(spec, owner, rank, P, l2g)
     return sub, plan
 
 

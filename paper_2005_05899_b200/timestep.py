@@ -117,8 +117,11 @@ class FlowSolver:
         # memory (ddcg.FusedDDSolver), validated once against the NCCL-driven
         # two-kernel solve; fused_cg=False keeps the latter
         self.ddcg = None
+        self.ddcg_kind = None
+        self._force_dd2 = fused_cg == "two-kernel"  # tests: skip the on-chip form
         # (fused_cg=True also forces it on other backends, e.g. gloo ranks sharing one GPU in tests)
-        if halo is not None and (fused_cg is True or (fused_cg is None and self._nccl(halo))):
+        if halo is not None and (fused_cg in (True, "two-kernel")
+                                 or (fused_cg is None and (self._nccl(halo) or getattr(halo, "graph_safe", False)))):
             self.ddcg = self._fused_solver(dm, pf, fused_cg)
         self.graph = None
         self._side = None  # step_host: G p^n while u uploads
@@ -132,51 +135,63 @@ class FlowSolver:
         return dist.is_initialized() and dist.get_backend(halo.group) == "nccl"
 
     def _fused_solver(self, dm, pf, required):
+        """The pressure solve fused with its interface exchange over peer
+        memory: the on-chip solver (ddcg.FusedDDSolver, one cooperative
+        kernel per solve) when the rank's rows fit on chip, else the
+        two-kernel form (peer.FusedDD2Solver).  Each is validated once
+        against the NCCL-driven solve (8 iterations, max-norm 1e-10).
+        Every branch is collective: all ranks take the same one."""
         import torch.distributed as dist
         from .ddcg import FusedDDSolver
+        from .peer import FusedDD2Solver
         plan = self.halo.plan
         fixed = self.p_fixed if pf.any() else None
+
         def consensus(ok: bool) -> bool:  # every rank takes the same branch
             t = torch.tensor([1 if ok else 0], dtype=torch.int32, device=self.B.device)
             dist.all_reduce(t, op=dist.ReduceOp.MIN, group=self.halo.group)
             return bool(int(t.item()))
 
-        err = None
-        try:
-            dd = FusedDDSolver(dm, self.L, self.dinv, fixed, plan, self.B, group=self.halo.group)
-        except Exception as e:  # FusedDDSolver's own checks are collective
-            dd, err = None, e
-        if dd is not None:
+        errs = []
+        for kind, cls in (("resident", FusedDDSolver), ("two-kernel", FusedDD2Solver)):
+            if kind == "resident" and getattr(self, "_force_dd2", False):
+                continue
+            try:
+                dd = cls(dm, self.L, self.dinv, fixed, plan, self.B, group=self.halo.group)
+            except Exception as e:  # the constructors' own checks are collective
+                errs.append(f"{kind}: {e}")
+                continue
             # validation solve: same iterate as the NCCL-driven kernels
             g = torch.Generator(device="cpu").manual_seed(1234)
             bh = torch.randn(len(plan.l2g), generator=g, dtype=torch.float64).to(self.B.device)
             self.B.copy_(bh)
             self.halo.sum_(self.B, 1, 1)
             b0 = self.B.clone()
+            ok = True
             try:
-                x_dd, _ = dd.solve(self.B, 8)
+                x_dd, it = dd.solve(self.B, 8)
                 x_dd = x_dd.clone()
-                ran = dd.rank.iterations == 8
+                dd.check()
             except Exception as e:
-                ran, err = False, e
-            if consensus(ran):
+                ok = False
+                errs.append(f"{kind}: {e}")
+            if consensus(ok):
                 self.B.copy_(b0)
                 x_ref, _ = self.pcg.solve(self.B, 8)
                 d = torch.tensor([float((x_dd - x_ref).abs().max() / x_ref.abs().max().clamp_min(1e-300))],
                                  dtype=torch.float64, device=self.B.device)
                 dist.all_reduce(d, op=dist.ReduceOp.MAX, group=self.halo.group)
-                if float(d.item()) > 1e-10:
-                    dd, err = None, RuntimeError(f"fused decomposed CG disagrees with the NCCL solve "
-                                                 f"({float(d.item()):.2e})")
-            else:
-                dd = None
+                self.B.zero_()
+                if float(d.item()) <= 1e-10:
+                    self.ddcg_kind = kind
+                    return dd
+                errs.append(f"{kind}: disagrees with the NCCL-driven solve ({float(d.item()):.2e})")
             self.B.zero_()
-        if dd is None:
-            if required:
-                raise RuntimeError(f"fused decomposed CG unavailable: {err}")
-            import warnings
-            warnings.warn(f"fused decomposed CG unavailable, using the NCCL-driven solve: {err}")
-        return dd
+        if required:
+            raise RuntimeError(f"fused decomposed CG unavailable: {'; '.join(errs)}")
+        import warnings
+        warnings.warn(f"fused decomposed CG unavailable, using the NCCL-driven solve: {'; '.join(errs)}")
+        return None
 
     def _grad(self, p, out4, scale: float = 1.0):
         if self.Bop is not None:
@@ -316,10 +331,17 @@ class FlowSolver:
         if self.ddcg is not None:
             self.ddcg.check()
 
+    @property
+    def graph_safe(self) -> bool:
+        """A fixed-iteration step can be captured: single domain, or a
+        decomposed one whose exchanges are peer-memory kernels (no NCCL call,
+        no host sync) and whose pressure solve is fused (no NCCL scalars)."""
+        return self.halo is None or (getattr(self.halo, "graph_safe", False) and self.ddcg is not None)
+
     def step(self, dt: float, cg_iters: int = 50, cg_tol: float = 0.0, graph: bool = False):
-        """Advance one step.  ``graph=True`` (fixed iterations, no halo)
-        captures the step once and replays the CUDA graph afterwards."""
-        if graph and cg_tol == 0.0 and self.halo is None:
+        """Advance one step.  ``graph=True`` (fixed iterations) captures the
+        step once and replays the CUDA graph afterwards when graph_safe."""
+        if graph and cg_tol == 0.0 and self.graph_safe:
             key = (dt, cg_iters)
             if self.graph is None or self.graph_key != key:
                 self.capture(dt, cg_iters)
