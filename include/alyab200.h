@@ -492,6 +492,55 @@ int ab_ddcg2_finish(const ab_ddcg2_rank* d, double* x_node, void* stream);
 /* doubles of `part` / uint32 of `cnt` the kernels need for n_rows */
 int64_t ab_ddcg2_part_size(int64_t n_rows);
 
+/* ---- Session: the whole time step behind four calls ---------------------
+ * (the plugin path it serves is the reference's bench
+ * timer / balancing loop, cli.py:171-187, balance.py:241).
+ *   ab_ctx_create(device)            context + setup stream on one GPU
+ *   ab_mesh_upload(ctx, desc)        HOST arrays in; on the device: SFC element
+ *                                    order, node windows, Vreman filter width,
+ *                                    lumped mass, CSR pattern (sort/unique),
+ *                                    Laplacian + Dirichlet, gradient operator,
+ *                                    SELL-32, Hilbert row order of the pressure
+ *                                    system (synchronous, setup only)
+ *   ab_state_set / ab_state_get      u [n][3], p [n] from/to host or device
+ *                                    memory (UVA), asynchronous on `stream`
+ *   ab_step(ctx, dt, cg_iters, s)    one fractional step (Algorithm 1): 3 x
+ *                                    (K2 + K8 + K3 + velocity BC), K4, Jacobi-PCG
+ *                                    with cg_iters iterations on P L P^T, K6+K7;
+ *                                    asynchronous, no host synchronisation
+ *   ab_ctx_destroy(ctx)
+ * One context per GPU, one stream at a time, not shared across threads.
+ * Element node order and the bank-spread reference order of the Python setup
+ * are not applied (results differ from FlowSolver's by rounding only). */
+typedef struct ab_ctx ab_ctx;
+typedef struct ab_mesh_desc {
+  int64_t n_nodes;
+  const double* coords;        /* [n_nodes][3], host */
+  double period[3];            /* periodic box lengths, 0 = not periodic */
+  int32_t n_cat, pad_;
+  ab_category cat[5];          /* conn in HOST memory, reference VTK node order */
+  const uint8_t* p_fixed;      /* [n_nodes] pressure Dirichlet nodes (nullable), host */
+  const uint8_t* u_fixed;      /* [n_nodes] velocity Dirichlet bits: 1 x, 2 y, 4 z (nullable), host */
+  const double* u_values;      /* [n_nodes][3] their values (nullable = 0), host */
+  int64_t n_wall_faces;        /* wall-model faces (meshgen.wall_model_bcs), 0 = none */
+  const int32_t* wall_face;    /* [n_wall_faces][4], host */
+  const int32_t* wall_off;     /* [n_wall_faces][4], host */
+  ab_phys phys;
+} ab_mesh_desc;
+typedef struct ab_ctx_info_t {
+  int64_t n_nodes, nnz;
+  int32_t n_cat, ready;
+  int64_t n_elem[5];
+  int64_t n_velocity_bc, n_wall_faces;
+} ab_ctx_info_t;
+int ab_ctx_create(int32_t device, ab_ctx** ctx);
+int ab_ctx_destroy(ab_ctx* ctx);
+int ab_mesh_upload(ab_ctx* ctx, const ab_mesh_desc* desc);
+int ab_ctx_info(const ab_ctx* ctx, ab_ctx_info_t* info);
+int ab_state_set(ab_ctx* ctx, const double* u, const double* p, void* stream);
+int ab_state_get(ab_ctx* ctx, double* u, double* p, void* stream);
+int ab_step(ab_ctx* ctx, double dt, int32_t cg_iters, void* stream);
+
 /* ---- K3: fused RK stage update (one HBM pass) -------------
  *   uout = a*u0 + b*(uprev + k*minv*(rhs - gp));  rhs = 0 afterwards.     */
 int ab_rk_stage(int64_t n, double a, double b, double k, const double* u0, const double* uprev,

@@ -75,8 +75,26 @@ class AbDdcg2Rank(C.Structure):
                    ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX)])
 
 
+class AbMeshDesc(C.Structure):
+    _fields_ = [("n_nodes", i64), ("coords", vp), ("period", f64 * 3), ("n_cat", i32), ("pad_", i32),
+                ("cat", AbCategory * 5), ("p_fixed", vp), ("u_fixed", vp), ("u_values", vp), ("n_wall_faces", i64),
+                ("wall_face", vp), ("wall_off", vp), ("phys", AbPhys)]
+
+
+class AbCtxInfo(C.Structure):
+    _fields_ = [("n_nodes", i64), ("nnz", i64), ("n_cat", i32), ("ready", i32), ("n_elem", i64 * 5),
+                ("n_velocity_bc", i64), ("n_wall_faces", i64)]
+
+
 P = C.POINTER
 _SIGS = {
+    "ab_ctx_create": ([i32, vp], C.c_int),
+    "ab_ctx_destroy": ([vp], C.c_int),
+    "ab_mesh_upload": ([vp, P(AbMeshDesc)], C.c_int),
+    "ab_ctx_info": ([vp, P(AbCtxInfo)], C.c_int),
+    "ab_state_set": ([vp, vp, vp, vp], C.c_int),
+    "ab_state_get": ([vp, vp, vp, vp], C.c_int),
+    "ab_step": ([vp, f64, i32, vp], C.c_int),
     "ab_peer_halo_put": ([P(AbPeerHalo), vp, i32, i32, vp], C.c_int),
     "ab_peer_halo_add": ([P(AbPeerHalo), vp, i32, i32, vp], C.c_int),
     "ab_peer_halo_grid": ([i32], C.c_int),

@@ -16,7 +16,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libalyab200.so"
-SOURCES = ["ab_api.cu", "ab_element.cu", "ab_solver.cu", "ab_node.cu", "ab_gradop.cu", "ab_cg_dd.cu", "ab_wall.cu", "ab_io.cu", "ab_peer.cu"]
+SOURCES = ["ab_api.cu", "ab_element.cu", "ab_solver.cu", "ab_node.cu", "ab_gradop.cu", "ab_cg_dd.cu", "ab_wall.cu", "ab_io.cu", "ab_peer.cu", "ab_session.cu"]
 HEADERS = ["ab_common.cuh", "ab_cg_common.cuh", "ab_tables.inc"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
