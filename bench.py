@@ -200,8 +200,10 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
     return 0, 0
 
 
-# flops per element of K2 as written in the kernel (DESIGN.md §4.1 counts)
-FLOPS_K2 = {"tet4": 417.8}  # ncu (current K2): 138 DFMA + 66 DMUL + 75.8 DADD thread-instructions per tet4 element
+# fp64 flops per element of K2 as the kernel executes them: ncu thread
+# instructions 2 x DFMA + DMUL + DADD per element of each category
+# (profiles/r2_c4_ncu.md, one C4 step; tet4 also r1g on C2: 417.8)
+FLOPS_K2 = {"tet4": 416.7, "pri6": 3867.9, "hex8": 6461.1, "pyr5": 2821.3}
 
 
 def load_peaks():
@@ -221,11 +223,14 @@ def load_fp64_peak():
         return 37.0, "nominal"
 
 
-def load_traffic():
-    p = ROOT / "profiles" / "ncu_traffic.json"
+def load_traffic(workload: str = "c2"):
+    """ncu DRAM bytes per launch of the step kernels of this workload
+    (profiles/ncu_traffic_c4.json for C4, profiles/ncu_traffic.json for C2)."""
+    p = ROOT / "profiles" / ("ncu_traffic_c4.json" if workload == "c4" else "ncu_traffic.json")
     if p.exists():
         try:
-            return json.loads(p.read_text())
+            d = json.loads(p.read_text())
+            return d.get("traffic", d)
         except Exception:
             return {}
     return {}
@@ -244,24 +249,42 @@ def host_cpu() -> dict:
     return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
-def cpu_baseline_sample(steps: int = 2):
-    """Oracle port (numpy, 1 thread) on a bounded sample of the C2 workload."""
-    from threadpoolctl import threadpool_limits
+def cpu_sample(workload: str, scale: float, seed: int = 0):
+    """(oracle, initial state, description) of a bounded CPU sample of the
+    workload: the same recipe at a smaller size (boundary-layer box with the
+    wall model for C3/C4/C5, a jittered Kuhn box for C2)."""
     from oracle import fem
-    from paper_2005_05899_b200 import meshgen
-    with threadpool_limits(1):
-        m = meshgen.box_tets(24, 24, 24, jitter=0.2, seed=20200131)
+    from paper_2005_05899_b200 import dmesh, meshgen
+    if workload == "c2":
+        n = max(4, int(round(88 * scale)))
+        m = meshgen.box_tets(n, n, n, jitter=0.2, seed=20200131 + seed)
         u, p = meshgen.c2_initial(m.coords)
-        o = fem.FlowOracle(m, 1.0, 1e-3, 0.07, p_fixed=meshgen.boundary_nodes(m))
-        st = o.init_state(u, p)
+        o = fem.FlowOracle(m, **PHYS, p_fixed=meshgen.boundary_nodes(m))
+        return o, o.init_state(u, p), m.n_elements, f"jittered Kuhn TET04 {n}^3 cells"
+    spec = dmesh.c3_spec(scale)
+    m = spec.global_mesh()
+    bc, wall = meshgen.wall_model_bcs(m)
+    u = np.zeros((m.n_nodes, 3))
+    u[:, 0] = 1.0
+    o = fem.FlowOracle(m, **PHYS, **bc, wall=wall)
+    return (o, o.init_state(u, np.zeros(m.n_nodes)), m.n_elements,
+            f"mixed boundary-layer box {spec.nx}x{spec.ny}x{spec.nz} cells, {spec.layers} prism layers, wall model "
+            "(the C3/C4 recipe at reduced size)")
+
+
+def cpu_baseline_sample(workload: str = "c4", steps: int = 2):
+    """Oracle port (numpy, 1 thread) on a bounded sample of the workload."""
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):
+        o, st, n_el, what = cpu_sample(workload, 0.12 if workload != "c2" else 24 / 88)
         st = o.step(st, DT, cg_iters=CG_ITERS)  # warm-up
         t0 = time.perf_counter()
         for _ in range(steps):
             st = o.step(st, DT, cg_iters=CG_ITERS)
         dt = time.perf_counter() - t0
-    return {"value": m.n_elements * steps / dt / 1e6, "unit": "M element-steps/s", "cores": 1, "kind": "port",
-            "sample": f"oracle/fem.py FlowOracle, jittered Kuhn TET04 24^3 cells ({m.n_elements} elements), "
-                      f"{steps} full steps (CG {CG_ITERS} it), numpy single thread", **host_cpu()}
+    return {"value": n_el * steps / dt / 1e6, "unit": "M element-steps/s", "cores": 1, "kind": "port",
+            "sample": f"oracle/fem.py FlowOracle, {what} ({n_el} elements), {steps} full steps (CG {CG_ITERS} it), "
+                      "numpy single thread", **host_cpu()}
 
 
 KINDS = ("hex8", "pri6", "pyr5", "tet4")
@@ -428,11 +451,16 @@ def run_native(args):
                       "gflops": F / avg / 1e9 if F and avg > 0 else None}
     dom = max((k for k in kern if k.startswith("K")), key=lambda k: kern[k]["total_ms"])
     peak, peak_kind = load_peaks()
-    traffic = load_traffic().get(dom)
+    traffic = load_traffic(name if ws == 1 else "")
+    traffic = traffic.get(dom) if isinstance(traffic.get(dom), (int, float)) else None
     roof = {"kernel": dom, "bound": "hbm", "achieved": round(kern[dom]["gbs"], 1), "peak": peak, "unit": "GB/s",
             "frac": round(kern[dom]["gbs"] / peak, 4), "peak_source": peak_kind,
             "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"],
             "alg_bytes_definition": "SURVEY.md §8(d) per-unit figure x units per launch"}
+    if traffic:
+        # the same kernel's DRAM bytes (ncu) over this run's launch time
+        roof["frac_dram"] = round(traffic / (kern[dom]["avg_us"] * 1e-6) / 1e9 / peak, 4)
+        roof["traffic_over_alg"] = round(traffic / kern[dom]["alg_bytes"], 4)
     # the element assembly's binding roof is the FP64 pipe
     roof_k2 = None
     if "K2_momentum" in kern and kern["K2_momentum"]["gflops"]:
@@ -440,8 +468,9 @@ def run_native(args):
         ach = kern["K2_momentum"]["gflops"] / 1e3
         roof_k2 = {"kernel": "K2_momentum", "bound": "fp64", "achieved": round(ach, 3), "peak": fp_peak,
                    "unit": "TFLOP/s", "frac": round(ach / fp_peak, 4), "peak_source": fp_src,
-                   "flops_definition": "tet4: 417.8 fp64 flops per element = 2 x 138 DFMA + 66 DMUL + 75.8 DADD "
-                                       "(ncu-counted thread instructions of the current K2), DESIGN.md §4"}
+                   "flops_definition": "fp64 flops per element executed by K2 (ncu thread instructions 2 x DFMA + "
+                                       "DMUL + DADD, profiles/r2_c4_ncu.md): " +
+                                       ", ".join(f"{k} {v}" for k, v in FLOPS_K2.items())}
     if dom == "K5_cg_resident":
         # what this design must move at minimum per iteration: the stored SELL
         # entries (8 B value + 2 B local column, ab_cg_local), the z write and
@@ -487,7 +516,7 @@ def run_native(args):
         result["note"] = f"{ws} ranks on one GPU over {backend}: functional check, not a performance number"
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            result["cpu_baseline"] = cpu_baseline_sample()
+            result["cpu_baseline"] = cpu_baseline_sample(name)
             # the paper's co-execution model with this box's measured rates (context only: no CPU path runs)
             from paper_2005_05899_b200 import coexec
             cb = result["cpu_baseline"]
@@ -530,17 +559,12 @@ def c2_point(args, flush) -> dict:
 
 
 def _ref_worker(args):
-    steps, warmup, seed = args
+    workload, steps, warmup, seed = args
     os.environ["OMP_NUM_THREADS"] = "1"
     from threadpoolctl import threadpool_limits
     sys.path.insert(0, str(ROOT))
-    from oracle import fem
-    from paper_2005_05899_b200 import meshgen
     with threadpool_limits(1):
-        m = meshgen.box_tets(20, 20, 20, jitter=0.2, seed=20200131 + seed)
-        u, p = meshgen.c2_initial(m.coords)
-        o = fem.FlowOracle(m, 1.0, 1e-3, 0.07, p_fixed=meshgen.boundary_nodes(m))
-        st = o.init_state(u, p)
+        o, st, n_el, what = cpu_sample(workload, 0.1 if workload != "c2" else 20 / 88, seed)
         for _ in range(warmup):
             st = o.step(st, DT, cg_iters=CG_ITERS)
         times = []
@@ -548,32 +572,34 @@ def _ref_worker(args):
             t0 = time.perf_counter()
             st = o.step(st, DT, cg_iters=CG_ITERS)
             times.append(time.perf_counter() - t0)
-    return m.n_elements, times
+    return n_el, times, what
 
 
 def run_reference(args):
     """Reference arm: the CPU restatement of the path (oracle port; the
     reference package has no NS step to run), one single-threaded process per
-    host core, each stepping an independent replica of a bounded C2 sample."""
+    host core, each stepping an independent replica of a bounded sample of
+    the workload (the C4 recipe at reduced size by default)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     import multiprocessing as mp
     cores = min(os.cpu_count() or 1, 64)
     steps, warmup = max(1, min(args.steps, 3)), 1
+    name = "c5" if args.weak else args.workload
     with mp.get_context("spawn").Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(steps, warmup, i) for i in range(cores)])
-    n_el = res[0][0]
+        res = pool.map(_ref_worker, [(name, steps, warmup, i) for i in range(cores)])
+    n_el, what = res[0][0], res[0][2]
     per_step = [max(r[1][s] for r in res) for s in range(steps)]
     value = n_el * cores * steps / sum(per_step) / 1e6
-    sample = (f"oracle/fem.py FlowOracle on {cores} processes x jittered Kuhn TET04 20^3 cells ({n_el} elements "
-              f"each), {steps} timed steps after {warmup} warm-up, full step with CG {CG_ITERS} it")
+    sample = (f"oracle/fem.py FlowOracle on {cores} processes x {what} ({n_el} elements each), {steps} timed "
+              f"steps after {warmup} warm-up, full step with CG {CG_ITERS} it")
     out = {"impl": "reference", "metric": "M element-steps/s per time step (assembly + CG)",
            "value": round(value, 5), "unit": "M element-steps/s", "n_gpus": args.gpus, "steps": steps,
            "warmup": warmup, "ms_per_step": round(1e3 * sum(per_step) / steps, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": "C2 sample (BASELINE configs[1] algorithm, bounded size)", "cg_iters": CG_ITERS,
-                      "parallelism": f"{cores} CPU processes"},
+           "config": {"workload": f"{name.upper()} sample (same recipe and algorithm, bounded size: {what})",
+                      "cg_iters": CG_ITERS, "parallelism": f"{cores} CPU processes"},
            "cpu_baseline": {"value": round(value, 5), "unit": "M element-steps/s", "cores": cores, "kind": "port",
                             "sample": sample, **host_cpu()},
            "e2e": {"value": round(value, 5), "unit": "M element-steps/s", "h2d_bytes_per_step": 0,

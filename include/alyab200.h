@@ -209,6 +209,14 @@ int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fix
                double* x, double* r, double* z, double* p, double* q, const double* own, double* red, double* sc,
                double* part, uint32_t* cnt, void* stream);
 int ab_cg_set_bb(double* red, double* sc, void* stream);
+/* Single domain on P A P^T: ab_cg_init + ab_cg_set_bb with the right-hand
+ * side read in node order, r_i = b[perm[i]] (b[perm[i]] = 0 if zero_b);
+ * fixed, dinv in row order.  ab_perm_scatter: out[perm[i]] = in[i] (x back
+ * to node order). */
+int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                    const double* dinv, double* x, double* r, double* z, double* p, double* q, double* red, double* sc,
+                    double* part, uint32_t* cnt, void* stream);
+int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* out, void* stream);
 int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
                const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);
 int ab_cg_dot(int64_t n, const double* z, const double* t, double* p, double* q, const double* own, double* red,

@@ -125,6 +125,8 @@ _SIGS = {
     "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
     "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
+    "ab_cg_init_perm": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_perm_scatter": ([i64, vp, vp, vp, vp], C.c_int),
     "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_dot": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_update": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),

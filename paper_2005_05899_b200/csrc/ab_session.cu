@@ -163,11 +163,6 @@ __global__ void k_gather_u8(int64_t m, const uint8_t* __restrict__ a, const int6
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (k < m) b[k] = a[idx[k]];
 }
-__global__ void k_scatter_f64(int64_t m, const double* __restrict__ a, const int64_t* __restrict__ idx,
-                              double* __restrict__ b) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (k < m) b[idx[k]] = a[k];
-}
 __global__ void k_invert(int64_t n, const int64_t* __restrict__ perm, int64_t* __restrict__ iperm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) iperm[perm[i]] = i;
@@ -179,15 +174,6 @@ __global__ void k_slice_width(int64_t n, const int64_t* __restrict__ rp, int64_t
   int64_t w = 0;
   for (int64_t i = 32 * s; i < 32 * s + 32 && i < n; ++i) w = max(w, rp[i + 1] - rp[i]);
   w32[s] = 32 * w;
-}
-__global__ void k_gather_zero_f64(int64_t n, double* __restrict__ b, const int64_t* __restrict__ perm,
-                                  double* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[i] = b[perm[i]];
-}
-__global__ void k_zero_f64(int64_t n, double* __restrict__ a) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) a[i] = 0.0;
 }
 __global__ void k_set_diag_fixed(int64_t n, const uint8_t* __restrict__ fixed, double* __restrict__ d) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -248,7 +234,7 @@ struct ab_ctx {
   int64_t* perm = nullptr;
   double* dinv_p = nullptr;
   uint8_t* fixed_p = nullptr;
-  double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *bp = nullptr, *xn = nullptr;
+  double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *xn = nullptr;
   double *red = nullptr, *sc = nullptr, *part = nullptr;
   uint32_t* cnt = nullptr;
   // state
@@ -610,7 +596,6 @@ int ab_mesh_upload(ab_ctx* c, const ab_mesh_desc* d) {
   AB_ALLOC(c->z, double, n);
   AB_ALLOC(c->p, double, n);
   AB_ALLOC(c->q, double, n);
-  AB_ALLOC(c->bp, double, n);
   AB_ALLOC(c->xn, double, n);
   AB_ALLOC(c->red, double, 8);
   AB_ALLOC(c->sc, double, 8);
@@ -721,16 +706,13 @@ int ab_step(ab_ctx* c, double dt, int32_t cg_iters, void* stream) {
   }
   AB_TRY(ab_gradop_div(&c->B3, c->U, -c->phys.rho / dt, c->Bv, s));  // K4: b = -(rho/dt) D u_3
   // K5: Jacobi-PCG on P L P^T (b gathered in, x scattered out)
-  k_gather_zero_f64<<<g256(n), 256, 0, s>>>(n, c->Bv, c->perm, c->bp);
-  k_zero_f64<<<g256(n), 256, 0, s>>>(n, c->Bv);
-  AB_TRY(ab_cg_init(n, c->bp, nullptr, c->fixed_p, c->dinv_p, c->x, c->r, c->z, c->p, c->q, nullptr, c->red, c->sc,
-                    c->part, c->cnt, s));
-  AB_TRY(ab_cg_set_bb(c->red, c->sc, s));
+  AB_TRY(ab_cg_init_perm(n, c->perm, c->Bv, 1, c->fixed_p, c->dinv_p, c->x, c->r, c->z, c->p, c->q, c->red, c->sc,
+                         c->part, c->cnt, s));
   for (int it = 0; it < cg_iters; ++it) {
     AB_TRY(ab_cg_spmv(&c->Lp, c->z, c->p, c->q, nullptr, 1, nullptr, c->red, c->sc, c->part, c->cnt, s));
     AB_TRY(ab_cg_update(n, c->p, c->q, c->dinv_p, c->x, c->r, c->z, nullptr, c->red, c->sc, c->part, c->cnt, s));
   }
-  k_scatter_f64<<<g256(n), 256, 0, s>>>(n, c->x, c->perm, c->xn);
+  AB_TRY(ab_perm_scatter(n, c->perm, c->x, c->xn, s));
   // K6 + K7: u = u_3 - dt/rho M^-1 B dp; p += dp; Gp += B dp
   AB_TRY(ab_gradop_correct(&c->B3, c->xn, k, c->U, c->U0, c->minv, c->P, c->GP, s));
   AB_TRY(apply_bc(c, c->U0, s));

@@ -105,6 +105,45 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init(int64_t n, const double* _
   }
 }
 
+// Single-domain init on P A P^T straight from the node-order right-hand
+// side: r_i = b[perm[i]] (b zeroed behind it), and sc[BB] = r.r (no
+// separate set_bb: nothing is all-reduced in between).
+__global__ void __launch_bounds__(kCgBlock) k_cg_init_perm(int64_t n, const int64_t* __restrict__ perm, double* b,
+                                                           int zero_b, const uint8_t* __restrict__ fixed,
+                                                           const double* __restrict__ dinv, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ z,
+                                                           double* __restrict__ p, double* __restrict__ q, double* red,
+                                                           double* sc, double* part, uint32_t* cnt) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
+    const int64_t ni = perm[i];
+    double ri = b[ni];
+    if (zero_b) b[ni] = 0.0;
+    if (fixed && fixed[i]) ri = 0.0;
+    const double zi = dinv[i] * ri;
+    r[i] = ri;
+    z[i] = zi;
+    x[i] = 0.0;
+    p[i] = 0.0;
+    q[i] = 0.0;
+    v[0] += ri * zi;
+    v[1] += ri * ri;
+  }
+  double t[2];
+  if (grid_sum<2, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = t[0];
+    red[AB_RED_RR] = t[1];
+    sc[AB_SC_RZ] = 0.0;
+    sc[AB_SC_BB] = t[1];
+  }
+}
+
+__global__ void k_perm_scatter(int64_t n, const int64_t* __restrict__ perm, const double* __restrict__ in,
+                               double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = in[i];
+}
+
 // Copy red[RR] -> sc[BB] after the (optionally all-reduced) init sums.
 __global__ void k_cg_set_bb(const double* red, double* sc) { sc[AB_SC_BB] = red[AB_RED_RR]; }
 
@@ -530,6 +569,21 @@ int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fix
   k_cg_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, z, p, q, own, red, sc, part,
                                                     cnt);
   return check_launch("ab_cg_init");
+}
+
+int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                    const double* dinv, double* x, double* r, double* z, double* p, double* q, double* red, double* sc,
+                    double* part, uint32_t* cnt, void* stream) {
+  if (n <= 0 || !perm || !b) return fail("ab_cg_init_perm: empty system or null permutation");
+  k_cg_init_perm<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, perm, b, zero_b, fixed, dinv, x, r, z, p, q, red, sc,
+                                                         part, cnt);
+  return check_launch("ab_cg_init_perm");
+}
+
+int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* out, void* stream) {
+  if (n <= 0) return AB_OK;
+  k_perm_scatter<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, perm, in, out);
+  return check_launch("ab_perm_scatter");
 }
 
 int ab_cg_set_bb(double* red, double* sc, void* stream) {

@@ -292,7 +292,7 @@ class PCG:
             pl = order.to(device=dev, dtype=torch.int64).contiguous()
             self.perm2 = dict(A=permute_matrix(A, pl), perm=pl, dinv=dinv[pl].contiguous(),
                               fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
-                              b=z(), x=z())
+                              x=z())
 
     def _m(self, name):
         import contextlib
@@ -356,13 +356,9 @@ class PCG:
         s = stream_handle()
         pm = self.perm2
         A = ctypes.byref(pm["A"].struct)
-        torch.index_select(b, 0, pm["perm"], out=pm["b"])
-        if zero_b:
-            b.zero_()
-        call("ab_cg_init", self.n, ptr(pm["b"]), None, ptr(pm["fixed"]), ptr(pm["dinv"]), ptr(self.x),
-             ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), None, ptr(self.red), ptr(self.sc), ptr(self.part),
-             ptr(self.cnt), s)
-        call("ab_cg_set_bb", ptr(self.red), ptr(self.sc), s)
+        call("ab_cg_init_perm", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
+             ptr(pm["dinv"]), ptr(self.x), ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.red),
+             ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
         it = 0
         while it < maxit:
             if tol > 0 and it % check_every == 0:
@@ -376,7 +372,7 @@ class PCG:
                 call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(pm["dinv"]), ptr(self.x), ptr(self.r),
                      ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             it += 1
-        pm["x"].index_copy_(0, pm["perm"], self.x)
+        call("ab_perm_scatter", self.n, ptr(pm["perm"]), ptr(self.x), ptr(pm["x"]), s)
         return pm["x"], it
 
     def residual(self) -> float:
