@@ -38,6 +38,11 @@ class AbSell(C.Structure):
                 ("vals", vp)]
 
 
+class AbSell16(C.Structure):
+    _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cptr", vp), ("cbase", vp), ("cols", vp),
+                ("vals", vp)]
+
+
 class AbSell3(C.Structure):
     _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cols", vp), ("vx", vp), ("vy", vp),
                 ("vz", vp)]
@@ -125,6 +130,9 @@ _SIGS = {
     "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
     "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
+    "ab_sell16_plan": ([P(AbSell), vp, vp, vp], C.c_int),
+    "ab_sell16_fill": ([P(AbSell), vp, vp, vp, vp], C.c_int),
+    "ab_cg_spmv16": ([P(AbSell16), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_init_perm": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_perm_scatter": ([i64, vp, vp, vp, vp], C.c_int),
     "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),

@@ -374,7 +374,7 @@ class DD2Solver:
                     call(fn, C.byref(r.struct), s)
         for r in self.ranks:
             call("ab_ddcg2_finish", C.byref(r.struct), ptr(r.x_node), s)
-        if tol > 0 or len(self.ranks) > 1:
+        if tol > 0 or (len(self.ranks) > 1 and not torch.cuda.is_current_stream_capturing()):
             for r in self.ranks:
                 if r.failed():
                     raise RuntimeError("decomposed CG: a peer wait timed out (ranks out of step)")

@@ -21,7 +21,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import AbCgLocal, AbSell, AbSell3, call, lib, ptr, stream_handle
+from ._lib import AbCgLocal, AbSell, AbSell3, AbSell16, call, lib, ptr, stream_handle
 from .device import DeviceMesh
 
 
@@ -170,6 +170,27 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
                 nbr_ptr=nbr_ptr)
 
 
+def compress_columns(A: SellMatrix) -> dict:
+    """Column-compressed copy of A's SELL-32 columns (ab_sell16: 16-bit
+    offsets from a per-slice base where the slice's columns span < 64k rows,
+    int32 elsewhere); values and slice pointers are shared with A."""
+    s = stream_handle()
+    dev = A.vals.device
+    ns = A.slice_ptr.numel() - 1
+    cbase = torch.empty(max(1, ns), dtype=torch.int32, device=dev)
+    nbytes = torch.zeros(max(1, ns), dtype=torch.int64, device=dev)
+    call("ab_sell16_plan", ctypes.byref(A.struct), ptr(cbase), ptr(nbytes), s)
+    cptr = torch.zeros(ns + 1, dtype=torch.int64, device=dev)
+    cptr[1:] = torch.cumsum(nbytes[:ns], 0)
+    total = int(cptr[-1].item())
+    cols = torch.zeros(total + 64, dtype=torch.uint8, device=dev)
+    call("ab_sell16_fill", ctypes.byref(A.struct), ptr(cbase), ptr(cptr), ptr(cols), s)
+    struct = AbSell16(n_rows=A.n_rows, n_slices=ns, slice_ptr=ptr(A.slice_ptr), cptr=ptr(cptr), cbase=ptr(cbase),
+                      cols=ptr(cols), vals=ptr(A.vals))
+    near = float((cbase[:ns] >= 0).float().mean().item()) if ns else 1.0
+    return dict(cptr=cptr, cbase=cbase, cols=cols, struct=struct, near_fraction=near, col_bytes=total)
+
+
 def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
     """Assemble L (SPD after Dirichlet rows/cols of ``fixed`` -> identity)."""
     dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
@@ -235,7 +256,7 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
-                 reorder_two_kernel: bool = True):
+                 reorder_two_kernel: bool = True, compress_cols: bool = True):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -293,6 +314,9 @@ class PCG:
             self.perm2 = dict(A=permute_matrix(A, pl), perm=pl, dinv=dinv[pl].contiguous(),
                               fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
                               x=z())
+            # 16-bit columns in the slices whose columns span < 64k rows
+            # (most of them in the Hilbert order): fewer matrix bytes per SpMV
+            self.perm2["A16"] = compress_columns(self.perm2["A"]) if compress_cols else None
 
     def _m(self, name):
         import contextlib
@@ -366,8 +390,12 @@ class PCG:
                 if bb == 0.0 or math.sqrt(rr / bb) <= tol:
                     break
             with self._m("K5_cg_spmv"):
-                call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
-                     ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                if pm["A16"] is not None:
+                    call("ab_cg_spmv16", ctypes.byref(pm["A16"]["struct"]), ptr(self.z), ptr(self.p), ptr(self.q),
+                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                else:
+                    call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
+                         ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             with self._m("K5_cg_update"):
                 call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(pm["dinv"]), ptr(self.x), ptr(self.r),
                      ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
