@@ -555,7 +555,57 @@ def c2_point(args, flush) -> dict:
     e = s_.dm.n_elements
     return {"workload": "C2: jittered Kuhn TET04 88^3 (BASELINE configs[1])", "elements": e,
             "value": round(e * len(ms) / (sum(ms) / 1e3) / 1e6, 3), "ms_per_step": round(float(np.mean(ms)), 4),
-            "steps": len(ms), "warmup": 3}
+            "steps": len(ms), "warmup": 3, "k1_mass": k1_point(s_.dm)}
+
+
+def k1_point(dm) -> dict:
+    """The reference's own kernel (assemble_packs: per-element mass matrices
+    + lumped mass, assembly.py:227-244, :306-333) as K1 on the GPU vs its CPU
+    restatement on this host (oracle element_mass, 1 thread, a 20^3-cell
+    sample of the same recipe); the reference itself cannot run here, its
+    ratio to the restatement was measured in the build container
+    (profiles/r2_reference_k1_calibration.json)."""
+    import ctypes
+    import torch
+    from threadpoolctl import threadpool_limits
+    from oracle import fem
+    from paper_2005_05899_b200 import meshgen
+    from paper_2005_05899_b200._lib import call, ptr, stream_handle
+    E = dm.n_elements
+    ae = torch.empty((E, 4, 4), dtype=torch.float64, device="cuda")
+    ml = torch.zeros(dm.n_nodes, dtype=torch.float64, device="cuda")
+    ts = []
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        call("ab_mass", ctypes.byref(dm.struct), 0, ptr(ae), None, ptr(ml), 128, stream_handle())
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b) / 1e3)
+    gpu = E / float(np.median(ts[1:])) / 1e6
+    with threadpool_limits(1):
+        m = meshgen.box_tets(20, 20, 20, jitter=0.2, seed=20200131)
+        X = fem.element_coords(m.coords, m.conn["tet4"])
+        fem.element_mass(X, "tet4")
+        tc = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            fem.element_mass(X, "tet4")
+            tc.append(time.perf_counter() - t0)
+    port = m.n_elements / float(np.median(tc)) / 1e6
+    cal = {}
+    try:
+        cal = json.loads((ROOT / "profiles" / "r2_reference_k1_calibration.json").read_text())
+    except Exception:
+        pass
+    out = {"gpu_Melem_s": round(gpu, 1), "gpu_ms": round(float(np.median(ts[1:])) * 1e3, 4),
+           "output": "Ae f64[E][4][4] (523 MB) + lumped mass", "cpu_port_Melem_s": round(port, 4),
+           "cpu_port": "oracle/fem.py element_mass (restates assemble_packs), 1 thread, 48000 elements"}
+    if cal.get("port_over_reference"):
+        out["reference_estimate_Melem_s"] = round(port / cal["port_over_reference"], 4)
+        out["reference_estimate"] = ("cpu_port / port_over_reference (reference assemble_packs, pack 32, measured "
+                                     "in the build container)")
+    return out
 
 
 def _ref_worker(args):
