@@ -217,6 +217,22 @@ int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, c
                     const double* dinv, double* x, double* r, double* z, double* p, double* q, double* red, double* sc,
                     double* part, uint32_t* cnt, void* stream);
 int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* out, void* stream);
+/* Symmetrically scaled single-domain form: Jacobi-PCG on A is plain CG on
+ * A' = D^-1/2 A D^-1/2 (same iterates in exact arithmetic), with r' =
+ * D^-1/2 r playing z's role, so per iteration neither z nor D^-1 moves (16
+ * bytes per row less).  ab_sell_symscale: vals *= s_row s_col (s = d^-1/2,
+ * row order, on a copy the caller owns); init: r'_i = s_i b[perm[i]];
+ * the SpMV is ab_cg_spmv / ab_cg_spmv16 with z := r'; update: x' += alpha p,
+ * r' -= alpha q, red[RZN] = r'.r', red[RR] = sum d r'^2 (d non-NULL, when a
+ * tolerance is tested) or r'.r'; finish: out[perm[i]] = s_i x'_i. */
+int ab_sell_symscale(const ab_sell* a, const double* s, void* stream);
+int ab_cg_init_scaled(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                      const double* s, const double* d, double* x, double* r, double* p, double* q, double* red,
+                      double* sc, double* part, uint32_t* cnt, void* stream);
+int ab_cg_update_scaled(int64_t n, const double* p, const double* q, double* x, double* r, const double* d,
+                        double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
+int ab_cg_finish_scaled(int64_t n, const int64_t* perm, const double* s, const double* x, double* out,
+                        void* stream);
 int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
                const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);
 /* Column-compressed SELL-32 for the single-domain two-kernel CG: the same

@@ -144,6 +144,100 @@ __global__ void k_perm_scatter(int64_t n, const int64_t* __restrict__ perm, cons
   if (i < n) out[perm[i]] = in[i];
 }
 
+// ---------------------------------------------------------------------------
+// Symmetrically scaled form (single domain, two kernels).  Jacobi-PCG on A
+// is plain CG on A' = D^-1/2 A D^-1/2 with r' = D^-1/2 r, x = D^-1/2 x'
+// (the same iterates in exact arithmetic): z = D^-1 r becomes r' itself, so
+// per iteration the z write and the D^-1 read disappear (16 bytes per row)
+// and r.z = r'.r'.  ||r||^2 = sum d r'^2 is formed only when a tolerance is
+// tested (d non-NULL).
+// ---------------------------------------------------------------------------
+__global__ void k_sell_symscale(int64_t n, const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
+                                double* __restrict__ sval, const double* __restrict__ s) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t sl = i >> 5;
+  const int lane = (int)(i & 31);
+  const double si = s[i];
+  for (int64_t k = sp[sl] + lane; k < sp[sl + 1]; k += 32) sval[k] *= si * s[scol[k]];
+}
+
+__global__ void __launch_bounds__(kCgBlock) k_cg_init_scaled(int64_t n, const int64_t* __restrict__ perm, double* b,
+                                                             int zero_b, const uint8_t* __restrict__ fixed,
+                                                             const double* __restrict__ s,
+                                                             const double* __restrict__ d, double* __restrict__ x,
+                                                             double* __restrict__ r, double* __restrict__ p,
+                                                             double* __restrict__ q, double* red, double* sc,
+                                                             double* part, uint32_t* cnt) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
+    const int64_t ni = perm[i];
+    double bi = b[ni];
+    if (zero_b) b[ni] = 0.0;
+    if (fixed && fixed[i]) bi = 0.0;
+    const double ri = s[i] * bi;
+    r[i] = ri;
+    x[i] = 0.0;
+    p[i] = 0.0;
+    q[i] = 0.0;
+    v[0] += ri * ri;
+    v[1] += d ? d[i] * ri * ri : ri * ri;
+  }
+  double t[2];
+  if (grid_sum<2, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = t[0];
+    red[AB_RED_RR] = t[1];
+    sc[AB_SC_RZ] = 0.0;
+    sc[AB_SC_BB] = t[1];
+  }
+}
+
+__global__ void __launch_bounds__(kCgBlock) k_cg_update_scaled(int64_t n, const double* __restrict__ p,
+                                                               const double* __restrict__ q, double* __restrict__ x,
+                                                               double* __restrict__ r, const double* __restrict__ d,
+                                                               double* red, const double* sc, double* part,
+                                                               uint32_t* cnt) {
+  double v[2] = {0.0, 0.0};
+  const int64_t i = 2 * ((int64_t)blockIdx.x * kCgBlock + threadIdx.x);
+  const double pq = red[AB_RED_PQ];
+  const double rz = sc[AB_SC_RZ];
+  const double alpha = pq != 0.0 ? rz / pq : 0.0;
+  if (i + 1 < n) {
+    const double2 pv = *reinterpret_cast<const double2*>(p + i);
+    const double2 xv = *reinterpret_cast<const double2*>(x + i);
+    const double2 qv = *reinterpret_cast<const double2*>(q + i);
+    const double2 rv = *reinterpret_cast<const double2*>(r + i);
+    const double r0 = fma(-alpha, qv.x, rv.x), r1 = fma(-alpha, qv.y, rv.y);
+    *reinterpret_cast<double2*>(x + i) = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    *reinterpret_cast<double2*>(r + i) = make_double2(r0, r1);
+    v[0] = r0 * r0 + r1 * r1;
+    if (d) {
+      const double2 dv = __ldg(reinterpret_cast<const double2*>(d + i));
+      v[1] = dv.x * r0 * r0 + dv.y * r1 * r1;
+    } else {
+      v[1] = v[0];
+    }
+  } else if (i < n) {
+    x[i] = fma(alpha, p[i], x[i]);
+    const double ri = fma(-alpha, q[i], r[i]);
+    r[i] = ri;
+    v[0] = ri * ri;
+    v[1] = d ? d[i] * ri * ri : ri * ri;
+  }
+  double tot[2];
+  if (grid_sum<2, kCgBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = tot[0];
+    red[AB_RED_RR] = tot[1];
+  }
+}
+
+// x_node[perm[i]] = s_i x'_i
+__global__ void k_cg_finish_scaled(int64_t n, const int64_t* __restrict__ perm, const double* __restrict__ s,
+                                   const double* __restrict__ x, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = s[i] * x[i];
+}
+
 // Copy red[RR] -> sc[BB] after the (optionally all-reduced) init sums.
 __global__ void k_cg_set_bb(const double* red, double* sc) { sc[AB_SC_BB] = red[AB_RED_RR]; }
 
@@ -641,6 +735,36 @@ int ab_cg_init(int64_t n, const double* b_in, double* b_zero, const uint8_t* fix
   k_cg_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, b_in, b_zero, fixed, dinv, x, r, z, p, q, own, red, sc, part,
                                                     cnt);
   return check_launch("ab_cg_init");
+}
+
+int ab_sell_symscale(const ab_sell* a, const double* s, void* stream) {
+  if (!a || !s) return fail("ab_sell_symscale: null argument");
+  if (a->n_rows > 0)
+    k_sell_symscale<<<grid_for(a->n_rows, 256), 256, 0, S(stream)>>>(a->n_rows, a->slice_ptr, a->cols,
+                                                                     const_cast<double*>(a->vals), s);
+  return check_launch("ab_sell_symscale");
+}
+
+int ab_cg_init_scaled(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                      const double* s, const double* d, double* x, double* r, double* p, double* q, double* red,
+                      double* sc, double* part, uint32_t* cnt, void* stream) {
+  if (n <= 0 || !perm || !b || !s) return fail("ab_cg_init_scaled: empty system or null argument");
+  k_cg_init_scaled<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, perm, b, zero_b, fixed, s, d, x, r, p, q, red, sc, part,
+                                                           cnt);
+  return check_launch("ab_cg_init_scaled");
+}
+
+int ab_cg_update_scaled(int64_t n, const double* p, const double* q, double* x, double* r, const double* d,
+                        double* red, const double* sc, double* part, uint32_t* cnt, void* stream) {
+  k_cg_update_scaled<<<grid_for((n + 1) / 2, kCgBlock), kCgBlock, 0, S(stream)>>>(n, p, q, x, r, d, red, sc, part,
+                                                                                cnt);
+  return check_launch("ab_cg_update_scaled");
+}
+
+int ab_cg_finish_scaled(int64_t n, const int64_t* perm, const double* s, const double* x, double* out,
+                        void* stream) {
+  if (n > 0) k_cg_finish_scaled<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, perm, s, x, out);
+  return check_launch("ab_cg_finish_scaled");
 }
 
 int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,

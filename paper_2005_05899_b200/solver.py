@@ -256,7 +256,7 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
-                 reorder_two_kernel: bool = True, compress_cols: bool = True):
+                 reorder_two_kernel: bool = True, compress_cols: bool = True, scaled: bool = True):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -313,7 +313,12 @@ class PCG:
             pl = order.to(device=dev, dtype=torch.int64).contiguous()
             self.perm2 = dict(A=permute_matrix(A, pl), perm=pl, dinv=dinv[pl].contiguous(),
                               fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
-                              x=z())
+                              x=z(), scaled=bool(scaled))
+            if scaled:
+                # CG on D^-1/2 P A P^T D^-1/2 (the permuted copy's values are scaled in place)
+                self.perm2["s"] = torch.sqrt(self.perm2["dinv"]).contiguous()
+                self.perm2["d"] = (1.0 / self.perm2["dinv"]).contiguous()
+                call("ab_sell_symscale", ctypes.byref(self.perm2["A"].struct), ptr(self.perm2["s"]), stream_handle())
             # 16-bit columns in the slices whose columns span < 64k rows
             # (most of them in the Hilbert order): fewer matrix bytes per SpMV
             self.perm2["A16"] = compress_columns(self.perm2["A"]) if compress_cols else None
@@ -380,9 +385,17 @@ class PCG:
         s = stream_handle()
         pm = self.perm2
         A = ctypes.byref(pm["A"].struct)
-        call("ab_cg_init_perm", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
-             ptr(pm["dinv"]), ptr(self.x), ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.red),
-             ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+        sc_ = pm["scaled"]
+        d = pm["d"] if (sc_ and tol > 0) else None  # true ||r|| only when a tolerance is tested
+        if sc_:
+            call("ab_cg_init_scaled", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
+                 ptr(pm["s"]), ptr(d), ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.q), ptr(self.red),
+                 ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+        else:
+            call("ab_cg_init_perm", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
+                 ptr(pm["dinv"]), ptr(self.x), ptr(self.r), ptr(self.z), ptr(self.p), ptr(self.q), ptr(self.red),
+                 ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+        zvec = self.r if sc_ else self.z  # the scaled form gathers r' where Jacobi gathers z
         it = 0
         while it < maxit:
             if tol > 0 and it % check_every == 0:
@@ -391,16 +404,23 @@ class PCG:
                     break
             with self._m("K5_cg_spmv"):
                 if pm["A16"] is not None:
-                    call("ab_cg_spmv16", ctypes.byref(pm["A16"]["struct"]), ptr(self.z), ptr(self.p), ptr(self.q),
+                    call("ab_cg_spmv16", ctypes.byref(pm["A16"]["struct"]), ptr(zvec), ptr(self.p), ptr(self.q),
                          ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
                 else:
-                    call("ab_cg_spmv", A, ptr(self.z), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
+                    call("ab_cg_spmv", A, ptr(zvec), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
                          ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             with self._m("K5_cg_update"):
-                call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(pm["dinv"]), ptr(self.x), ptr(self.r),
-                     ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                if sc_:
+                    call("ab_cg_update_scaled", self.n, ptr(self.p), ptr(self.q), ptr(self.x), ptr(self.r), ptr(d),
+                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                else:
+                    call("ab_cg_update", self.n, ptr(self.p), ptr(self.q), ptr(pm["dinv"]), ptr(self.x),
+                         ptr(self.r), ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             it += 1
-        call("ab_perm_scatter", self.n, ptr(pm["perm"]), ptr(self.x), ptr(pm["x"]), s)
+        if sc_:
+            call("ab_cg_finish_scaled", self.n, ptr(pm["perm"]), ptr(pm["s"]), ptr(self.x), ptr(pm["x"]), s)
+        else:
+            call("ab_perm_scatter", self.n, ptr(pm["perm"]), ptr(self.x), ptr(pm["x"]), s)
         return pm["x"], it
 
     def residual(self) -> float:

@@ -144,7 +144,8 @@ CG_VARIANTS = {
     "local-sfc": dict(order=True),          # ab_cg_resident_local, SFC row order, z gathers from shared memory
     "local": dict(),                        # local column map, node order
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
-    "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on P A P^T (SFC row order)
+    "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC order, 16-bit cols)
+    "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False, compress_cols=False),  # z = D^-1 r form
 }
 
 
@@ -168,7 +169,7 @@ def test_pcg_fixed_iterations_and_convergence(name, variant):
     # fixed iteration count: same iterate as the oracle
     pcg = PCG(A, dinv, fixed=torch.from_numpy(fixed), **kw)
     assert pcg.resident == (not variant.startswith("two-kernel"))
-    assert (pcg.perm2 is not None) == (variant == "two-kernel-sfc")
+    assert (pcg.perm2 is not None) == variant.startswith("two-kernel-sfc")
     if variant in ("local-sfc", "local"):
         assert pcg.local is not None
     bt = torch.from_numpy(b).cuda()
