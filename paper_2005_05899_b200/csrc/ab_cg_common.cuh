@@ -100,16 +100,20 @@ __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, c
 // rows, else as int32 (cbase[s] = -1); the branch is uniform per warp (one
 // slice = one warp) and the FMA order is sell_row_dot's, so the result is
 // bitwise the same.
+#ifndef SPMV16_CHUNK
+#define SPMV16_CHUNK 16
+#endif
 template <bool NEAR>
 __device__ __forceinline__ double sell16_row_body(const unsigned char* __restrict__ cb, int64_t cofs, int cbase,
                                                   const double* __restrict__ sval, int64_t base, int lane, int width,
                                                   const double* zv) {
+  constexpr int CH = SPMV16_CHUNK;
   double acc = 0.0;
-  for (int j0 = 0; j0 < width; j0 += kChunk) {
-    int c[kChunk];
-    double a[kChunk];
+  for (int j0 = 0; j0 < width; j0 += CH) {
+    int c[CH];
+    double a[CH];
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) {
+    for (int u = 0; u < CH; ++u) {
       const bool ok = j0 + u < width;
       const int64_t k = (int64_t)(j0 + u) * 32 + lane;
       if constexpr (NEAR)
@@ -118,11 +122,11 @@ __device__ __forceinline__ double sell16_row_body(const unsigned char* __restric
         c[u] = ok ? __ldcs(reinterpret_cast<const int32_t*>(cb + cofs) + k) : 0;
       a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
     }
-    double g[kChunk];
+    double g[CH];
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) g[u] = zv[c[u]];
+    for (int u = 0; u < CH; ++u) g[u] = zv[c[u]];
 #pragma unroll
-    for (int u = 0; u < kChunk; ++u) acc = fma(a[u], g[u], acc);
+    for (int u = 0; u < CH; ++u) acc = fma(a[u], g[u], acc);
   }
   return acc;
 }

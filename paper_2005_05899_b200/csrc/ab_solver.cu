@@ -279,7 +279,10 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* 
 
 // Single domain on the column-compressed SELL (ab_sell16): the DOT form of
 // k_cg_spmv with 2-byte columns in the slices that allow them.
-__global__ void __launch_bounds__(kCgBlock) k_cg_spmv16(int64_t n, const int64_t* __restrict__ sp,
+#ifndef SPMV16_MINB
+#define SPMV16_MINB 1
+#endif
+__global__ void __launch_bounds__(kCgBlock, SPMV16_MINB) k_cg_spmv16(int64_t n, const int64_t* __restrict__ sp,
                                                         const int64_t* __restrict__ cptr,
                                                         const int32_t* __restrict__ cbase,
                                                         const unsigned char* __restrict__ cb,
