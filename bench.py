@@ -183,6 +183,8 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
         return 48 * N, 6 * N
     if kernel == "K5_cg_update":    # x p r q dinv in, x r z out
         return 64 * N, 10 * N
+    if kernel == "K5_cg_update_scaled":  # symmetrically scaled form: x p r q in, x r out (no z, no D^-1)
+        return 48 * N, 8 * N
     if kernel == "K2_momentum":     # conn, coords, u in; rhs out
         return conn_bytes + 48 * N + 24 * N, sum(FLOPS_K2.get(r, 0) * e for r, e in counts.items())
     if kernel == "K3_rk_stage":     # u0 uprev rhs gp in (24 B each), minv, uout + rhs zero out

@@ -280,7 +280,7 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* 
 // Single domain on the column-compressed SELL (ab_sell16): the DOT form of
 // k_cg_spmv with 2-byte columns in the slices that allow them.
 #ifndef SPMV16_MINB
-#define SPMV16_MINB 1
+#define SPMV16_MINB 8  // 32 registers, full occupancy (1 block: 90 registers, 2x slower)
 #endif
 __global__ void __launch_bounds__(kCgBlock, SPMV16_MINB) k_cg_spmv16(int64_t n, const int64_t* __restrict__ sp,
                                                         const int64_t* __restrict__ cptr,
