@@ -504,8 +504,10 @@ typedef struct ab_ddcg2_rank {
   const double* dinv;                 /* row order, D of the assembled global operator */
   const uint8_t* fixed;               /* row order, nullable */
   const double* own;                  /* row order: 1 on the lowest sharing rank, else 0 */
+  const double* s;                    /* scaled != 0: D^-1/2 (row order); the values are those of
+                                         D^-1/2 P L P^T D^-1/2 and r' takes z's role (ab_sell_symscale) */
   const int32_t* perm;                /* row -> local node */
-  double *x, *r, *z, *p, *q;          /* row order */
+  double *x, *r, *z, *p, *q;          /* row order (z unused when scaled) */
   double* tif;                        /* [n_if] this rank's (A z) at the interface rows */
   const int32_t* send_ptr;            /* [n_if + 1] into send_peer / send_off */
   const int32_t* send_peer;           /* index into peer_* */
@@ -520,7 +522,7 @@ typedef struct ab_ddcg2_rank {
   uint32_t* cnt;                      /* grid-sum counters (zeroed once) */
   double* scal;                       /* [AB_D2_NSCAL] */
   int32_t nsig;                       /* blocks of this rank's SpMV holding interface rows */
-  int32_t pad_;
+  int32_t scaled;                     /* symmetrically scaled form (see s) */
   int32_t peer_rank[AB_PEER_MAX];
   int32_t peer_nsig[AB_PEER_MAX];     /* that peer's signalling blocks (0: not a neighbour) */
   double* peer_recv[AB_PEER_MAX];     /* mapped */

@@ -73,10 +73,10 @@ class AbPeerHalo(C.Structure):
 class AbDdcg2Rank(C.Structure):
     _fields_ = ([("n_rows", i64), ("n_if", i64), ("rank", i32), ("n_ranks", i32), ("n_peers", i32),
                  ("recv_stride", i32)]
-                + [(n, vp) for n in ("slice_ptr", "cols", "vals", "dinv", "fixed", "own", "perm", "x", "r", "z",
+                + [(n, vp) for n in ("slice_ptr", "cols", "vals", "dinv", "fixed", "own", "s", "perm", "x", "r", "z",
                                      "p", "q", "tif", "send_ptr", "send_peer", "send_off", "recv_ptr", "recv_rank",
                                      "recv_off", "recv", "cnt_in", "rec", "part", "cnt", "scal")]
-                + [("nsig", i32), ("pad_", i32), ("peer_rank", i32 * PEER_MAX), ("peer_nsig", i32 * PEER_MAX),
+                + [("nsig", i32), ("scaled", i32), ("peer_rank", i32 * PEER_MAX), ("peer_nsig", i32 * PEER_MAX),
                    ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX)])
 
 

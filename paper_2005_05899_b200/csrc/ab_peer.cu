@@ -15,7 +15,7 @@
 namespace ab {
 
 static_assert(sizeof(ab_peer_halo) == 272, "ab_peer_halo layout (mirrored by _lib.AbPeerHalo)");
-static_assert(sizeof(ab_ddcg2_rank) == 496, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
+static_assert(sizeof(ab_ddcg2_rank) == 504, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
 
 constexpr int kPeerBlock = 256;
 constexpr long long kPeerTimeoutNs = 10000000000ll;
@@ -196,15 +196,21 @@ __global__ void __launch_bounds__(kD2Block) k_d2_init(ab_ddcg2_rank d, const dou
     const int64_t ni = d.perm[i];
     double ri = b[ni];
     if (d.fixed && d.fixed[i]) ri = 0.0;
-    const double zi = d.dinv[i] * ri;
+    const double w = d.own[i];
+    if (d.scaled) {  // r' = D^-1/2 r; r.z = r'.r'; ||r||^2 = sum r'^2 / dinv when a tolerance is tested
+      ri *= d.s[i];
+      v[0] += w * ri * ri;
+      v[1] += tol > 0.0 ? w * ri * ri / d.dinv[i] : w * ri * ri;
+    } else {
+      const double zi = d.dinv[i] * ri;
+      d.z[i] = zi;
+      v[0] += w * ri * zi;
+      v[1] += w * ri * ri;
+    }
     d.r[i] = ri;
-    d.z[i] = zi;
     d.x[i] = 0.0;
     d.p[i] = 0.0;
     d.q[i] = 0.0;
-    const double w = d.own[i];
-    v[0] += w * ri * zi;
-    v[1] += w * ri * ri;
   }
   double tot[2];
   if (grid_sum<2, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
@@ -252,13 +258,14 @@ __global__ void __launch_bounds__(kD2Block) k_d2_spmv(ab_ddcg2_rank d) {
   const double beta = it > 0 && rz_old != 0.0 ? rz_new / rz_old : 0.0;
   const int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x;
   double v[1] = {0.0};
+  const double* zv = d.scaled ? d.r : d.z;  // the scaled form gathers r' where Jacobi gathers z
   if (i < d.n_rows) {
-    const double az = sell_row_dot(d.slice_ptr, d.cols, d.vals, d.z, i);
+    const double az = sell_row_dot(d.slice_ptr, d.cols, d.vals, zv, i);
     if (i < d.n_if) {
       d.tif[i] = az;
       for (int e = d.send_ptr[i]; e < d.send_ptr[i + 1]; ++e) d.peer_recv[d.send_peer[e]][d.send_off[e]] = az;
     } else {
-      const double pi = fma(beta, d.p[i], d.z[i]);
+      const double pi = fma(beta, d.p[i], zv[i]);
       const double qi = fma(beta, d.q[i], az);
       d.p[i] = pi;
       d.q[i] = qi;
@@ -311,7 +318,7 @@ __global__ void __launch_bounds__(kD2Block) k_d2_iface(ab_ddcg2_rank d) {
         t += __ldcg(d.recv + d.recv_off[e]);
       }
       if (!mine) t += own_t;
-      const double pi = fma(beta, d.p[i], d.z[i]);
+      const double pi = fma(beta, d.p[i], d.scaled ? d.r[i] : d.z[i]);
       const double qi = fma(beta, d.q[i], t);
       d.p[i] = pi;
       d.q[i] = qi;
@@ -354,15 +361,21 @@ __global__ void __launch_bounds__(kD2Block) k_d2_update(ab_ddcg2_rank d) {
   const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
   double v[2] = {0.0, 0.0};
   const int64_t i = 2 * ((int64_t)blockIdx.x * kD2Block + threadIdx.x);
+  const bool true_norm = d.scal[AB_D2_TOL] > 0.0;
   for (int64_t k = i; k < i + 2 && k < d.n_rows; ++k) {
     d.x[k] = fma(alpha, d.p[k], d.x[k]);
     const double rk = fma(-alpha, d.q[k], d.r[k]);
-    const double zk = d.dinv[k] * rk;
     d.r[k] = rk;
-    d.z[k] = zk;
     const double w = d.own[k];
-    v[0] += w * rk * zk;
-    v[1] += w * rk * rk;
+    if (d.scaled) {
+      v[0] += w * rk * rk;
+      v[1] += true_norm ? w * rk * rk / d.dinv[k] : w * rk * rk;
+    } else {
+      const double zk = d.dinv[k] * rk;
+      d.z[k] = zk;
+      v[0] += w * rk * zk;
+      v[1] += w * rk * rk;
+    }
   }
   double tot[2];
   if (grid_sum<2, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
@@ -376,7 +389,7 @@ __global__ void __launch_bounds__(kD2Block) k_d2_update(ab_ddcg2_rank d) {
 
 __global__ void k_d2_finish(ab_ddcg2_rank d, double* __restrict__ x_node) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < d.n_rows) x_node[d.perm[i]] = d.x[i];
+  if (i < d.n_rows) x_node[d.perm[i]] = d.scaled ? d.s[i] * d.x[i] : d.x[i];
 }
 
 }  // namespace ab

@@ -224,7 +224,8 @@ class DD2Rank:
     first, in this order, then the interior nodes in this order)."""
 
     def __init__(self, rank: int, n_ranks: int, A: SellMatrix, dinv: torch.Tensor, own, shared: dict,
-                 order: torch.Tensor, fixed: torch.Tensor | None = None, max_shared: int | None = None):
+                 order: torch.Tensor, fixed: torch.Tensor | None = None, max_shared: int | None = None,
+                 scaled: bool = True):
         dev = A.vals.device
         n = A.n_rows
         self.rank, self.n_ranks, self.n = rank, n_ranks, n
@@ -241,6 +242,12 @@ class DD2Rank:
         iperm[perm] = torch.arange(n, device=dev)
         self.A = permute_matrix(A, self.perm)
         self.dinv = dinv.to(dev)[perm].contiguous()
+        # symmetrically scaled form (CG on D^-1/2 A D^-1/2, D the GLOBAL diagonal, so every rank scales its
+        # partial rows alike): no z vector and no D^-1 stream per iteration
+        self.scaled = bool(scaled)
+        self.s = torch.sqrt(self.dinv).contiguous() if scaled else None
+        if scaled:
+            call("ab_sell_symscale", C.byref(self.A.struct), ptr(self.s), stream_handle())
         self.fixed = fixed.to(device=dev, dtype=torch.uint8)[perm].contiguous() if fixed is not None else None
         self.own = torch.as_tensor(np.asarray(own), dtype=torch.float64, device=dev)[perm].contiguous()
         self.M = int(max_shared if max_shared is not None else max([0] + [len(v) for v in shared.values()]))
@@ -302,7 +309,8 @@ class DD2Rank:
         d = AbDdcg2Rank(n_rows=self.n, n_if=self.n_if, rank=self.rank, n_ranks=self.n_ranks,
                         n_peers=len(self.peers), recv_stride=self.M)
         for name, t in (("slice_ptr", self.A.slice_ptr), ("cols", self.A.cols), ("vals", self.A.vals),
-                        ("dinv", self.dinv), ("fixed", self.fixed), ("own", self.own), ("perm", self.perm),
+                        ("dinv", self.dinv), ("fixed", self.fixed), ("own", self.own), ("s", self.s),
+                        ("perm", self.perm),
                         ("x", self.x), ("r", self.r), ("z", self.zv), ("p", self.p), ("q", self.q),
                         ("tif", self.tif), ("send_ptr", self.send_ptr), ("send_peer", self.send_peer),
                         ("send_off", self.send_off), ("recv_ptr", self.recv_ptr), ("recv_rank", self.recv_rank),
@@ -310,6 +318,7 @@ class DD2Rank:
                         ("rec", self.rec), ("part", self.part), ("cnt", self.cnt), ("scal", self.scal)):
             setattr(d, name, ptr(t))
         d.nsig = self.nsig
+        d.scaled = 1 if self.scaled else 0
         for k, q in enumerate(self.peers):
             d.peer_rank[k] = q
             d.peer_nsig[k] = int(peers[q]["nsig"]) if q in self.neighbors else 0

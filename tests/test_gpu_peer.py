@@ -62,7 +62,7 @@ def test_peer_halo_sum_rank_ordered(P):
     assert all(not h.failed() for h in halos)
 
 
-def _dd2_setup(P, spec=SPEC):
+def _dd2_setup(P, spec=SPEC, scaled=True):
     from paper_2005_05899_b200.device import DeviceMesh
     from paper_2005_05899_b200.peer import DD2Rank, virtual_dd2
     from paper_2005_05899_b200.solver import assemble_laplacian
@@ -79,15 +79,17 @@ def _dd2_setup(P, spec=SPEC):
         fl = torch.from_numpy(fixed[plan.l2g])
         A = assemble_laplacian(dm, fl)
         dinv = torch.from_numpy(1.0 / dglob[plan.l2g]).cuda()
-        ranks.append(DD2Rank(r, P, A, dinv, plan.own, plan.shared, dm.node_order(), fixed=fl, max_shared=ms))
+        ranks.append(DD2Rank(r, P, A, dinv, plan.own, plan.shared, dm.node_order(), fixed=fl, max_shared=ms,
+                             scaled=scaled))
     virtual_dd2(ranks)
     return L, fixed, locs, ranks
 
 
-@pytest.mark.parametrize("P", [2, 3, 4])
-def test_dd2_cg_matches_single_domain(P):
+@pytest.mark.parametrize("P,scaled", [(2, True), (3, True), (4, True), (3, False)])
+def test_dd2_cg_matches_single_domain(P, scaled):
+    """scaled: CG on D^-1/2 A D^-1/2 (default); False: the Jacobi z-form."""
     from paper_2005_05899_b200.peer import DD2Solver
-    L, fixed, locs, ranks = _dd2_setup(P)
+    L, fixed, locs, ranks = _dd2_setup(P, scaled=scaled)
     assert all(r.n_if > 0 for r in ranks)
     b = np.random.default_rng(11).standard_normal(L.shape[0])
     b[fixed] = 0.0
