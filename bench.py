@@ -438,17 +438,17 @@ def run_native(args):
     solver._step_body(DT, args.cg_iters, 0.0)
     torch.cuda.synchronize()
     per = {}
-    for name, a, b in solver.timeline:
-        per.setdefault(name, []).append(a.elapsed_time(b) / 1e3)
+    for kname, a, b in solver.timeline:
+        per.setdefault(kname, []).append(a.elapsed_time(b) / 1e3)
     solver.timeline = None
     counts = solver.dm.element_counts()
     nnz = solver.L.nnz
     kern = {}
-    for name, ts in per.items():
-        B, F = algorithmic_cost(name, counts, solver.n, nnz, args.cg_iters,
+    for kname, ts in per.items():
+        B, F = algorithmic_cost(kname, counts, solver.n, nnz, args.cg_iters,
                                 n_faces=solver.wall.n_faces if solver.wall is not None else 0)
         avg = float(np.mean(ts))
-        kern[name] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
+        kern[kname] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
                       "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,
                       "gflops": F / avg / 1e9 if F and avg > 0 else None}
     dom = max((k for k in kern if k.startswith("K")), key=lambda k: kern[k]["total_ms"])

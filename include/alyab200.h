@@ -224,14 +224,15 @@ int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* ou
  * row order, on a copy the caller owns); init: r'_i = s_i b[perm[i]];
  * the SpMV is ab_cg_spmv / ab_cg_spmv16 with z := r'; update: x' += alpha p,
  * r' -= alpha q, red[RZN] = r'.r', red[RR] = sum d r'^2 (d non-NULL, when a
- * tolerance is tested) or r'.r'; finish: out[perm[i]] = s_i x'_i. */
+ * tolerance is tested) or r'.r'; finish: out[j] = s_i x'_i, i = iperm[j]
+ * (the inverse permutation: coalesced writes). */
 int ab_sell_symscale(const ab_sell* a, const double* s, void* stream);
 int ab_cg_init_scaled(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
                       const double* s, const double* d, double* x, double* r, double* p, double* q, double* red,
                       double* sc, double* part, uint32_t* cnt, void* stream);
 int ab_cg_update_scaled(int64_t n, const double* p, const double* q, double* x, double* r, const double* d,
                         double* red, const double* sc, double* part, uint32_t* cnt, void* stream);
-int ab_cg_finish_scaled(int64_t n, const int64_t* perm, const double* s, const double* x, double* out,
+int ab_cg_finish_scaled(int64_t n, const int64_t* iperm, const double* s, const double* x, double* out,
                         void* stream);
 int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
                const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);

@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init_perm(int64_t n, const int6
   for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
     const int64_t ni = perm[i];
     double ri = b[ni];
-    if (zero_b) b[ni] = 0.0;
     if (fixed && fixed[i]) ri = 0.0;
     const double zi = dinv[i] * ri;
     r[i] = ri;
@@ -173,7 +172,6 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_init_scaled(int64_t n, const in
   for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
     const int64_t ni = perm[i];
     double bi = b[ni];
-    if (zero_b) b[ni] = 0.0;
     if (fixed && fixed[i]) bi = 0.0;
     const double ri = s[i] * bi;
     r[i] = ri;
@@ -231,11 +229,15 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_update_scaled(int64_t n, const 
   }
 }
 
-// x_node[perm[i]] = s_i x'_i
-__global__ void k_cg_finish_scaled(int64_t n, const int64_t* __restrict__ perm, const double* __restrict__ s,
+// out[j] = s_i x'_i with i = iperm[j] (node j's solver row): coalesced
+// writes, gathered reads (a scatter through perm writes partial sectors)
+__global__ void k_cg_finish_scaled(int64_t n, const int64_t* __restrict__ iperm, const double* __restrict__ s,
                                    const double* __restrict__ x, double* __restrict__ out) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) out[perm[i]] = s[i] * x[i];
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const int64_t i = iperm[j];
+    out[j] = s[i] * x[i];
+  }
 }
 
 // Copy red[RR] -> sc[BB] after the (optionally all-reduced) init sums.
@@ -754,6 +756,10 @@ int ab_cg_init_scaled(int64_t n, const int64_t* perm, double* b, int32_t zero_b,
   if (n <= 0 || !perm || !b || !s) return fail("ab_cg_init_scaled: empty system or null argument");
   k_cg_init_scaled<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, perm, b, zero_b, fixed, s, d, x, r, p, q, red, sc, part,
                                                            cnt);
+  // b is zeroed by a coalesced pass once every row has read it (a scattered
+  // b[perm[i]] = 0 in the kernel costs a partial-sector write per row)
+  if (zero_b && cudaMemsetAsync(b, 0, (size_t)n * sizeof(double), S(stream)) != cudaSuccess)
+    return fail("ab_cg_init_scaled: cannot zero b");
   return check_launch("ab_cg_init_scaled");
 }
 
@@ -764,9 +770,9 @@ int ab_cg_update_scaled(int64_t n, const double* p, const double* q, double* x, 
   return check_launch("ab_cg_update_scaled");
 }
 
-int ab_cg_finish_scaled(int64_t n, const int64_t* perm, const double* s, const double* x, double* out,
+int ab_cg_finish_scaled(int64_t n, const int64_t* iperm, const double* s, const double* x, double* out,
                         void* stream) {
-  if (n > 0) k_cg_finish_scaled<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, perm, s, x, out);
+  if (n > 0) k_cg_finish_scaled<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, iperm, s, x, out);
   return check_launch("ab_cg_finish_scaled");
 }
 
@@ -776,6 +782,8 @@ int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, c
   if (n <= 0 || !perm || !b) return fail("ab_cg_init_perm: empty system or null permutation");
   k_cg_init_perm<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, perm, b, zero_b, fixed, dinv, x, r, z, p, q, red, sc,
                                                          part, cnt);
+  if (zero_b && cudaMemsetAsync(b, 0, (size_t)n * sizeof(double), S(stream)) != cudaSuccess)
+    return fail("ab_cg_init_perm: cannot zero b");
   return check_launch("ab_cg_init_perm");
 }
 

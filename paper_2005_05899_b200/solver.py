@@ -317,6 +317,8 @@ class PCG:
             if scaled:
                 # CG on D^-1/2 P A P^T D^-1/2 (the permuted copy's values are scaled in place)
                 self.perm2["s"] = torch.sqrt(self.perm2["dinv"]).contiguous()
+                self.perm2["iperm"] = torch.empty_like(pl)
+                self.perm2["iperm"][pl] = torch.arange(n, device=dev)
                 self.perm2["d"] = (1.0 / self.perm2["dinv"]).contiguous()
                 call("ab_sell_symscale", ctypes.byref(self.perm2["A"].struct), ptr(self.perm2["s"]), stream_handle())
             # optional 16-bit columns in the slices whose columns span < 64k
@@ -418,7 +420,7 @@ class PCG:
                          ptr(self.r), ptr(self.z), None, ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
             it += 1
         if sc_:
-            call("ab_cg_finish_scaled", self.n, ptr(pm["perm"]), ptr(pm["s"]), ptr(self.x), ptr(pm["x"]), s)
+            call("ab_cg_finish_scaled", self.n, ptr(pm["iperm"]), ptr(pm["s"]), ptr(self.x), ptr(pm["x"]), s)
         else:
             call("ab_perm_scatter", self.n, ptr(pm["perm"]), ptr(self.x), ptr(pm["x"]), s)
         return pm["x"], it
