@@ -227,6 +227,11 @@ int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* ou
  * tolerance is tested) or r'.r'; finish: out[j] = s_i x'_i, i = iperm[j]
  * (the inverse permutation: coalesced writes). */
 int ab_sell_symscale(const ab_sell* a, const double* s, void* stream);
+/* The scaled SpMV with A' stored WITHOUT its diagonal (every diagonal entry
+ * of A' is 1): q = A' z + beta q as z + offdiag . z (ab_cg_spmv with_dot,
+ * own = NULL, otherwise). */
+int ab_cg_spmv_unit(const ab_sell* a, const double* z, double* p, double* q, double* red, double* sc, double* part,
+                    uint32_t* cnt, void* stream);
 int ab_cg_init_scaled(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
                       const double* s, const double* d, double* x, double* r, double* p, double* q, double* red,
                       double* sc, double* part, uint32_t* cnt, void* stream);

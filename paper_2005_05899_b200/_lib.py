@@ -132,6 +132,7 @@ _SIGS = {
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
     "ab_sell16_plan": ([P(AbSell), vp, vp, vp], C.c_int),
     "ab_sell_symscale": ([P(AbSell), vp, vp], C.c_int),
+    "ab_cg_spmv_unit": ([P(AbSell), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_init_scaled": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_update_scaled": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_finish_scaled": ([i64, vp, vp, vp, vp, vp], C.c_int),

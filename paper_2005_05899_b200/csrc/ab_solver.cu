@@ -279,6 +279,36 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_spmv(int64_t n, const int64_t* 
   }
 }
 
+// Single domain, symmetrically scaled matrix with its unit diagonal NOT
+// stored (ab_cg_spmv_unit): (A' z)_i = z_i + sum_{j != i} a'_ij z_j, the z_i
+// the recurrence reads anyway; 12 bytes per row less than storing the 1.
+__global__ void __launch_bounds__(kCgBlock) k_cg_spmv_unit(int64_t n, const int64_t* __restrict__ sp,
+                                                           const int32_t* __restrict__ scol,
+                                                           const double* __restrict__ sval,
+                                                           const double* __restrict__ z, double* __restrict__ p,
+                                                           double* __restrict__ q, double* red, double* sc,
+                                                           double* part, uint32_t* cnt) {
+  const int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x;
+  const double rz_old = sc[AB_SC_RZ];
+  const double rz_new = red[AB_RED_RZN];
+  const double beta = rz_old != 0.0 ? rz_new / rz_old : 0.0;
+  double v[1] = {0.0};
+  if (i < n) {
+    const double zi = z[i];
+    const double az = sell_row_dot(sp, scol, sval, z, i) + zi;
+    const double pi = fma(beta, p[i], zi);
+    const double qi = fma(beta, q[i], az);
+    p[i] = pi;
+    q[i] = qi;
+    v[0] = pi * qi;
+  }
+  double tot[1];
+  if (grid_sum<1, kCgBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_PQ] = tot[0];
+    sc[AB_SC_RZ] = rz_new;
+  }
+}
+
 // Single domain on the column-compressed SELL (ab_sell16): the DOT form of
 // k_cg_spmv with 2-byte columns in the slices that allow them.
 #ifndef SPMV16_MINB
@@ -810,6 +840,15 @@ int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* 
     k_cg_spmv<false><<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p, q,
                                                                         t, own, red, sc, part, cnt);
   return check_launch("ab_cg_spmv");
+}
+
+int ab_cg_spmv_unit(const ab_sell* a, const double* z, double* p, double* q, double* red, double* sc, double* part,
+                    uint32_t* cnt, void* stream) {
+  if (!a) return fail("ab_cg_spmv_unit: null matrix");
+  const int64_t n = a->n_rows;
+  k_cg_spmv_unit<<<grid_for(n, kCgBlock), kCgBlock, 0, S(stream)>>>(n, a->slice_ptr, a->cols, a->vals, z, p, q, red, sc,
+                                                                    part, cnt);
+  return check_launch("ab_cg_spmv_unit");
 }
 
 int ab_sell16_plan(const ab_sell* a, int32_t* cbase, int64_t* bytes, void* stream) {

@@ -102,9 +102,10 @@ def csr_to_sell(n: int, row_ptr, cols, vals) -> SellMatrix:
                       csr=(row_ptr, cols, vals))
 
 
-def permute_matrix(A: SellMatrix, perm: torch.Tensor) -> SellMatrix:
+def permute_matrix(A: SellMatrix, perm: torch.Tensor, drop_diag: bool = False) -> SellMatrix:
     """P A P^T as SELL-32: row i of the result is row perm[i] of A (columns
-    renumbered the same way, ascending within each row)."""
+    renumbered the same way, ascending within each row).  ``drop_diag``
+    leaves the diagonal entries out (the unit-diagonal scaled solver)."""
     row_ptr, cols, vals = A.csr
     n = A.n_rows
     dev = vals.device
@@ -112,6 +113,9 @@ def permute_matrix(A: SellMatrix, perm: torch.Tensor) -> SellMatrix:
     iperm = torch.empty_like(perm)
     iperm[perm] = torch.arange(n, device=dev)
     rows = torch.repeat_interleave(torch.arange(n, device=dev), row_ptr[1:] - row_ptr[:-1])
+    if drop_diag:
+        off = rows != cols.to(torch.int64)
+        rows, cols, vals = rows[off], cols[off], vals[off]
     key = iperm[rows] * n + iperm[cols.to(torch.int64)]
     key, order = torch.sort(key)
     new_rows = key // n
@@ -256,7 +260,8 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
-                 reorder_two_kernel: bool = True, compress_cols: bool = False, scaled: bool = True):
+                 reorder_two_kernel: bool = True, compress_cols: bool = False, scaled: bool = True,
+                 unit_diag: bool | None = None):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -311,9 +316,12 @@ class PCG:
         self.perm2 = None
         if not self.resident and halo is None and order is not None and reorder_two_kernel:
             pl = order.to(device=dev, dtype=torch.int64).contiguous()
-            self.perm2 = dict(A=permute_matrix(A, pl), perm=pl, dinv=dinv[pl].contiguous(),
+            # scaled form: every diagonal entry of D^-1/2 A D^-1/2 is 1, so it is not stored
+            unit = bool(scaled and not compress_cols) if unit_diag is None else bool(unit_diag and scaled)
+            self.perm2 = dict(A=permute_matrix(A, pl, drop_diag=unit), perm=pl,
+                              dinv=dinv[pl].contiguous(),
                               fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
-                              x=z(), scaled=bool(scaled))
+                              x=z(), scaled=bool(scaled), unit=unit)
             if scaled:
                 # CG on D^-1/2 P A P^T D^-1/2 (the permuted copy's values are scaled in place)
                 self.perm2["s"] = torch.sqrt(self.perm2["dinv"]).contiguous()
@@ -405,7 +413,10 @@ class PCG:
                 if bb == 0.0 or math.sqrt(rr / bb) <= tol:
                     break
             with self._m("K5_cg_spmv"):
-                if pm["A16"] is not None:
+                if pm["unit"]:
+                    call("ab_cg_spmv_unit", A, ptr(zvec), ptr(self.p), ptr(self.q), ptr(self.red), ptr(self.sc),
+                         ptr(self.part), ptr(self.cnt), s)
+                elif pm["A16"] is not None:
                     call("ab_cg_spmv16", ctypes.byref(pm["A16"]["struct"]), ptr(zvec), ptr(self.p), ptr(self.q),
                          ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
                 else:

@@ -146,6 +146,7 @@ CG_VARIANTS = {
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
     "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC order, 16-bit cols)
     "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False, compress_cols=False),  # z = D^-1 r form
+    "two-kernel-sfc-diag": dict(order=True, resident=False, unit_diag=False),  # scaled, diagonal stored
 }
 
 

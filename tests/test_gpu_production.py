@@ -250,7 +250,7 @@ def test_column_compressed_spmv_is_bitwise_equal(c2):
     xs = []
     for comp in (True, False):
         pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), order=dm.node_order(), resident=False,
-                  compress_cols=comp)  # (the option is off by default: measured slower)
+                  compress_cols=comp, unit_diag=False)  # (the option is off by default: measured slower)
         assert (pcg.perm2["A16"] is not None) == comp
         x, _ = pcg.solve(torch.from_numpy(b).cuda(), 12, zero_b=False)
         xs.append(x.clone())
