@@ -169,7 +169,7 @@ class ClockSampler:
 
 
 def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters: int = CG_ITERS,
-                     n_faces: int = 0):
+                     n_faces: int = 0, unit_diag: bool = False):
     """Algorithmic bytes (and flops for K2) per launch, layout-independent
     (SURVEY §8(d) per-unit figures): int32 indices, fp64 values."""
     from paper_2005_05899_b200.meshgen import NODE_COUNT, RULE_KIND
@@ -178,6 +178,8 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
     if kernel in ("K5_cg_resident", "K5_cg_fused_dd"):  # SURVEY §8(d) K5 per iteration: 12Z + 4(N+1) + 104N
         return cg_iters * (12 * nnz + 4 * (N + 1) + 104 * N), cg_iters * (2 * nnz + 12 * N)
     if kernel == "K5_cg_spmv":      # vals+cols, z gathered once, p & q read + written
+        if unit_diag:  # scaled form: the unit diagonal of D^-1/2 A D^-1/2 is implicit (never read)
+            return 12 * (nnz - N) + 8 * N + 32 * N, 2 * nnz + 4 * N
         return 12 * nnz + 8 * N + 32 * N, 2 * nnz + 4 * N
     if kernel == "K5_cg_dot":       # z t p q in, p q out
         return 48 * N, 6 * N
@@ -446,7 +448,8 @@ def run_native(args):
     kern = {}
     for kname, ts in per.items():
         B, F = algorithmic_cost(kname, counts, solver.n, nnz, args.cg_iters,
-                                n_faces=solver.wall.n_faces if solver.wall is not None else 0)
+                                n_faces=solver.wall.n_faces if solver.wall is not None else 0,
+                                unit_diag=bool(getattr(solver.pcg, "perm2", None) and solver.pcg.perm2["unit"]))
         avg = float(np.mean(ts))
         kern[kname] = {"launches": len(ts), "avg_us": avg * 1e6, "total_ms": float(np.sum(ts)) * 1e3,
                       "alg_bytes": B, "gbs": B / avg / 1e9 if avg > 0 else None,

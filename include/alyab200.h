@@ -117,6 +117,22 @@ int ab_set_windows(const int32_t* conn, int32_t block, const int64_t* blk_ptr, c
  * references t*nnode .. t*nnode+nnode-1 (one fp64 reduction per window node
  * it touches). */
 int ab_set_window_refs(const int32_t* conn, const uint32_t* wref);
+/* Colour mode of the pipelined kernels (the north star's "mesh colouring"
+ * scatter, chosen against fp64 atomics by measurement): the
+ * category's blocks are processed colour by colour (corder: block ids grouped
+ * by colour, cptr [ncol+1] offsets), no two blocks of a colour share a window
+ * node, and every node sum is formed in a fixed order, so K2/K4/K6 results
+ * are bitwise reproducible run to run (the reference's scatter_global sums in
+ * a fixed order, assembly.py:317-326).  gbar: one device uint32 (barrier
+ * word).  ncol 0 / NULL corder restores the fp64-atomic scatter. */
+int ab_set_window_colours(const int32_t* conn, int32_t ncol, const int32_t* corder, const int64_t* cptr,
+                          uint32_t* gbar);
+/* Jones-Plassmann colouring of the window blocks (setup): blocks b, b' are
+ * neighbours when they share a window node; nptr/nblk: node -> blocks CSR
+ * (N+1 / n_window_entries); flags: 2 device int32 scratch.  Synchronises the
+ * stream once per round; colour[b] in [0, 64). */
+int ab_colour_blocks(int64_t n_blocks, const int64_t* blk_ptr, const int32_t* wnode, const int64_t* nptr,
+                     const int32_t* nblk, int32_t* colour, int32_t* flags, void* stream);
 
 /* ---- Partition file I/O (host; reference sfc.py:385-417 `part 1` body) ----
  * ab_format_partition: lines "i parts[i]\n" for i = first .. first+n-1 into
@@ -154,6 +170,16 @@ typedef struct ab_wall {
   int64_t n_faces;
   const int32_t* face;  /* [n_faces][4] */
   const int32_t* off;   /* [n_faces][4] */
+  /* optional fixed-order accumulation (all NULL/0: fp64 reductions per face
+   * node): the face tractions go to ftrac [n_faces][3], then each of the
+   * n_nodes wall nodes node[i] adds the tractions of its faces
+   * fref[ptr[i] .. ptr[i+1]) (ascending face ids) in that order, so K8's
+   * result is bitwise reproducible. */
+  int64_t n_nodes;
+  const int32_t* node;  /* [n_nodes] wall node ids */
+  const int64_t* ptr;   /* [n_nodes + 1] */
+  const int32_t* fref;  /* faces of each wall node, ascending */
+  double* ftrac;        /* [n_faces][3] scratch */
 } ab_wall;
 int ab_wall_traction(const ab_wall* w, const ab_phys* phys, const double* coords4, const double* u4, double* rhs4,
                      void* stream);

@@ -49,7 +49,8 @@ class AbSell3(C.Structure):
 
 
 class AbWall(C.Structure):
-    _fields_ = [("n_faces", i64), ("face", vp), ("off", vp)]
+    _fields_ = [("n_faces", i64), ("face", vp), ("off", vp), ("n_nodes", i64), ("node", vp), ("ptr", vp),
+                ("fref", vp), ("ftrac", vp)]
 
 
 class AbCgLocal(C.Structure):
@@ -114,6 +115,8 @@ _SIGS = {
     "ab_launch_count": ([], i64),
     "ab_set_windows": ([vp, i32, vp, vp, vp, vp, vp, vp, i32], C.c_int),
     "ab_set_window_refs": ([vp, vp], C.c_int),
+    "ab_set_window_colours": ([vp, i32, vp, vp, vp], C.c_int),
+    "ab_colour_blocks": ([i64, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_format_partition": ([vp, i64, i64, vp, i64], C.c_int64),
     "ab_filter_width": ([P(AbMesh), i32, vp, vp], C.c_int),
     "ab_set_filter_width": ([vp, i64, vp], C.c_int),

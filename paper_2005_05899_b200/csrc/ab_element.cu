@@ -47,6 +47,15 @@ struct WinP {
   const uint32_t* __restrict__ wref;
   int block;                             // elements per block (== blockDim.x)
   int wmax;                              // largest window (nodes) of any block
+  // Colour mode (ab_set_window_colours; NULL corder = fp64-atomic scatter):
+  // blocks grouped by colour, no two blocks of a colour share a window node,
+  // colours processed in order behind a grid barrier, and every window
+  // node's sum formed by one thread in a fixed order -> plain read-add-write,
+  // bitwise reproducible results.
+  const int32_t* __restrict__ corder;    // [n_blocks] logical -> physical block, grouped by colour
+  const int64_t* __restrict__ cptr;      // [ncol+1] colour offsets into corder
+  unsigned* gbar;                        // grid-barrier counter (zeroed before every launch)
+  int ncol;
 };
 
 template <int NN>
@@ -854,6 +863,61 @@ template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 
 template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
 template <> struct PipeOcc<AB_RULE_TET4, OP_MOMENTUM> { static constexpr int value = PIPE_OCC_K2; };
 
+// Work sequence of a persistent CTA.  Atomic mode: blocks blockIdx.x,
+// +gridDim.x, ... in SFC order.  Colour mode: the same walk inside each
+// colour's slice of corder, colour after colour.  j = logical position
+// (-1 = end), c = colour of that position (ncol at the end).
+struct Pos {
+  int64_t j;
+  int c;
+};
+template <bool COL>
+__device__ __forceinline__ Pos pos_first(const WinP& w, int64_t n_blocks) {
+  Pos p{-1, 0};
+  if constexpr (COL) {
+    for (; p.c < w.ncol; ++p.c) {
+      const int64_t j = __ldg(w.cptr + p.c) + blockIdx.x;
+      if (j < __ldg(w.cptr + p.c + 1)) {
+        p.j = j;
+        return p;
+      }
+    }
+  } else {
+    if ((int64_t)blockIdx.x < n_blocks) p.j = blockIdx.x;
+  }
+  return p;
+}
+template <bool COL>
+__device__ __forceinline__ Pos pos_next(const WinP& w, int64_t n_blocks, Pos p) {
+  if (p.j < 0) return p;
+  p.j += gridDim.x;
+  if constexpr (COL) {
+    while (p.j >= __ldg(w.cptr + p.c + 1)) {
+      if (++p.c >= w.ncol) {
+        p.j = -1;
+        return p;
+      }
+      p.j = __ldg(w.cptr + p.c) + blockIdx.x;
+    }
+  } else {
+    if (p.j >= n_blocks) p.j = -1;
+  }
+  return p;
+}
+template <bool COL>
+__device__ __forceinline__ int64_t pos_block(const WinP& w, Pos p) {
+  if constexpr (COL) return p.j >= 0 ? (int64_t)__ldg(w.corder + p.j) : -1;
+  return p.j;
+}
+
+// Colour-mode scratch behind the slot buffer: each thread's first window
+// index (bit 31: the thread holds a single run), last window index and first
+// run's partial sum.
+template <int NC, int BLOCK>
+struct ColSmem {
+  static __host__ __device__ size_t bytes() { return (size_t)BLOCK * (8 + 8 * NC); }
+};
+
 // Persistent pipelined element kernel.  Iteration i (element block b_i):
 //   A  wait metadata(b_{i+1}) [mbarrier], cp.async node data(b_{i+1})
 //   B  wait node data(b_i) [cp.async group], __syncthreads; thread 0 then
@@ -863,7 +927,18 @@ template <> struct PipeOcc<AB_RULE_TET4, OP_MOMENTUM> { static constexpr int val
 //   D  window-node reductions of b_i -> global fp64 REDs
 // Three metadata stages and two node stages make every buffer reuse safe
 // with two CTA barriers per block.
-template <int R, int OP, int BLOCK>
+// COL (mesh colouring, deterministic): before phase D of a block of colour c
+// the CTA has announced every colour < c as finished (release-add on
+// w.gbar) and waits until all CTAs have (counter >= c * gridDim.x); phase D
+// then forms each window node's total in one thread (the references in
+// sorted order, runs crossing lanes summed by the lane where they start) and
+// issues ONE fp64 reduction per node: no two blocks of a colour share a
+// node and the colours are ordered by the barrier (release/acquire, so the
+// reductions of colour c happen before those of c+1 in every node's
+// coherence order), hence every node's sum has a fixed order and the result
+// is bitwise reproducible without paying for a read-add-write round trip.
+// The prefetch pipeline runs across colour boundaries (it only reads).
+template <int R, int OP, int BLOCK, bool COL>
 __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, WinP w, ab_phys ph, double scale,
                                                                        const double* __restrict__ f,
                                                                        double* __restrict__ out, int64_t n_blocks) {
@@ -875,9 +950,14 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
   const int wmax = w.wmax;
   double* nodes0 = reinterpret_cast<double*>(smem + 3 * L::meta_bytes(wmax));
   double* slots = reinterpret_cast<double*>(smem + 3 * L::meta_bytes(wmax) + 2 * L::node_bytes(wmax));
-  const int64_t stride = gridDim.x;
-  const int64_t b_first = blockIdx.x;
-  if (b_first >= n_blocks) return;
+  Pos p0 = pos_first<COL>(w, n_blocks);
+  int done = 0;  // COL: colours this CTA has announced as finished
+  if (p0.j < 0) {
+    if constexpr (COL) {
+      if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(w.ncol) : "memory");
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     mbar_init1(&bars[0]);
     mbar_init1(&bars[1]);
@@ -885,33 +965,49 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  // block descriptors (16 B each) of the current and the next two blocks
-  int4 d0 = __ldg(w.desc + b_first);
-  int4 d1 = b_first + stride < n_blocks ? __ldg(w.desc + b_first + stride) : d0;
-  int4 d2 = b_first + 2 * stride < n_blocks ? __ldg(w.desc + b_first + 2 * stride) : d0;
-  if (threadIdx.x == 0) {
-    issue_meta<NN>(w, c.n, b_first, d0, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), &bars[0]);
-    if (b_first + stride < n_blocks)
-      issue_meta<NN>(w, c.n, b_first + stride, d1, meta_ptr<NN, NV, BLOCK>(smem, wmax, 1), &bars[1]);
+  // positions, physical blocks and descriptors (16 B each) of the current
+  // and the next two blocks
+  // (atomic mode derives the next blocks from b0 where they are used, so
+  // only colour mode carries them across iterations)
+  const int64_t stride = gridDim.x;
+  auto nxt = [&](int64_t b) -> int64_t { return (b >= 0 && b + stride < n_blocks) ? b + stride : (int64_t)-1; };
+  Pos p1 = pos_next<COL>(w, n_blocks, p0);
+  Pos p2 = pos_next<COL>(w, n_blocks, p1);
+  int64_t b0 = pos_block<COL>(w, p0);
+  int64_t cb1 = COL ? pos_block<COL>(w, p1) : -1, cb2 = COL ? pos_block<COL>(w, p2) : -1;
+  int4 d0, d1, d2;
+  {
+    const int64_t b1 = COL ? cb1 : nxt(b0), b2 = COL ? cb2 : nxt(b1);
+    d0 = __ldg(w.desc + b0);
+    d1 = b1 >= 0 ? __ldg(w.desc + b1) : d0;
+    d2 = b2 >= 0 ? __ldg(w.desc + b2) : d0;
+    if (threadIdx.x == 0) {
+      issue_meta<NN>(w, c.n, b0, d0, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), &bars[0]);
+      if (b1 >= 0) issue_meta<NN>(w, c.n, b1, d1, meta_ptr<NN, NV, BLOCK>(smem, wmax, 1), &bars[1]);
+    }
   }
   mbar_wait_parity(&bars[0], 0);
   issue_nodes<NV, BLOCK>(c, f, wmax, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), block_view(w, d0), nodes0);
 
   int it = 0;
-  for (int64_t b = b_first; b < n_blocks; b += stride, ++it) {
+  for (; b0 >= 0; ++it) {
     const int mq = it % 3, mq1 = (it + 1) % 3, mq2 = (it + 2) % 3;
     double* nodes_cur = nodes0 + (size_t)(it & 1) * NV * wmax;
     double* nodes_nxt = nodes0 + (size_t)((it + 1) & 1) * NV * wmax;
-    const int64_t b2 = b + 2 * stride, b3 = b + 3 * stride;
-    const int4 d3 = b3 < n_blocks ? __ldg(w.desc + b3) : d0;  // lands during this block
+    const int64_t b1 = COL ? cb1 : nxt(b0);
+    const int64_t b2 = COL ? cb2 : nxt(b1);
+    Pos p3{-1, 0};
+    if constexpr (COL) p3 = pos_next<COL>(w, n_blocks, p2);
+    const int64_t b3 = COL ? pos_block<COL>(w, p3) : nxt(b2);
+    const int4 d3 = b3 >= 0 ? __ldg(w.desc + b3) : d0;  // lands during this block
     // precomputed filter width of this thread's element: in flight across the waits below
     double d2e = -1.0;
     if constexpr (OP == OP_MOMENTUM) {
-      const int64_t ee = b * BLOCK + threadIdx.x;
+      const int64_t ee = b0 * BLOCK + threadIdx.x;
       if (c.delta2 && ee < c.n) d2e = __ldg(c.delta2 + ee);
     }
     // A: node data of the next block
-    if (b + stride < n_blocks) {
+    if (b1 >= 0) {
       mbar_wait_parity(&bars[mq1], (uint32_t)(((it + 1) / 3) & 1));
       issue_nodes<NV, BLOCK>(c, f, wmax, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq1), block_view(w, d1), nodes_nxt);
       cp_async_wait<1>();
@@ -919,14 +1015,25 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       cp_async_wait<0>();
     }
     __syncthreads();  // B
-    if (threadIdx.x == 0 && b2 < n_blocks) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_meta<NN>(w, c.n, b2, d2, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq2), &bars[mq2]);
+    bool col_wait = false;
+    if (threadIdx.x == 0) {
+      if (b2 >= 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue_meta<NN>(w, c.n, b2, d2, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq2), &bars[mq2]);
+      }
+      if constexpr (COL) {
+        // every thread's phase D of the previous block is behind barrier B
+        if (p0.c > done) {
+          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(p0.c - done) : "memory");
+          done = p0.c;
+          col_wait = true;
+        }
+      }
     }
     // C: elements of this block
     const MetaPtr mc = meta_ptr<NN, NV, BLOCK>(smem, wmax, mq);
     const BlockView vc = block_view(w, d0);
-    const int64_t e = b * BLOCK + threadIdx.x;
+    const int64_t e = b0 * BLOCK + threadIdx.x;
     if (e < c.n) {
       double x[NN][3], fv[NN][NV == 6 ? 3 : 1];
       int li[NN];
@@ -976,6 +1083,15 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       for (int a = 0; a < NN; ++a)
 #pragma unroll
         for (int k = 0; k < NC; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = 0.0;
+    }
+    if constexpr (COL) {
+      if (col_wait) {
+        const unsigned target = (unsigned)p0.c * gridDim.x;
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w.gbar) : "memory");
+        } while (v < target);
+      }
     }
     __syncthreads();
     // D: thread t sums the block's sorted references t*NN .. t*NN+NN-1 (the
@@ -1035,27 +1151,66 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
         }
       }
       const uint32_t f = rr[0] >> 16, l = cur;
-      const int lane = threadIdx.x & 31;
-      const uint32_t mine = f | (np >= 2 ? 0x80000000u : 0u);
-      const uint32_t nxt = __shfl_down_sync(0xffffffffu, mine, 1);
-      const uint32_t prv = __shfl_up_sync(0xffffffffu, l, 1);
-      double hn[NC];
+      if constexpr (COL) {
+        // runs crossing lanes: summed in lane order by the lane holding
+        // their start (its last piece), from the heads published here
+        uint32_t* s_first = reinterpret_cast<uint32_t*>(slots + 3 * NN * BLOCK);
+        uint32_t* s_last = s_first + BLOCK;
+        double* s_head = reinterpret_cast<double*>(s_last + BLOCK);
+        const int t = threadIdx.x;
+        s_first[t] = f | (np == 1 ? 0x80000000u : 0u);
+        s_last[t] = l;
 #pragma unroll
-      for (int q = 0; q < NC; ++q) hn[q] = __shfl_down_sync(0xffffffffu, H[q], 1);
-      const bool recv = lane != 31 && (nxt >> 31) && (nxt & 0xffffu) == l && l != 0xffffu;
-      const bool give = lane != 0 && np >= 2 && prv == f && f != 0xffffu;
-      if (np >= 2 && !give && f != 0xffffu) red_node(f, H);
-      if (l != 0xffffu) {
-        if (recv) {
+        for (int q = 0; q < NC; ++q) s_head[q * BLOCK + t] = np == 1 ? acc[q] : H[q];
+        __syncthreads();
+        const bool cont_prev = t > 0 && s_last[t - 1] == f;
+        if (np >= 2 && !cont_prev && f != 0xffffu) red_node(f, H);
+        if (l != 0xffffu && (np >= 2 || !cont_prev)) {
+          for (int u = t + 1; u < BLOCK; ++u) {
+            const uint32_t fu = s_first[u];
+            if ((fu & 0xffffu) != l) break;
 #pragma unroll
-          for (int q = 0; q < NC; ++q) acc[q] += hn[q];
+            for (int q = 0; q < NC; ++q) acc[q] += s_head[q * BLOCK + u];
+            if (!(fu >> 31)) break;
+          }
+          red_node(l, acc);
         }
-        red_node(l, acc);
+      } else {
+        const int lane = threadIdx.x & 31;
+        const uint32_t mine = f | (np >= 2 ? 0x80000000u : 0u);
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, mine, 1);
+        const uint32_t prv = __shfl_up_sync(0xffffffffu, l, 1);
+        double hn[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) hn[q] = __shfl_down_sync(0xffffffffu, H[q], 1);
+        const bool recv = lane != 31 && (nxt >> 31) && (nxt & 0xffffu) == l && l != 0xffffu;
+        const bool give = lane != 0 && np >= 2 && prv == f && f != 0xffffu;
+        if (np >= 2 && !give && f != 0xffffu) red_node(f, H);
+        if (l != 0xffffu) {
+          if (recv) {
+#pragma unroll
+            for (int q = 0; q < NC; ++q) acc[q] += hn[q];
+          }
+          red_node(l, acc);
+        }
       }
     }
+    if constexpr (COL) {
+      p0 = p1;
+      p1 = p2;
+      p2 = p3;
+      cb1 = b2;
+      cb2 = b3;
+    }
+    b0 = b1;
     d0 = d1;
     d1 = d2;
     d2 = d3;
+  }
+  if constexpr (COL) {
+    __syncthreads();  // this CTA's last phase D is issued
+    if (threadIdx.x == 0 && w.ncol > done)
+      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(w.ncol - done) : "memory");
   }
 }
 
@@ -1063,15 +1218,15 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
 // tests check that the persistent CTAs walk several blocks each).
 static thread_local int64_t g_pipe_grid = 0, g_pipe_blocks = 0;
 
-template <int R, int OP, int BLOCK>
-static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double scale, const double* f, double* out,
-                       cudaStream_t stream) {
+template <int R, int OP, int BLOCK, bool COL>
+static int launch_pipe_impl(const CatP& c, const WinP& w, const ab_phys& ph, double scale, const double* f,
+                            double* out, cudaStream_t stream) {
   constexpr int NN = RuleT<R>::NN;
   constexpr int NV = OpT<R, OP>::NV;
   using L = PipeSmem<NN, NV, BLOCK>;
   if (!w.wref) return fail("pipelined element kernel: sorted window references not registered (ab_set_window_refs)");
-  const size_t smem = L::total(w.wmax);
-  auto kern = k_pipe<R, OP, BLOCK>;
+  const size_t smem = L::total(w.wmax) + (COL ? ColSmem<3, BLOCK>::bytes() : 0);
+  auto kern = k_pipe<R, OP, BLOCK, COL>;
   if (smem > 48 * 1024 &&
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return fail("pipelined element kernel: shared memory request rejected");
@@ -1089,8 +1244,21 @@ static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double s
   if (grid > n_blocks) grid = n_blocks;
   g_pipe_grid = grid;
   g_pipe_blocks = n_blocks;
+  if (COL) {
+    // every CTA must be resident at once (colour barrier): grid <= sms * per_sm
+    if (!w.gbar || !w.cptr || w.ncol < 1) return fail("k_pipe colour mode: colours not registered");
+    if (cudaMemsetAsync(w.gbar, 0, sizeof(unsigned), stream) != cudaSuccess)
+      return fail("k_pipe colour mode: barrier reset failed");
+  }
   kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w, ph, scale, f, out, n_blocks);
   return check_launch("k_pipe");
+}
+
+template <int R, int OP, int BLOCK>
+static int launch_pipe(const CatP& c, const WinP& w, const ab_phys& ph, double scale, const double* f, double* out,
+                       cudaStream_t stream) {
+  if (w.corder) return launch_pipe_impl<R, OP, BLOCK, true>(c, w, ph, scale, f, out, stream);
+  return launch_pipe_impl<R, OP, BLOCK, false>(c, w, ph, scale, f, out, stream);
 }
 // ---------------------------------------------------------------------------
 // Vreman filter width Delta^2 = V_e^(2/3) per element (setup): the same
@@ -1298,6 +1466,52 @@ static int dispatch_rule(int rule, F&& f) {
   return fail("unknown rule");
 }
 
+// ---------------------------------------------------------------------------
+// Block colouring for the deterministic scatter (setup): Jones-Plassmann
+// rounds with hashed priorities.  An uncoloured block whose uncoloured
+// neighbours (blocks sharing a window node) all have lower priority takes the
+// smallest colour none of its coloured neighbours has.  Two blocks coloured
+// in the same round are never neighbours, so the result is a proper
+// colouring, and it does not depend on thread scheduling.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t colour_prio(uint32_t b) {
+  b ^= b >> 16; b *= 0x7feb352du; b ^= b >> 15; b *= 0x846ca68bu; b ^= b >> 16;
+  return b;
+}
+__global__ void k_colour_round(int64_t nb, const int64_t* __restrict__ blk_ptr, const int32_t* __restrict__ wnode,
+                               const int64_t* __restrict__ nptr, const int32_t* __restrict__ nblk, int32_t* colour,
+                               int32_t* flags) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= nb) return;
+  volatile int32_t* col = colour;
+  if (col[b] >= 0) return;
+  const uint32_t pb = colour_prio((uint32_t)b);
+  uint64_t mask = 0;
+  for (int64_t k = blk_ptr[b]; k < blk_ptr[b + 1]; ++k) {
+    const int n = wnode[k];
+    for (int64_t m = nptr[n]; m < nptr[n + 1]; ++m) {
+      const int32_t b2 = nblk[m];
+      if (b2 == b) continue;
+      const int32_t c2 = col[b2];
+      if (c2 < 0) {
+        const uint32_t p2 = colour_prio((uint32_t)b2);
+        if (p2 > pb || (p2 == pb && b2 > b)) {
+          flags[0] = 1;  // still work to do
+          return;
+        }
+      } else {
+        mask |= 1ull << c2;
+      }
+    }
+  }
+  const int c = __ffsll((long long)~mask) - 1;
+  if (c < 0) {
+    flags[1] = 1;  // more than 64 colours needed
+    return;
+  }
+  col[b] = c;
+}
+
 static constexpr int kBlock = 128;
 
 // Opt a kernel into > 48 KB of dynamic shared memory when a window needs it.
@@ -1356,6 +1570,54 @@ int ab_set_window_refs(const int32_t* conn, const uint32_t* wref) {
       return AB_OK;
     }
   return fail("ab_set_window_refs: no windows registered for this connectivity");
+}
+
+// Colour mode of a category's pipelined kernels (NULL corder / ncol 0:
+// back to fp64 atomics).  corder: blocks grouped by colour; cptr: [ncol+1];
+// gbar: one device uint32 for the colour barrier.
+int ab_set_window_colours(const int32_t* conn, int32_t ncol, const int32_t* corder, const int64_t* cptr,
+                          uint32_t* gbar) {
+  for (int i = 0; i < g_nwin; ++i)
+    if (g_win[i].conn == conn) {
+      if (!corder || ncol < 1) {
+        g_win[i].w.corder = nullptr;
+        g_win[i].w.cptr = nullptr;
+        g_win[i].w.gbar = nullptr;
+        g_win[i].w.ncol = 0;
+        return AB_OK;
+      }
+      if (!cptr || !gbar) return fail("ab_set_window_colours: null cptr or barrier word");
+      if (!g_win[i].w.desc) return fail("ab_set_window_colours: colour mode needs the pipelined windows (desc)");
+      g_win[i].w.corder = corder;
+      g_win[i].w.cptr = cptr;
+      g_win[i].w.gbar = reinterpret_cast<unsigned*>(gbar);
+      g_win[i].w.ncol = ncol;
+      return AB_OK;
+    }
+  return fail("ab_set_window_colours: no windows registered for this connectivity");
+}
+
+// Jones-Plassmann colouring of n_blocks window blocks (device arrays;
+// synchronises the stream once per round): colour[b] in [0, 64).
+int ab_colour_blocks(int64_t n_blocks, const int64_t* blk_ptr, const int32_t* wnode, const int64_t* nptr,
+                     const int32_t* nblk, int32_t* colour, int32_t* flags, void* stream) {
+  if (n_blocks < 0 || !blk_ptr || !wnode || !nptr || !nblk || !colour || !flags)
+    return fail("ab_colour_blocks: null argument");
+  if (n_blocks == 0) return 0;
+  cudaStream_t st = S(stream);
+  if (cudaMemsetAsync(colour, 0xff, sizeof(int32_t) * n_blocks, st) != cudaSuccess)
+    return fail("ab_colour_blocks: memset failed");
+  for (int round = 0; round < 100000; ++round) {
+    int32_t h[2] = {0, 0};
+    cudaMemsetAsync(flags, 0, sizeof(int32_t) * 2, st);
+    k_colour_round<<<grid_for(n_blocks, 256), 256, 0, st>>>(n_blocks, blk_ptr, wnode, nptr, nblk, colour, flags);
+    if (int rc = check_launch("ab_colour_blocks")) return rc;
+    cudaMemcpyAsync(h, flags, sizeof(h), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return fail("ab_colour_blocks: round failed");
+    if (h[1]) return fail("ab_colour_blocks: more than 64 colours needed");
+    if (!h[0]) break;
+  }
+  return AB_OK;
 }
 
 int ab_filter_width(const ab_mesh* m, int32_t k, double* delta2, void* stream) {

@@ -638,7 +638,7 @@ int ab_mesh_upload(ab_ctx* c, const ab_mesh_desc* d) {
     AB_ALLOC(o, int32_t, 4 * d->n_wall_faces);
     cudaMemcpyAsync(f, d->wall_face, 16 * d->n_wall_faces, cudaMemcpyDefault, c->st);
     cudaMemcpyAsync(o, d->wall_off, 16 * d->n_wall_faces, cudaMemcpyDefault, c->st);
-    c->wall = ab_wall{d->n_wall_faces, f, o};
+    c->wall = ab_wall{d->n_wall_faces, f, o, 0, nullptr, nullptr, nullptr, nullptr};
   }
   if (cudaStreamSynchronize(c->st) != cudaSuccess) return check_launch("ab_mesh_upload");
   c->ready = true;

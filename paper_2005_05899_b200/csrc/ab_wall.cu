@@ -5,7 +5,9 @@
 //   n = outward unit normal of the (planar) face, y = |(x_e - x_c) . n|,
 //   u_t = u_e - (u_e . n) n, u_tau from Reichardt's law (fixed Newton count),
 //   every face node receives -rho u_tau^2 u_t/|u_t| * A / n_face_nodes
-// accumulated into rhs4 (fp64 reductions: wall nodes are shared by faces).
+// accumulated into rhs4 (fp64 reductions: wall nodes are shared by faces),
+// or, in the fixed-order form, stored per face and summed per wall node in
+// ascending face order by k_wall_gather (bitwise reproducible).
 #include "ab_common.cuh"
 
 namespace ab {
@@ -27,7 +29,7 @@ __device__ __forceinline__ void cross3(const double* a, const double* b, double*
 
 __global__ void k_wall(int64_t nfaces, const int32_t* __restrict__ face, const int32_t* __restrict__ off,
                        const double* __restrict__ coords4, const double* __restrict__ u4, double rho, double mu,
-                       double* __restrict__ rhs4) {
+                       double* __restrict__ rhs4, double* __restrict__ ftrac) {
   const int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= nfaces) return;
   int fn[4], on[4];
@@ -88,7 +90,10 @@ __global__ void k_wall(int64_t nfaces, const int32_t* __restrict__ face, const i
   const double un = ue[0] * nv[0] + ue[1] * nv[1] + ue[2] * nv[2];
   const double ut[3] = {ue[0] - un * nv[0], ue[1] - un * nv[1], ue[2] - un * nv[2]};
   const double utm = sqrt(ut[0] * ut[0] + ut[1] * ut[1] + ut[2] * ut[2]);
-  if (!(utm > 0.0)) return;
+  if (!(utm > 0.0)) {
+    if (ftrac) ftrac[3 * f] = ftrac[3 * f + 1] = ftrac[3 * f + 2] = 0.0;
+    return;
+  }
   const double nu = mu / rho;
   double utau = sqrt(nu * utm / y);
   for (int it = 0; it < kReichardtIters; ++it) {
@@ -100,6 +105,12 @@ __global__ void k_wall(int64_t nfaces, const int32_t* __restrict__ face, const i
     utau = fmax(utau - fv / df, 0.0);
   }
   const double coef = -rho * utau * utau / utm * area / nf;
+  if (ftrac) {
+    ftrac[3 * f] = coef * ut[0];
+    ftrac[3 * f + 1] = coef * ut[1];
+    ftrac[3 * f + 2] = coef * ut[2];
+    return;
+  }
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (k < nf) {
@@ -109,6 +120,26 @@ __global__ void k_wall(int64_t nfaces, const int32_t* __restrict__ face, const i
       red_add(r + 2, coef * ut[2]);
     }
   }
+}
+
+// Fixed-order accumulation: wall node i adds its faces' tractions in
+// ascending face order (one thread per node, plain read-add-write).
+__global__ void k_wall_gather(int64_t n, const int32_t* __restrict__ node, const int64_t* __restrict__ ptr,
+                              const int32_t* __restrict__ fref, const double* __restrict__ ftrac,
+                              double* __restrict__ rhs4) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  for (int64_t k = ptr[i]; k < ptr[i + 1]; ++k) {
+    const int64_t f = fref[k];
+    s0 += ftrac[3 * f];
+    s1 += ftrac[3 * f + 1];
+    s2 += ftrac[3 * f + 2];
+  }
+  double* r = rhs4 + 4 * (int64_t)node[i];
+  r[0] += s0;
+  r[1] += s1;
+  r[2] += s2;
 }
 
 }  // namespace ab
@@ -122,9 +153,16 @@ int ab_wall_traction(const ab_wall* w, const ab_phys* phys, const double* coords
   if (!w || !phys || !coords4 || !u4 || !rhs4) return fail("ab_wall_traction: null argument");
   if (w->n_faces <= 0) return AB_OK;
   if (!w->face || !w->off) return fail("ab_wall_traction: null face lists");
+  const bool ordered = w->node != nullptr;
+  if (ordered && (!w->ptr || !w->fref || !w->ftrac || w->n_nodes <= 0))
+    return fail("ab_wall_traction: incomplete fixed-order node lists");
   k_wall<<<grid_for(w->n_faces, 128), 128, 0, S(stream)>>>(w->n_faces, w->face, w->off, coords4, u4, phys->rho,
-                                                          phys->mu, rhs4);
-  return check_launch("ab_wall_traction");
+                                                          phys->mu, rhs4, ordered ? w->ftrac : nullptr);
+  if (int rc = check_launch("ab_wall_traction")) return rc;
+  if (!ordered) return AB_OK;
+  k_wall_gather<<<grid_for(w->n_nodes, 128), 128, 0, S(stream)>>>(w->n_nodes, w->node, w->ptr, w->fref, w->ftrac,
+                                                                 rhs4);
+  return check_launch("ab_wall_traction(gather)");
 }
 
 }  // extern "C"

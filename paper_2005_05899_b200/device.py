@@ -26,7 +26,7 @@ WINDOW_BLOCK = 128
 
 class DeviceMesh:
     def __init__(self, mesh: MeshArrays, device="cuda", reorder: str | None = None, windows: bool = False,
-                 pipelined: bool = True):
+                 pipelined: bool = True, scatter: str = "atomic"):
         if not torch.cuda.is_available():
             raise RuntimeError("DeviceMesh needs a CUDA device (there is no CPU fallback)")
         self.device = torch.device(device)
@@ -42,7 +42,13 @@ class DeviceMesh:
             self.conn.append(torch.from_numpy(np.ascontiguousarray(conn, dtype=np.int32)).to(self.device))
             self.ids.append(torch.from_numpy(np.asarray(ids, dtype=np.int64)).to(self.device))
         self._win = []
+        self._col = []
         self.pipelined = pipelined
+        if scatter not in ("atomic", "colour"):
+            raise ValueError(f"scatter must be 'atomic' or 'colour', not {scatter!r}")
+        if scatter == "colour" and not (windows and pipelined):
+            raise ValueError("scatter='colour' needs the pipelined node windows (windows=True, pipelined=True)")
+        self.scatter = scatter
         self._build_struct()
         if reorder == "sfc":
             self.reorder_sfc()
@@ -206,6 +212,61 @@ class DeviceMesh:
                  ptr(loc), ptr(desc) if self.pipelined else None, wmax)
             call("ab_set_window_refs", ptr(conn), ptr(wref))
         self.windows = True
+        if self.scatter == "colour":
+            self.build_colours()
+
+    def build_colours(self):
+        """Colour the window blocks of every category (two blocks conflict
+        when they share a window node; Jones-Plassmann on the GPU,
+        ``ab_colour_blocks``) and register the colour mode: the pipelined
+        kernels then process the blocks colour by colour and update each node
+        with one plain read-add-write in a fixed order (bitwise reproducible
+        K2/K4/K6, the north star's "mesh colouring" scatter)."""
+        self.clear_colours()
+        dev = self.device
+        N = self.n_nodes
+        for conn, w in zip(self.conn, self._win):
+            if w is None:
+                self._col.append(None)
+                continue
+            blk_ptr, wnode = w[0], w[1]
+            nb = blk_ptr.numel() - 1
+            nw = int(blk_ptr[-1].item())
+            counts = blk_ptr[1:] - blk_ptr[:-1]
+            wblk = torch.repeat_interleave(torch.arange(nb, device=dev, dtype=torch.int32), counts)
+            wn = wnode[:nw].to(torch.int64)
+            order = torch.sort(wn, stable=True).indices
+            nblk = wblk[order].contiguous()
+            del wblk, order
+            nptr = torch.zeros(N + 1, dtype=torch.int64, device=dev)
+            nptr[1:] = torch.cumsum(torch.bincount(wn, minlength=N), 0)
+            del wn
+            colour = torch.empty(nb, dtype=torch.int32, device=dev)
+            flags = torch.zeros(2, dtype=torch.int32, device=dev)
+            call("ab_colour_blocks", nb, ptr(blk_ptr), ptr(wnode), ptr(nptr), ptr(nblk), ptr(colour), ptr(flags),
+                 stream_handle())
+            del nptr, nblk
+            ncol = int(colour.max().item()) + 1
+            corder = torch.sort(colour, stable=True).indices.to(torch.int32).contiguous()
+            cptr = torch.zeros(ncol + 1, dtype=torch.int64, device=dev)
+            cptr[1:] = torch.cumsum(torch.bincount(colour.to(torch.int64), minlength=ncol), 0)
+            gbar = torch.zeros(1, dtype=torch.int32, device=dev)
+            call("ab_set_window_colours", ptr(conn), ncol, ptr(corder), ptr(cptr), ptr(gbar))
+            self._col.append((corder, cptr, gbar, ncol, colour))
+
+    def clear_colours(self):
+        for conn, c in zip(self.conn, self._col):
+            if c is not None:
+                call("ab_set_window_colours", ptr(conn), 0, None, None, None)
+        self._col = []
+
+    def colour_stats(self):
+        """Per category: number of colours and blocks per colour."""
+        out = {}
+        for rule, c in zip(self.rules, self._col):
+            if c is not None:
+                out[rule] = {"colours": c[3], "blocks": [int(v) for v in (c[1][1:] - c[1][:-1]).tolist()]}
+        return out
 
     def build_filter_width(self):
         """Vreman filter width Delta^2 = V_e^(2/3) of every element (geometry
@@ -234,6 +295,7 @@ class DeviceMesh:
         return out
 
     def clear_windows(self):
+        self.clear_colours()
         for conn, w in zip(self.conn, self._win):
             if w is not None:
                 call("ab_set_windows", ptr(conn), WINDOW_BLOCK, None, None, None, None, None, None, 0)

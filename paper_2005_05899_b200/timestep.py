@@ -54,10 +54,11 @@ class FlowSolver:
 
     def __init__(self, mesh, params: FlowParams | None = None, p_fixed=None, u_fixed=None, u_fixed_values=None,
                  windows: bool = True, reorder: str | None = "sfc", halo=None, own=None, ops: str = "spmv",
-                 fused_cg: bool | None = None, wall=None):
+                 fused_cg: bool | None = None, wall=None, scatter: str = "atomic"):
         self.params = params or FlowParams()
         self.phys = self.params.struct()
-        self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows)
+        self.dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh, reorder=reorder, windows=windows,
+                                                                       scatter=scatter)
         dm = self.dm
         # boundary assembly (Algorithm 1 line 4): wall model faces, (faces, off) or a WallModel
         if wall is not None and not hasattr(wall, "add_traction"):

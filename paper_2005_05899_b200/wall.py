@@ -55,10 +55,32 @@ def wall_faces(mesh, on_wall) -> tuple[np.ndarray, np.ndarray]:
 class WallModel:
     """Device face lists + the K8 launch: rhs4 += wall traction of u4."""
 
-    def __init__(self, faces: np.ndarray, off: np.ndarray, device="cuda"):
+    def __init__(self, faces: np.ndarray, off: np.ndarray, device="cuda", ordered: bool = True):
+        """``ordered``: the face tractions are summed per wall node in
+        ascending face order (second small kernel, bitwise reproducible);
+        False keeps the fp64 reductions per face node."""
         self.face = torch.from_numpy(np.ascontiguousarray(faces, dtype=np.int32)).to(device)
         self.off = torch.from_numpy(np.ascontiguousarray(off, dtype=np.int32)).to(device)
         self.struct = AbWall(n_faces=int(self.face.shape[0]), face=ptr(self.face), off=ptr(self.off))
+        self.ordered = bool(ordered and self.face.shape[0] > 0)
+        if self.ordered:
+            f = self.face.to(torch.int64)
+            nf = f.shape[0]
+            fid = torch.arange(nf, device=f.device, dtype=torch.int64)[:, None].expand(nf, 4).reshape(-1)
+            nd = f.reshape(-1)
+            keep = nd >= 0
+            nd, fid = nd[keep], fid[keep]
+            order = torch.sort(nd * nf + fid).indices  # by node, then ascending face id
+            nd, fid = nd[order], fid[order]
+            self.wnode, counts = torch.unique_consecutive(nd, return_counts=True)
+            self.wnode = self.wnode.to(torch.int32).contiguous()
+            self.wptr = torch.zeros(self.wnode.numel() + 1, dtype=torch.int64, device=f.device)
+            self.wptr[1:] = torch.cumsum(counts, 0)
+            self.fref = fid.to(torch.int32).contiguous()
+            self.ftrac = torch.zeros((nf, 3), dtype=torch.float64, device=f.device)
+            s = self.struct
+            s.n_nodes = int(self.wnode.numel())
+            s.node, s.ptr, s.fref, s.ftrac = ptr(self.wnode), ptr(self.wptr), ptr(self.fref), ptr(self.ftrac)
 
     @property
     def n_faces(self) -> int:

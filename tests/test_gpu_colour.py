@@ -1,0 +1,211 @@
+"""The mesh-colouring scatter of the pipelined element kernels (north star
+item (1): "scatter-adds to nodes through mesh colouring or fp64 atomics,
+chosen by measurement").
+
+Colour mode: the 128-element window blocks are coloured so that no two blocks
+of a colour share a node (Jones-Plassmann on the GPU, ab_colour_blocks),
+processed colour by colour behind a grid barrier, and every window node's sum
+is formed by one thread in a fixed order and written with a plain
+read-add-write.  The results must (a) match the oracle within the north
+star's tolerances like the atomic scatter and (b) be bitwise reproducible,
+which the fp64-atomic scatter is not (the reference's scatter_global sums in a
+fixed order, assembly.py:317-326)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import fem
+from paper_2005_05899_b200 import meshgen
+
+pytestmark = pytest.mark.gpu
+
+TOL_RHS = 1e-10
+TOL_STATE = 1e-8
+
+MESHES = {
+    "tet": lambda: meshgen.box_tets(6, 5, 4, jitter=0.2, seed=3),
+    "hex_periodic": lambda: meshgen.c1_mesh(6),
+    "mixed": lambda: meshgen.c3_mesh(0.05),
+    "hex": lambda: meshgen.box_hexes(4, 3, 5, lengths=(1.0, 0.7, 1.3)),
+    "tet_large": lambda: meshgen.box_tets(40, 40, 40, jitter=0.2, seed=5),
+}
+
+
+def _field(m, seed=0):
+    rng = np.random.default_rng(seed)
+    x = m.coords
+    u = np.stack([np.sin(3 * x[:, 0]) * np.cos(2 * x[:, 1]), np.cos(x[:, 2]) * x[:, 0], x[:, 1] ** 2], axis=1)
+    return u + 0.1 * rng.standard_normal(u.shape), np.cos(2 * x[:, 0] + x[:, 1]) + rng.standard_normal(len(x)) * 0.1
+
+
+def _dm(m, scatter="colour"):
+    from paper_2005_05899_b200.device import DeviceMesh
+    return DeviceMesh(m, reorder="sfc", windows=True, pipelined=True, scatter=scatter)
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_colouring_is_proper(name):
+    """Every block coloured, no two blocks of a colour share a window node,
+    corder groups the blocks by colour in ascending block order."""
+    m = MESHES[name]()
+    dm = _dm(m)
+    for k, (conn, w, col) in enumerate(zip(dm.conn, dm._win, dm._col)):
+        if w is None:
+            continue
+        corder, cptr, _gbar, ncol, colour = col
+        blk_ptr, wnode = w[0].cpu().numpy(), w[1].cpu().numpy()
+        colour = colour.cpu().numpy()
+        nb = len(blk_ptr) - 1
+        assert colour.min() >= 0 and colour.max() == ncol - 1 and ncol <= 64
+        co = corder.cpu().numpy()
+        cp = cptr.cpu().numpy()
+        assert cp[0] == 0 and cp[-1] == nb
+        assert np.array_equal(np.sort(co), np.arange(nb))
+        for c in range(ncol):
+            blocks = co[cp[c]:cp[c + 1]]
+            assert np.all(colour[blocks] == c) and np.all(np.diff(blocks) > 0)
+            nodes = np.concatenate([wnode[blk_ptr[b]:blk_ptr[b + 1]] for b in blocks])
+            assert len(np.unique(nodes)) == len(nodes), f"colour {c} of category {k} shares a node"
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+@pytest.mark.parametrize("c_vreman", [0.0, 0.07])
+def test_colour_k2_matches_oracle_and_is_reproducible(name, c_vreman):
+    from paper_2005_05899_b200.ops import assemble_momentum
+    from paper_2005_05899_b200.timestep import FlowParams
+    m = MESHES[name]()
+    u, _ = _field(m)
+    ph = FlowParams(rho=1.3, mu=0.01, c_vreman=c_vreman)
+    ref = fem.momentum_rhs(m, u, rho=1.3, mu=0.01, c_vreman=c_vreman)
+    dm = _dm(m)
+    a = assemble_momentum(dm, u, ph).cpu().numpy()
+    assert rel_l2(a, ref) <= TOL_RHS
+    for _ in range(3):
+        b = assemble_momentum(dm, u, ph).cpu().numpy()
+        assert np.array_equal(a, b), "colour-mode K2 is not bitwise reproducible"
+    # a second, independently built colouring gives the same bits
+    c = assemble_momentum(_dm(m), u, ph).cpu().numpy()
+    assert np.array_equal(a, c)
+    # and the atomic scatter agrees to rounding
+    d = assemble_momentum(_dm(m, "atomic"), u, ph).cpu().numpy()
+    assert rel_l2(d, a) <= 1e-13
+
+
+@pytest.mark.parametrize("name", list(MESHES))
+def test_colour_element_divergence_gradient(name):
+    from paper_2005_05899_b200.ops import assemble_divergence, assemble_gradient
+    m = MESHES[name]()
+    u, p = _field(m, 2)
+    dm = _dm(m)
+    d = assemble_divergence(dm, u, -2.0).cpu().numpy()
+    assert rel_l2(d, -2.0 * fem.divergence(m, u)) <= TOL_RHS
+    assert np.array_equal(d, assemble_divergence(dm, u, -2.0).cpu().numpy())
+    g = assemble_gradient(dm, p).cpu().numpy()
+    assert rel_l2(g, fem.gradient(m, p)) <= TOL_RHS
+    assert np.array_equal(g, assemble_gradient(dm, p).cpu().numpy())
+
+
+def test_colour_multi_block_regime():
+    """~1M tets: several colours, each CTA walking blocks of many colours and
+    crossing colour barriers with the prefetch ring in flight."""
+    from paper_2005_05899_b200.ops import assemble_momentum
+    from paper_2005_05899_b200.timestep import FlowParams
+    m = meshgen.box_tets(56, 56, 56, jitter=0.2, seed=7)
+    u, _ = _field(m, 3)
+    dm = _dm(m)
+    st = dm.colour_stats()["tet4"]
+    assert st["colours"] >= 4 and min(st["blocks"]) > 0
+    ph = FlowParams(rho=1.2, mu=3e-3, c_vreman=0.07)
+    a = assemble_momentum(dm, u, ph).cpu().numpy()
+    ref = fem.momentum_rhs(m, u, rho=1.2, mu=3e-3, c_vreman=0.07)
+    assert rel_l2(a, ref) <= TOL_RHS
+    b = assemble_momentum(dm, u, ph).cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_colour_time_steps_match_oracle_and_repeat_bitwise(graph):
+    """Full time steps with the colour scatter: within the state tolerance of
+    the oracle, and two runs from the same state on the same solver give the
+    same bits (the CG reductions are fixed trees; no wall model here)."""
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+    m = meshgen.box_tets(10, 9, 8, jitter=0.2, seed=11)
+    u, p = _field(m, 4)
+    bc = dict(p_fixed=meshgen.boundary_nodes(m))
+    params = dict(rho=1.0, mu=0.01, c_vreman=0.07)
+    ora = fem.FlowOracle(m, **params, **bc)
+    st = ora.init_state(u, p)
+    fs = FlowSolver(m, FlowParams(**params), **bc, scatter="colour")
+    runs = []
+    for rep in range(2):
+        fs.set_state(u, p)
+        for _ in range(3):
+            if rep == 0:
+                st = ora.step(st, 2e-3, cg_iters=40)
+            fs.step(2e-3, cg_iters=40, graph=graph)
+        torch.cuda.synchronize()
+        runs.append((fs.u.cpu().numpy().copy(), fs.p.cpu().numpy().copy()))
+    assert rel_l2(runs[0][0], st["u"]) <= TOL_STATE
+    assert rel_l2(runs[0][1], st["p"]) <= TOL_STATE
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])
+
+
+def test_colour_mode_errors():
+    from paper_2005_05899_b200.device import DeviceMesh
+    m = meshgen.box_tets(3, 3, 3)
+    with pytest.raises(ValueError):
+        DeviceMesh(m, windows=False, scatter="colour")
+    with pytest.raises(ValueError):
+        DeviceMesh(m, windows=True, scatter="graph")
+
+
+def test_ordered_wall_traction_reproducible():
+    """K8 in its fixed-order form (face tractions summed per wall node in
+    ascending face order) = the oracle, bitwise repeatable, and equal to the
+    fp64-reduction form up to rounding."""
+    from paper_2005_05899_b200.device import DeviceMesh, nodes_as4
+    from paper_2005_05899_b200.timestep import FlowParams
+    from paper_2005_05899_b200.wall import WallModel
+    m = meshgen.c3_mesh(0.08)
+    _bc, (F, O) = meshgen.wall_model_bcs(m)
+    u, _ = _field(m, 5)
+    u[:, 0] += 1.0
+    dm = DeviceMesh(m)
+    u4 = nodes_as4(torch.from_numpy(u).cuda())
+    ph = FlowParams(rho=1.3, mu=2e-3).struct()
+    outs = []
+    for ordered in (True, True, False):
+        out = torch.zeros((m.n_nodes, 4), dtype=torch.float64, device="cuda")
+        WallModel(F, O, ordered=ordered).add_traction(ph, dm.coords4, u4, out)
+        outs.append(out[:, :3].cpu().numpy())
+    ref = fem.wall_traction(m, F, O, u, 1.3, 2e-3)
+    assert rel_l2(outs[0], ref) <= TOL_RHS
+    assert np.array_equal(outs[0], outs[1])
+    assert rel_l2(outs[2], outs[0]) <= 1e-14
+
+
+def test_colour_wall_model_steps_repeat_bitwise():
+    """Mixed tet/prism/pyramid/hex mesh with the wall model: colour scatter +
+    ordered K8 -> the full step is bitwise repeatable and matches the oracle."""
+    from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
+    m = meshgen.c3_mesh(0.06)
+    bc, wall = meshgen.wall_model_bcs(m)
+    u, p = _field(m, 6)
+    params = dict(rho=1.0, mu=0.01, c_vreman=0.07)
+    ora = fem.FlowOracle(m, **params, **bc, wall=wall)
+    st = ora.init_state(u, p)
+    fs = FlowSolver(m, FlowParams(**params), **bc, wall=wall, scatter="colour")
+    runs = []
+    for rep in range(2):
+        fs.set_state(u, p)
+        for _ in range(2):
+            if rep == 0:
+                st = ora.step(st, 2e-3, cg_iters=40)
+            fs.step(2e-3, cg_iters=40, graph=True)
+        torch.cuda.synchronize()
+        runs.append((fs.u.cpu().numpy().copy(), fs.p.cpu().numpy().copy()))
+    assert rel_l2(runs[0][0], st["u"]) <= TOL_STATE
+    assert rel_l2(runs[0][1], st["p"]) <= TOL_STATE
+    assert np.array_equal(runs[0][0], runs[1][0]) and np.array_equal(runs[0][1], runs[1][1])

@@ -2,7 +2,7 @@
 int32 vs 16-bit columns, Jacobi z-form vs the symmetrically scaled form.
 Graph-replayed 50-iteration solves, L2 flushed before each, device time.
 
-    python tools/lab/time_spmv16.py [scale]
+    python tools/lab/time_spmv16.py [scale] [variant,variant,...]
 """
 import sys
 from pathlib import Path
@@ -23,8 +23,13 @@ b = torch.randn(A.n_rows, dtype=torch.float64, device="cuda")
 b[fixed.cuda()] = 0
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
 ref = None
-for name, kw in {"int32-jacobi": dict(compress_cols=False, scaled=False), "16-jacobi": dict(scaled=False),
-                 "int32-scaled": dict(compress_cols=False), "16-scaled": dict()}.items():
+VARIANTS = {"int32-jacobi": dict(compress_cols=False, scaled=False),
+            "16-jacobi": dict(compress_cols=True, scaled=False),
+            "int32-scaled-diag": dict(compress_cols=False, unit_diag=False),
+            "16-scaled-diag": dict(compress_cols=True),
+            "int32-scaled-unit": dict(compress_cols=False, unit_diag=True)}
+only = sys.argv[2].split(",") if len(sys.argv) > 2 else list(VARIANTS)
+for name, kw in ((k, VARIANTS[k]) for k in only):
     pcg = PCG(A, 1.0 / A.diag, fixed=fixed, order=order, resident=False, **kw)
     work = b.clone()
     pcg.solve(work, 50, zero_b=False)
@@ -42,5 +47,5 @@ for name, kw in {"int32-jacobi": dict(compress_cols=False, scaled=False), "16-ja
     if ref is None:
         ref = x
     d = float((x - ref).norm() / ref.norm())
-    near = pcg.perm2["A16"]["near_fraction"] if pcg.perm2["A16"] is not None else None
+    near = round(pcg.perm2["A16"]["near_fraction"], 4) if pcg.perm2["A16"] is not None else None
     print(f"{name:14s} {np.median(ts) * 1e3 / 50:8.1f} us/iteration  rel-diff {d:.2e}  near {near}", flush=True)
