@@ -1175,6 +1175,10 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
           }
           red_node(l, acc);
         }
+        // this thread's reductions are performed (gpu scope) before the
+        // CTA announces the colour as finished: the barrier arrival of thread
+        // 0 alone does not wait for the other warps' in-flight REDs
+        __threadfence();
       } else {
         const int lane = threadIdx.x & 31;
         const uint32_t mine = f | (np >= 2 ? 0x80000000u : 0u);

@@ -21,6 +21,7 @@ from collections import defaultdict
 RULES = {0: "tet1", 1: "tet4", 2: "pyr5", 3: "pri6", 4: "hex8"}
 NAMES = [  # (regex on the demangled kernel name, bench timeline label)
     (r"k_pipe<(\d), 0, 128", "K2_momentum[{}]"),
+    (r"k_wall_gather", "K8_wall_gather"),
     (r"k_wall", "K8_wall"),
     (r"k_rk_stage", "K3_rk_stage"),
     (r"k_go_div", "K4_divergence"),
