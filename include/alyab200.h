@@ -123,8 +123,9 @@ int ab_set_window_refs(const int32_t* conn, const uint32_t* wref);
  * by colour, cptr [ncol+1] offsets), no two blocks of a colour share a window
  * node, and every node sum is formed in a fixed order, so K2/K4/K6 results
  * are bitwise reproducible run to run (the reference's scatter_global sums in
- * a fixed order, assembly.py:317-326).  gbar: one device uint32 (barrier
- * word).  ncol 0 / NULL corder restores the fp64-atomic scatter. */
+ * a fixed order, assembly.py:317-326).  gbar: ncol device uint32 (one
+ * barrier counter per colour).  ncol 0 / NULL corder restores the fp64-atomic
+ * scatter. */
 int ab_set_window_colours(const int32_t* conn, int32_t ncol, const int32_t* corder, const int64_t* cptr,
                           uint32_t* gbar);
 /* Jones-Plassmann colouring of the window blocks (setup): blocks b, b' are

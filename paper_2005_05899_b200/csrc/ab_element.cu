@@ -10,6 +10,8 @@
 //     reduces them per unique node of the block's "node window" in a fixed
 //     order, issuing one global reduction per (block, node) instead of one
 //     per (element, node).
+#include <cstdlib>
+
 #include "ab_common.cuh"
 #include "ab_tables.inc"
 
@@ -54,7 +56,7 @@ struct WinP {
   // bitwise reproducible results.
   const int32_t* __restrict__ corder;    // [n_blocks] logical -> physical block, grouped by colour
   const int64_t* __restrict__ cptr;      // [ncol+1] colour offsets into corder
-  unsigned* gbar;                        // grid-barrier counter (zeroed before every launch)
+  unsigned* gbar;                        // [ncol] colour-barrier counters (zeroed before every launch)
   int ncol;
 };
 
@@ -910,6 +912,23 @@ __device__ __forceinline__ int64_t pos_block(const WinP& w, Pos p) {
   return p.j;
 }
 
+// Colour barrier: gbar[k] counts the CTAs that have finished colour k.  A
+// CTA moving on from colour `done` to colour c announces done .. c-1 (one
+// release-add each, in order), and before reducing into colour c it waits for
+// gbar[c-1] == gridDim.x: every CTA has announced c-1, hence finished every
+// colour <= c-1.  (One counter summed over all colours would let CTAs that
+// skip ahead several colours satisfy the target for CTAs still behind.)
+__device__ __forceinline__ void colour_arrive(unsigned* gbar, int from, int to) {
+  for (int k = from; k < to; ++k) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gbar + k) : "memory");
+}
+__device__ __forceinline__ void colour_wait(const unsigned* gbar, int c) {
+  if (c == 0) return;
+  unsigned v;
+  do {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gbar + c - 1) : "memory");
+  } while (v < gridDim.x);
+}
+
 // Colour-mode scratch behind the slot buffer: each thread's first window
 // index (bit 31: the thread holds a single run), last window index and first
 // run's partial sum.
@@ -928,8 +947,8 @@ struct ColSmem {
 // Three metadata stages and two node stages make every buffer reuse safe
 // with two CTA barriers per block.
 // COL (mesh colouring, deterministic): before phase D of a block of colour c
-// the CTA has announced every colour < c as finished (release-add on
-// w.gbar) and waits until all CTAs have (counter >= c * gridDim.x); phase D
+// the CTA has announced every colour < c as finished and waits until all
+// CTAs have (colour_arrive / colour_wait: one counter per colour); phase D
 // then forms each window node's total in one thread (the references in
 // sorted order, runs crossing lanes summed by the lane where they start) and
 // issues ONE fp64 reduction per node: no two blocks of a colour share a
@@ -954,7 +973,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
   int done = 0;  // COL: colours this CTA has announced as finished
   if (p0.j < 0) {
     if constexpr (COL) {
-      if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(w.ncol) : "memory");
+      if (threadIdx.x == 0) colour_arrive(w.gbar, 0, w.ncol);
     }
     return;
   }
@@ -1024,7 +1043,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
       if constexpr (COL) {
         // every thread's phase D of the previous block is behind barrier B
         if (p0.c > done) {
-          asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(p0.c - done) : "memory");
+          colour_arrive(w.gbar, done, p0.c);
           done = p0.c;
           col_wait = true;
         }
@@ -1085,13 +1104,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
         for (int k = 0; k < NC; ++k) slots[(k * NN + a) * BLOCK + threadIdx.x] = 0.0;
     }
     if constexpr (COL) {
-      if (col_wait) {
-        const unsigned target = (unsigned)p0.c * gridDim.x;
-        unsigned v;
-        do {
-          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(w.gbar) : "memory");
-        } while (v < target);
-      }
+      if (col_wait) colour_wait(w.gbar, p0.c);
     }
     __syncthreads();
     // D: thread t sums the block's sorted references t*NN .. t*NN+NN-1 (the
@@ -1175,10 +1188,6 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
           }
           red_node(l, acc);
         }
-        // this thread's reductions are performed (gpu scope) before the
-        // CTA announces the colour as finished: the barrier arrival of thread
-        // 0 alone does not wait for the other warps' in-flight REDs
-        __threadfence();
       } else {
         const int lane = threadIdx.x & 31;
         const uint32_t mine = f | (np >= 2 ? 0x80000000u : 0u);
@@ -1213,8 +1222,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
   }
   if constexpr (COL) {
     __syncthreads();  // this CTA's last phase D is issued
-    if (threadIdx.x == 0 && w.ncol > done)
-      asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(w.gbar), "r"(w.ncol - done) : "memory");
+    if (threadIdx.x == 0) colour_arrive(w.gbar, done, w.ncol);
   }
 }
 
@@ -1251,7 +1259,18 @@ static int launch_pipe_impl(const CatP& c, const WinP& w, const ab_phys& ph, dou
   if (COL) {
     // every CTA must be resident at once (colour barrier): grid <= sms * per_sm
     if (!w.gbar || !w.cptr || w.ncol < 1) return fail("k_pipe colour mode: colours not registered");
-    if (cudaMemsetAsync(w.gbar, 0, sizeof(unsigned), stream) != cudaSuccess)
+    static const bool split = getenv("AB_COLOUR_SPLIT") != nullptr;  // lab: one launch per colour
+    if (split) {
+      for (int cc = 0; cc < w.ncol; ++cc) {
+        WinP w1 = w;
+        w1.cptr = w.cptr + cc;
+        w1.ncol = 1;
+        kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w1, ph, scale, f, out, n_blocks);
+        if (int rc = check_launch("k_pipe")) return rc;
+      }
+      return AB_OK;
+    }
+    if (cudaMemsetAsync(w.gbar, 0, sizeof(unsigned) * w.ncol, stream) != cudaSuccess)
       return fail("k_pipe colour mode: barrier reset failed");
   }
   kern<<<(unsigned)grid, BLOCK, smem, stream>>>(c, w, ph, scale, f, out, n_blocks);

@@ -250,7 +250,7 @@ class DeviceMesh:
             corder = torch.sort(colour, stable=True).indices.to(torch.int32).contiguous()
             cptr = torch.zeros(ncol + 1, dtype=torch.int64, device=dev)
             cptr[1:] = torch.cumsum(torch.bincount(colour.to(torch.int64), minlength=ncol), 0)
-            gbar = torch.zeros(1, dtype=torch.int32, device=dev)
+            gbar = torch.zeros(max(ncol, 1), dtype=torch.int32, device=dev)  # one barrier counter per colour
             call("ab_set_window_colours", ptr(conn), ncol, ptr(corder), ptr(cptr), ptr(gbar))
             self._col.append((corder, cptr, gbar, ncol, colour))
 
