@@ -760,13 +760,14 @@ __device__ __forceinline__ Chunk chunk16(const void* base, int64_t lo_elem, int6
   return Chunk{reinterpret_cast<const char*>(a), (uint32_t)(b - a), (uint32_t)((lo - a) / es)};
 }
 
-// Shared-memory layout: 3 metadata stages (window node ids, sorted
-// references, element window indices), 2 node-data stages, 1 slot buffer.
+// Shared-memory layout: 3 metadata stages (the descriptor of the CTA's next
+// block, window node ids, sorted references, element window indices), 2
+// node-data stages, 1 slot buffer.
 template <int NN, int NV, int BLOCK>
 struct PipeSmem {
   static __host__ __device__ size_t wcap(int wmax) { return ((size_t)wmax + 8 + 3) & ~(size_t)3; }
   static __host__ __device__ size_t meta_bytes(int wmax) {
-    return wcap(wmax) * 4 + (size_t)BLOCK * NN * 4 + ((size_t)BLOCK * NN + 16) * 2;
+    return 16 + wcap(wmax) * 4 + (size_t)BLOCK * NN * 4 + ((size_t)BLOCK * NN + 16) * 2;
   }
   static __host__ __device__ size_t node_bytes(int wmax) { return (size_t)NV * wmax * 8; }
   static __host__ __device__ size_t slot_bytes() { return sizeof(double) * 3 * NN * BLOCK; }
@@ -776,6 +777,7 @@ struct PipeSmem {
 };
 
 struct MetaPtr {
+  int4* next;  // descriptor of the block after this one (bulk-copied with it)
   int32_t* wnode;
   uint32_t* wref;
   uint16_t* loc;
@@ -787,6 +789,8 @@ __device__ __forceinline__ MetaPtr meta_ptr(unsigned char* smem, int wmax, int q
   unsigned char* base = smem + (size_t)q * L::meta_bytes(wmax);
   const size_t wn = L::wcap(wmax) * 4, wr = (size_t)BLOCK * NN * 4;
   MetaPtr m;
+  m.next = reinterpret_cast<int4*>(base);
+  base += 16;
   m.wnode = reinterpret_cast<int32_t*>(base);
   m.wref = reinterpret_cast<uint32_t*>(base + wn);
   m.loc = reinterpret_cast<uint16_t*>(base + wn + wr);
@@ -804,16 +808,19 @@ __device__ __forceinline__ BlockView block_view(const WinP& w, int4 d) {
   return v;
 }
 
-// Elected thread: bulk-copy the metadata of element block b.
+// Elected thread: bulk-copy the metadata of element block b, plus the
+// descriptor of block bnext (the CTA's block after b; none if < 0), so no
+// thread waits on a global descriptor load in the loop.
 template <int NN>
-__device__ __forceinline__ void issue_meta(const WinP& w, int64_t n_elem, int64_t b, int4 d, const MetaPtr& m,
-                                           uint64_t* bar) {
+__device__ __forceinline__ void issue_meta(const WinP& w, int64_t n_elem, int64_t b, int4 d, int64_t bnext,
+                                           const MetaPtr& m, uint64_t* bar) {
   const int64_t e0 = b * w.block;
   const int64_t e1 = e0 + w.block < n_elem ? e0 + w.block : n_elem;
   const Chunk cw = chunk16(w.wnode, d.x, d.y, 4);
   const Chunk cr = chunk16(w.wref, e0 * NN, (e0 + w.block) * NN, 4);  // padded to whole blocks
   const Chunk cl = chunk16(w.loc, e0 * NN, e1 * NN, 2);
-  mbar_arrive_tx(bar, cw.bytes + cr.bytes + cl.bytes);
+  mbar_arrive_tx(bar, cw.bytes + cr.bytes + cl.bytes + (bnext >= 0 ? 16u : 0u));
+  if (bnext >= 0) bulk_copy(m.next, w.desc + bnext, 16, bar);
   bulk_copy(m.wnode, cw.src, cw.bytes, bar);
   bulk_copy(m.wref, cr.src, cr.bytes, bar);
   bulk_copy(m.loc, cl.src, cl.bytes, bar);
@@ -860,6 +867,9 @@ template <int R> struct OpT<R, OP_GRADIENT> { static constexpr int NV = 4, NC = 
 
 #ifndef PIPE_OCC_K2
 #define PIPE_OCC_K2 3  // register cap of the tet4 K2 (launch_bounds min CTAs); the compiler then uses 96 registers and 5 CTAs/SM are resident. C2 bench: 157.3 us vs 159.1 with the cap for 4 (94 regs)
+#endif
+#ifndef PIPE_D_BRANCHLESS
+#define PIPE_D_BRANCHLESS 1
 #endif
 // minimum resident CTAs per SM requested from the register allocator
 template <int R, int OP> struct PipeOcc { static constexpr int value = 1; };
@@ -994,15 +1004,16 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
   Pos p2 = pos_next<COL>(w, n_blocks, p1);
   int64_t b0 = pos_block<COL>(w, p0);
   int64_t cb1 = COL ? pos_block<COL>(w, p1) : -1, cb2 = COL ? pos_block<COL>(w, p2) : -1;
-  int4 d0, d1, d2;
+  // d0, d1: descriptors of the current and the next block; the one after
+  // arrives with the next block's metadata (MetaPtr::next)
+  int4 d0, d1;
   {
     const int64_t b1 = COL ? cb1 : nxt(b0), b2 = COL ? cb2 : nxt(b1);
     d0 = __ldg(w.desc + b0);
     d1 = b1 >= 0 ? __ldg(w.desc + b1) : d0;
-    d2 = b2 >= 0 ? __ldg(w.desc + b2) : d0;
     if (threadIdx.x == 0) {
-      issue_meta<NN>(w, c.n, b0, d0, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), &bars[0]);
-      if (b1 >= 0) issue_meta<NN>(w, c.n, b1, d1, meta_ptr<NN, NV, BLOCK>(smem, wmax, 1), &bars[1]);
+      issue_meta<NN>(w, c.n, b0, d0, b1, meta_ptr<NN, NV, BLOCK>(smem, wmax, 0), &bars[0]);
+      if (b1 >= 0) issue_meta<NN>(w, c.n, b1, d1, b2, meta_ptr<NN, NV, BLOCK>(smem, wmax, 1), &bars[1]);
     }
   }
   mbar_wait_parity(&bars[0], 0);
@@ -1018,7 +1029,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     Pos p3{-1, 0};
     if constexpr (COL) p3 = pos_next<COL>(w, n_blocks, p2);
     const int64_t b3 = COL ? pos_block<COL>(w, p3) : nxt(b2);
-    const int4 d3 = b3 >= 0 ? __ldg(w.desc + b3) : d0;  // lands during this block
+    int4 d2 = d0;
     // precomputed filter width of this thread's element: in flight across the waits below
     double d2e = -1.0;
     if constexpr (OP == OP_MOMENTUM) {
@@ -1028,7 +1039,9 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     // A: node data of the next block
     if (b1 >= 0) {
       mbar_wait_parity(&bars[mq1], (uint32_t)(((it + 1) / 3) & 1));
-      issue_nodes<NV, BLOCK>(c, f, wmax, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq1), block_view(w, d1), nodes_nxt);
+      const MetaPtr m1 = meta_ptr<NN, NV, BLOCK>(smem, wmax, mq1);
+      if (b2 >= 0) d2 = *m1.next;
+      issue_nodes<NV, BLOCK>(c, f, wmax, m1, block_view(w, d1), nodes_nxt);
       cp_async_wait<1>();
     } else {
       cp_async_wait<0>();
@@ -1038,7 +1051,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     if (threadIdx.x == 0) {
       if (b2 >= 0) {
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        issue_meta<NN>(w, c.n, b2, d2, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq2), &bars[mq2]);
+        issue_meta<NN>(w, c.n, b2, d2, b3, meta_ptr<NN, NV, BLOCK>(smem, wmax, mq2), &bars[mq2]);
       }
       if constexpr (COL) {
         // every thread's phase D of the previous block is behind barrier B
@@ -1139,6 +1152,61 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
 #pragma unroll
         for (int q = 0; q < NC; ++q) red_add(out + (int64_t)node * STRIDE + q, v[q]);
       };
+#if PIPE_D_BRANCHLESS
+      if constexpr (!COL) {
+        // Branch-free form: segmented running sums a[k] over the runs of equal
+        // window index, the first run's end kf found by selects, one shuffle
+        // level of hand-over as below; only the reductions are predicated.
+        uint32_t wv[NN];
+#pragma unroll
+        for (int k = 0; k < NN; ++k) wv[k] = rr[k] >> 16;
+        double a[NN][NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) a[0][q] = vq[0][q];
+#pragma unroll
+        for (int k = 1; k < NN; ++k) {
+          const bool e = wv[k] == wv[k - 1];
+#pragma unroll
+          for (int q = 0; q < NC; ++q) a[k][q] = e ? a[k - 1][q] + vq[k][q] : vq[k][q];
+        }
+        bool end[NN];
+#pragma unroll
+        for (int k = 0; k < NN - 1; ++k) end[k] = wv[k + 1] != wv[k];
+        end[NN - 1] = true;
+        int kf = NN - 1;
+        double H[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) H[q] = a[NN - 1][q];
+#pragma unroll
+        for (int k = NN - 2; k >= 0; --k)
+          if (end[k]) {
+            kf = k;
+#pragma unroll
+            for (int q = 0; q < NC; ++q) H[q] = a[k][q];
+          }
+        const bool two = kf < NN - 1;
+        const uint32_t f = wv[0], l = wv[NN - 1];
+        const int lane = threadIdx.x & 31;
+        const uint32_t mine = f | (two ? 0x80000000u : 0u);
+        const uint32_t nxt = __shfl_down_sync(0xffffffffu, mine, 1);
+        const uint32_t prv = __shfl_up_sync(0xffffffffu, l, 1);
+        double hn[NC];
+#pragma unroll
+        for (int q = 0; q < NC; ++q) hn[q] = __shfl_down_sync(0xffffffffu, H[q], 1);
+        const bool recv = lane != 31 && (nxt >> 31) && (nxt & 0xffffu) == l && l != 0xffffu;
+        const bool give = lane != 0 && two && prv == f && f != 0xffffu;
+#pragma unroll
+        for (int k = 0; k < NN - 1; ++k)
+          if (end[k] && wv[k] != 0xffffu && !(k == kf && give)) red_node(wv[k], a[k]);
+        if (l != 0xffffu) {
+          double t[NC];
+#pragma unroll
+          for (int q = 0; q < NC; ++q) t[q] = recv ? a[NN - 1][q] + hn[q] : a[NN - 1][q];
+          red_node(l, t);
+        }
+      } else
+#endif
+      {
       double acc[NC], H[NC];
 #pragma unroll
       for (int q = 0; q < NC; ++q) acc[q] = H[q] = vq[0][q];
@@ -1207,6 +1275,7 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
           red_node(l, acc);
         }
       }
+      }
     }
     if constexpr (COL) {
       p0 = p1;
@@ -1218,7 +1287,6 @@ __global__ void __launch_bounds__(BLOCK, PipeOcc<R, OP>::value) k_pipe(CatP c, W
     b0 = b1;
     d0 = d1;
     d1 = d2;
-    d2 = d3;
   }
   if constexpr (COL) {
     __syncthreads();  // this CTA's last phase D is issued
