@@ -253,42 +253,69 @@ def host_cpu() -> dict:
     return {"cpu_model": model, "nproc": os.cpu_count()}
 
 
-def cpu_sample(workload: str, scale: float, seed: int = 0):
-    """(oracle, initial state, description) of a bounded CPU sample of the
-    workload: the same recipe at a smaller size (boundary-layer box with the
-    wall model for C3/C4/C5, a jittered Kuhn box for C2)."""
+def cpu_sample(workload: str, scale: float, seed: int = 0, c_threads: int | None = None):
+    """(oracle, initial state, element count, description) of a bounded CPU
+    sample of the workload: the same recipe at a smaller size (boundary-layer
+    box with the wall model for C3/C4/C5, a jittered Kuhn box for C2).
+    ``c_threads`` not None: the C + OpenMP restatement (oracle/fem_c.c) on that
+    many threads (0 = all cores) instead of the numpy oracle; setup (lumped
+    mass, Laplacian) is numpy either way and untimed."""
     from oracle import fem
     from paper_2005_05899_b200 import dmesh, meshgen
+    if c_threads is not None:
+        from oracle import femc
+        mk = lambda *a, **k: femc.CFlowOracle(*a, **k, threads=c_threads)  # noqa: E731
+    else:
+        mk = fem.FlowOracle
     if workload == "c2":
         n = max(4, int(round(88 * scale)))
         m = meshgen.box_tets(n, n, n, jitter=0.2, seed=20200131 + seed)
         u, p = meshgen.c2_initial(m.coords)
-        o = fem.FlowOracle(m, **PHYS, p_fixed=meshgen.boundary_nodes(m))
+        o = mk(m, **PHYS, p_fixed=meshgen.boundary_nodes(m))
         return o, o.init_state(u, p), m.n_elements, f"jittered Kuhn TET04 {n}^3 cells"
     spec = dmesh.c3_spec(scale)
     m = spec.global_mesh()
     bc, wall = meshgen.wall_model_bcs(m)
     u = np.zeros((m.n_nodes, 3))
     u[:, 0] = 1.0
-    o = fem.FlowOracle(m, **PHYS, **bc, wall=wall)
+    o = mk(m, **PHYS, **bc, wall=wall)
     return (o, o.init_state(u, np.zeros(m.n_nodes)), m.n_elements,
             f"mixed boundary-layer box {spec.nx}x{spec.ny}x{spec.nz} cells, {spec.layers} prism layers, wall model "
             "(the C3/C4 recipe at reduced size)")
 
 
-def cpu_baseline_sample(workload: str = "c4", steps: int = 2):
-    """Oracle port (numpy, 1 thread) on a bounded sample of the workload."""
+# sample sizes of the CPU legs: the C restatement on all host cores needs a larger sample than numpy on one core
+# for ~10-30 s of CPU work with a few steps
+C_SCALE = {"c2": 48 / 88, "other": 0.25}
+
+
+def cpu_baseline_sample(workload: str = "c4", steps: int = 20):
+    """The C + OpenMP restatement of the step (oracle/fem_c.c) on all host
+    cores, on a bounded sample of the workload; the single-thread numpy oracle
+    on a smaller sample is reported beside it."""
+    from oracle import femc
+    femc.build()
+    o, st, n_el, what = cpu_sample(workload, C_SCALE["c2" if workload == "c2" else "other"], c_threads=0)
+    st = o.step(st, DT, cg_iters=CG_ITERS)  # warm-up
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        st = o.step(st, DT, cg_iters=CG_ITERS)
+    dt = time.perf_counter() - t0
+    out = {"value": n_el * steps / dt / 1e6, "unit": "M element-steps/s", "cores": o.threads, "kind": "port",
+           "sample": f"oracle/fem_c.c (C + OpenMP restatement of oracle/fem.py FlowOracle.step), {what} "
+                     f"({n_el} elements), {steps} full steps (CG {CG_ITERS} it), {o.threads} threads",
+           **host_cpu()}
+    del o
     from threadpoolctl import threadpool_limits
     with threadpool_limits(1):
         o, st, n_el, what = cpu_sample(workload, 0.12 if workload != "c2" else 24 / 88)
-        st = o.step(st, DT, cg_iters=CG_ITERS)  # warm-up
+        st = o.step(st, DT, cg_iters=CG_ITERS)
         t0 = time.perf_counter()
-        for _ in range(steps):
-            st = o.step(st, DT, cg_iters=CG_ITERS)
+        o.step(st, DT, cg_iters=CG_ITERS)
         dt = time.perf_counter() - t0
-    return {"value": n_el * steps / dt / 1e6, "unit": "M element-steps/s", "cores": 1, "kind": "port",
-            "sample": f"oracle/fem.py FlowOracle, {what} ({n_el} elements), {steps} full steps (CG {CG_ITERS} it), "
-                      "numpy single thread", **host_cpu()}
+    out["numpy_oracle_1core"] = {"value": n_el / dt / 1e6, "sample": f"oracle/fem.py FlowOracle, {what} ({n_el} "
+                                 "elements), 1 full step, numpy single thread"}
+    return out
 
 
 KINDS = ("hex8", "pri6", "pyr5", "tet4")
@@ -525,9 +552,11 @@ def run_native(args):
             # the paper's co-execution model with this box's measured rates (context only: no CPU path runs)
             from paper_2005_05899_b200 import coexec
             cb = result["cpu_baseline"]
-            rep = coexec.report(coexec.measured_params(result["value"], cb["value"], n_core=cb.get("nproc") or 1))
+            per_core = cb["value"] / max(1, cb.get("cores") or 1)
+            rep = coexec.report(coexec.measured_params(result["value"], per_core, n_core=cb.get("nproc") or 1))
             result["coexec_model"] = {k: (round(v, 6) if isinstance(v, float) else v) for k, v in rep.items()}
-            result["coexec_model"]["inputs"] = "speedup = value / cpu_baseline.value (one core); ratio = 1 GPU / nproc"
+            result["coexec_model"]["inputs"] = ("speedup = value / (cpu_baseline.value / cores) (one core of the C "
+                                                "restatement); ratio = 1 GPU / nproc")
         except Exception as exc:  # pragma: no cover
             result["cpu_baseline"] = {"error": repr(exc)}
     if rank == 0:
@@ -613,48 +642,36 @@ def k1_point(dm) -> dict:
     return out
 
 
-def _ref_worker(args):
-    workload, steps, warmup, seed = args
-    os.environ["OMP_NUM_THREADS"] = "1"
-    from threadpoolctl import threadpool_limits
-    sys.path.insert(0, str(ROOT))
-    with threadpool_limits(1):
-        o, st, n_el, what = cpu_sample(workload, 0.1 if workload != "c2" else 20 / 88, seed)
-        for _ in range(warmup):
-            st = o.step(st, DT, cg_iters=CG_ITERS)
-        times = []
-        for _ in range(steps):
-            t0 = time.perf_counter()
-            st = o.step(st, DT, cg_iters=CG_ITERS)
-            times.append(time.perf_counter() - t0)
-    return n_el, times, what
-
-
 def run_reference(args):
-    """Reference arm: the CPU restatement of the path (oracle port; the
-    reference package has no NS step to run), one single-threaded process per
-    host core, each stepping an independent replica of a bounded sample of
-    the workload (the C4 recipe at reduced size by default)."""
+    """Reference arm: the CPU restatement of the path (the reference package
+    has no NS step to run) — oracle/fem_c.c, C + OpenMP on all host cores —
+    stepping a bounded sample of the workload (the C4 recipe at reduced
+    size by default)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    import multiprocessing as mp
-    cores = min(os.cpu_count() or 1, 64)
-    steps, warmup = max(1, min(args.steps, 3)), 1
+    from oracle import femc
+    femc.build()
+    steps, warmup = max(1, min(args.steps, 50)), max(1, min(args.warmup, 3))
     name = "c5" if args.weak else args.workload
-    with mp.get_context("spawn").Pool(cores) as pool:
-        res = pool.map(_ref_worker, [(name, steps, warmup, i) for i in range(cores)])
-    n_el, what = res[0][0], res[0][2]
-    per_step = [max(r[1][s] for r in res) for s in range(steps)]
-    value = n_el * cores * steps / sum(per_step) / 1e6
-    sample = (f"oracle/fem.py FlowOracle on {cores} processes x {what} ({n_el} elements each), {steps} timed "
-              f"steps after {warmup} warm-up, full step with CG {CG_ITERS} it")
+    o, st, n_el, what = cpu_sample(name, C_SCALE["c2" if name == "c2" else "other"], c_threads=0)
+    for _ in range(warmup):
+        st = o.step(st, DT, cg_iters=CG_ITERS)
+    times = []
+    for _ in range(steps):
+        t0 = time.perf_counter()
+        st = o.step(st, DT, cg_iters=CG_ITERS)
+        times.append(time.perf_counter() - t0)
+    value = n_el * steps / sum(times) / 1e6
+    cores = o.threads
+    sample = (f"oracle/fem_c.c (C + OpenMP restatement of the step) on {cores} threads, {what} ({n_el} elements), "
+              f"{steps} timed steps after {warmup} warm-up, full step with CG {CG_ITERS} it")
     out = {"impl": "reference", "metric": "M element-steps/s per time step (assembly + CG)",
            "value": round(value, 5), "unit": "M element-steps/s", "n_gpus": args.gpus, "steps": steps,
-           "warmup": warmup, "ms_per_step": round(1e3 * sum(per_step) / steps, 3), "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "warmup": warmup, "ms_per_step": round(1e3 * sum(times) / steps, 3), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{name.upper()} sample (same recipe and algorithm, bounded size: {what})",
-                      "cg_iters": CG_ITERS, "parallelism": f"{cores} CPU processes"},
+                      "cg_iters": CG_ITERS, "parallelism": f"{cores} CPU threads (OpenMP)"},
            "cpu_baseline": {"value": round(value, 5), "unit": "M element-steps/s", "cores": cores, "kind": "port",
                             "sample": sample, **host_cpu()},
            "e2e": {"value": round(value, 5), "unit": "M element-steps/s", "h2d_bytes_per_step": 0,
