@@ -332,6 +332,17 @@ typedef struct ab_cg_local {
   const int32_t* nbr_ptr;
   const int32_t* nbr;
 } ab_cg_local;
+/* Tiled ab_cg_spmv_unit: CTA b owns rows [b R, (b+1) R), R = m->rows_per_cta
+ * (a multiple of 64, m->n_cta * R >= n_rows, R + max_ghost <= 65536); it
+ * stages z of its rows and of its ghost rows (m->ghost[m->ghost_ptr[b] ..
+ * m->ghost_ptr[b+1]), the remote columns) in shared memory and reads the
+ * slices of `a` (values; same entry order) with the 16-bit tile-local
+ * columns m->cols (own row: c - b R, ghost g: R + g).  p and q are bitwise
+ * those of ab_cg_spmv_unit; red[PQ] sums per-tile partials (rounding-level
+ * different).  m->perm, prefetch_depth, variant, force_mode,
+ * nbr are ignored. */
+int ab_cg_spmv_tile(const ab_sell* a, const ab_cg_local* m, const double* z, double* p, double* q, double* red,
+                    double* sc, double* part, uint32_t* cnt, void* stream);
 /* Diagnostics: buf (device, >= 8 * n_cta int64, or NULL to disable) receives
  * globaltimer stamps of the resident solver's phase boundaries in iteration
  * 10 (per CTA: loop top, ghosts gathered, phase A reduced, barrier A,

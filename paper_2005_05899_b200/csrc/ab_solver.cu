@@ -309,6 +309,69 @@ __global__ void __launch_bounds__(kCgBlock) k_cg_spmv_unit(int64_t n, const int6
   }
 }
 
+// Tiled form of k_cg_spmv_unit: CTA b owns rows [b R, (b+1) R) of the
+// (SFC-ordered) system; it stages its own z and its ghost rows' z (the
+// remote columns, ab_cg_local ghost lists) in shared memory, then streams
+// its slices with 16-bit tile-local columns (10 instead of 12 bytes per
+// stored entry) and reads every z from shared memory: no per-entry global
+// gather, whose latency bounds the int32 form once the stream is near the
+// HBM roof.  Each row product has k_cg_spmv_unit's FMA order
+// (bitwise equal); the p.q partials are grouped per tile.
+#ifndef TILE_CHUNK
+#define TILE_CHUNK 8
+#endif
+#ifndef TILE_MINB
+#define TILE_MINB 1
+#endif
+constexpr int kTileBlock = 256;
+__global__ void __launch_bounds__(kTileBlock, TILE_MINB) k_cg_spmv_tile(
+    int64_t n, int rows_per_tile, const int64_t* __restrict__ sp, const uint16_t* __restrict__ lcol,
+    const double* __restrict__ sval, const int32_t* __restrict__ ghost_ptr, const int32_t* __restrict__ ghost,
+    const double* __restrict__ z, double* __restrict__ p, double* __restrict__ q, double* red, double* sc,
+    double* part, uint32_t* cnt) {
+  extern __shared__ __align__(16) double zs[];
+  const int R = rows_per_tile;
+  const int64_t row0 = (int64_t)blockIdx.x * R;
+  const int rows = (int)(n - row0 < R ? n - row0 : R);
+  const double rz_old = sc[AB_SC_RZ];
+  const double rz_new = red[AB_RED_RZN];
+  const double beta = rz_old != 0.0 ? rz_new / rz_old : 0.0;
+  // own rows (16-byte loads; R and row0 are even)
+  {
+    const double2* z2 = reinterpret_cast<const double2*>(z + row0);
+    double2* s2 = reinterpret_cast<double2*>(zs);
+    const int h = rows >> 1;
+    for (int k = threadIdx.x; k < h; k += kTileBlock) s2[k] = __ldcg(z2 + k);
+    if ((rows & 1) && threadIdx.x == 0) zs[rows - 1] = __ldcg(z + row0 + rows - 1);
+  }
+  const int g0 = ghost_ptr[blockIdx.x], ng = ghost_ptr[blockIdx.x + 1] - g0;
+  for (int k = threadIdx.x; k < ng; k += kTileBlock) zs[R + k] = __ldcg(z + __ldg(ghost + g0 + k));
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t s0 = row0 >> 5;
+  const int nsl = (rows + 31) >> 5;
+  double v[1] = {0.0};
+  for (int sl = warp; sl < nsl; sl += kTileBlock / 32) {
+    const double acc = sell_row_dot_smem<TILE_CHUNK>(sp + s0, lcol, sval, zs, sl, lane);
+    const int li = sl * 32 + lane;
+    if (li < rows) {
+      const int64_t i = row0 + li;
+      const double zi = zs[li];
+      const double az = acc + zi;
+      const double pi = fma(beta, p[i], zi);
+      const double qi = fma(beta, q[i], az);
+      p[i] = pi;
+      q[i] = qi;
+      v[0] += pi * qi;
+    }
+  }
+  double tot[1];
+  if (grid_sum<1, kTileBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_PQ] = tot[0];
+    sc[AB_SC_RZ] = rz_new;
+  }
+}
+
 // Single domain on the column-compressed SELL (ab_sell16): the DOT form of
 // k_cg_spmv with 2-byte columns in the slices that allow them.
 #ifndef SPMV16_MINB
@@ -804,6 +867,28 @@ int ab_cg_finish_scaled(int64_t n, const int64_t* iperm, const double* s, const 
                         void* stream) {
   if (n > 0) k_cg_finish_scaled<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, iperm, s, x, out);
   return check_launch("ab_cg_finish_scaled");
+}
+
+int ab_cg_spmv_tile(const ab_sell* a, const ab_cg_local* m, const double* z, double* p, double* q, double* red,
+                    double* sc, double* part, uint32_t* cnt, void* stream) {
+  if (!a || !m || !m->cols || !m->ghost_ptr || !m->ghost) return fail("ab_cg_spmv_tile: null argument");
+  const int64_t n = a->n_rows;
+  const int64_t R = m->rows_per_cta;
+  if (R < 64 || R % 64 || (int64_t)m->n_cta * R < n || R + m->max_ghost > 65536)
+    return fail("ab_cg_spmv_tile: tile map does not match the matrix (rows_per_cta % 64, n_cta * R >= n, "
+                "R + max_ghost <= 65536)");
+  if ((uintptr_t)z & 15) return fail("ab_cg_spmv_tile: z must be 16-byte aligned");
+  const size_t smem = (size_t)(R + m->max_ghost) * sizeof(double);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    if (cudaFuncSetAttribute(k_cg_spmv_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail("ab_cg_spmv_tile: shared memory request rejected (tile too large)");
+    smem_set = smem;
+  }
+  const unsigned grid = (unsigned)((n + R - 1) / R);
+  k_cg_spmv_tile<<<grid, kTileBlock, smem, S(stream)>>>(n, (int)R, a->slice_ptr, m->cols, a->vals, m->ghost_ptr,
+                                                        m->ghost, z, p, q, red, sc, part, cnt);
+  return check_launch("ab_cg_spmv_tile");
 }
 
 int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,

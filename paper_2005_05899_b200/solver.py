@@ -17,6 +17,7 @@ from __future__ import annotations
 import ctypes
 import ctypes as C
 import math
+import os
 from dataclasses import dataclass
 
 import torch
@@ -261,7 +262,7 @@ class PCG:
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
                  reorder_two_kernel: bool = True, compress_cols: bool = False, scaled: bool = True,
-                 unit_diag: bool | None = None):
+                 unit_diag: bool | None = None, tile_rows: int = 2048):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -279,7 +280,7 @@ class PCG:
         rb = C.c_int64(0)
         fits = lib().ab_cg_resident_fits(n, C.byref(rb), C.byref(n_cta))
         # (+ 5 replicated [4][nb] partial tables of the resident solver, all_sum_rep)
-        self.part = torch.zeros(max(2 * (nb + ng), 12 * n_cta.value + 1, 8 * n_cta.value + 20 * ((n_cta.value + 3) // 4 * 4)) + 8,
+        self.part = torch.zeros(max(5 * (nb + ng), 12 * n_cta.value + 1, 8 * n_cta.value + 20 * ((n_cta.value + 3) // 4 * 4)) + 8,
                                 dtype=torch.float64, device=dev)
         self.red = torch.zeros(8, dtype=torch.float64, device=dev)
         self.sc = torch.zeros(8, dtype=torch.float64, device=dev)
@@ -332,6 +333,18 @@ class PCG:
             # optional 16-bit columns in the slices whose columns span < 64k
             # rows: 7% fewer matrix bytes, but measured slower
             self.perm2["A16"] = compress_columns(self.perm2["A"]) if compress_cols else None
+            # tiled SpMV (ab_cg_spmv_tile): z of a tile's rows and ghost rows in
+            # shared memory, 16-bit tile-local columns
+            if os.environ.get("AB_CG_TILE") is not None:  # lab switch
+                tile_rows = int(os.environ["AB_CG_TILE"])
+            self.perm2["tile"] = None
+            if tile_rows and unit:
+                if tile_rows % 64:
+                    raise ValueError("tile_rows must be a multiple of 64")
+                n_t = (n + tile_rows - 1) // tile_rows
+                tm = cg_local_map(self.perm2["A"], tile_rows, n_t)
+                if tm is not None:
+                    self.perm2["tile"] = tm
 
     def _m(self, name):
         import contextlib
@@ -413,7 +426,10 @@ class PCG:
                 if bb == 0.0 or math.sqrt(rr / bb) <= tol:
                     break
             with self._m("K5_cg_spmv"):
-                if pm["unit"]:
+                if pm.get("tile") is not None:
+                    call("ab_cg_spmv_tile", A, ctypes.byref(pm["tile"]["struct"]), ptr(zvec), ptr(self.p),
+                         ptr(self.q), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+                elif pm["unit"]:
                     call("ab_cg_spmv_unit", A, ptr(zvec), ptr(self.p), ptr(self.q), ptr(self.red), ptr(self.sc),
                          ptr(self.part), ptr(self.cnt), s)
                 elif pm["A16"] is not None:

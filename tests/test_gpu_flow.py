@@ -144,7 +144,8 @@ CG_VARIANTS = {
     "local-sfc": dict(order=True),          # ab_cg_resident_local, SFC row order, z gathers from shared memory
     "local": dict(),                        # local column map, node order
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
-    "two-kernel-sfc": dict(order=True, resident=False),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC order, 16-bit cols)
+    "two-kernel-sfc": dict(order=True, resident=False, tile_rows=0),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC)
+    "two-kernel-sfc-tile": dict(order=True, resident=False, tile_rows=64),  # tiled SpMV, z in shared memory (default)
     "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False, compress_cols=False),  # z = D^-1 r form
     "two-kernel-sfc-diag": dict(order=True, resident=False, unit_diag=False),  # scaled, diagonal stored
 }
@@ -173,6 +174,8 @@ def test_pcg_fixed_iterations_and_convergence(name, variant):
     assert (pcg.perm2 is not None) == variant.startswith("two-kernel-sfc")
     if variant in ("local-sfc", "local"):
         assert pcg.local is not None
+    if pcg.perm2 is not None:
+        assert (pcg.perm2["tile"] is not None) == (variant == "two-kernel-sfc-tile")
     bt = torch.from_numpy(b).cuda()
     x, it = pcg.solve(bt.clone(), 7)
     xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 7)

@@ -123,7 +123,7 @@ def test_k2_full_c2(c2):
     assert rel_l2(got, ref) <= TOL_RHS
 
 
-@pytest.mark.parametrize("variant", ["resident-sfc", "two-kernel", "two-kernel-sfc"])
+@pytest.mark.parametrize("variant", ["resident-sfc", "two-kernel", "two-kernel-sfc", "two-kernel-sfc-tile"])
 def test_cg_full_c2_system(c2, variant):
     """9 fixed Jacobi-PCG iterations on the full C2 Laplacian (705k rows)."""
     from paper_2005_05899_b200.device import DeviceMesh
@@ -135,7 +135,8 @@ def test_cg_full_c2_system(c2, variant):
     dm = DeviceMesh(m)
     A = assemble_laplacian(dm, torch.from_numpy(fixed))
     kw = {"resident-sfc": dict(order=dm.node_order()), "two-kernel": dict(resident=False),
-          "two-kernel-sfc": dict(order=dm.node_order(), resident=False)}[variant]
+          "two-kernel-sfc": dict(order=dm.node_order(), resident=False, tile_rows=0),
+          "two-kernel-sfc-tile": dict(order=dm.node_order(), resident=False, tile_rows=2048)}[variant]  # ab_cg_spmv_tile
     pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), **kw)
     if variant == "resident-sfc":
         lm = pcg.local
