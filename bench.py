@@ -181,6 +181,8 @@ def algorithmic_cost(kernel: str, counts: dict, n_nodes: int, nnz: int, cg_iters
         if unit_diag:  # scaled form: the unit diagonal of D^-1/2 A D^-1/2 is implicit (never read)
             return 12 * (nnz - N) + 8 * N + 32 * N, 2 * nnz + 4 * N
         return 12 * nnz + 8 * N + 32 * N, 2 * nnz + 4 * N
+    if kernel == "K5_cg_tile_iter":  # one whole CG iteration (SURVEY §8(d) K5 per iteration)
+        return 12 * nnz + 4 * (N + 1) + 104 * N, 2 * nnz + 12 * N
     if kernel == "K5_cg_dot":       # z t p q in, p q out
         return 48 * N, 6 * N
     if kernel == "K5_cg_update":    # x p r q dinv in, x r z out
@@ -490,6 +492,31 @@ def run_native(args):
             "traffic": traffic, "alg_bytes_per_launch": kern[dom]["alg_bytes"],
             "alg_bytes_definition": "SURVEY.md §8(d) per-unit figure x units per launch"}
     pm = getattr(solver.pcg, "perm2", None)
+    if dom == "K5_cg_tile_iter" and pm is not None and pm.get("single"):
+        # The tiled single pass moves fewer bytes than the SURVEY per-iteration
+        # model (CSR int32 + Jacobi z/D^-1 vectors), so the roofline uses the
+        # bytes this format must move per iteration: 8 B value + 2 B tile-local
+        # column per stored entry, (r', q) read and written (32 B) and (x, p)
+        # read and written (32 B) per row, per ghost row a 4 B index and a
+        # 16 B (r', q) pair, slice and ghost pointers.
+        A2, tm = pm["A"], pm["tile"]
+        n2 = solver.pcg.n
+        n_tiles = (n2 + tm["struct"].rows_per_cta - 1) // tm["struct"].rows_per_cta
+        comp = (10 * A2.nnz_stored + 64 * n2 + 20 * int(tm["ghost"].numel()) + 8 * A2.slice_ptr.numel()
+                + 4 * (n_tiles + 1))
+        t_dom = kern[dom]["avg_us"] * 1e-6
+        roof.update({"achieved": round(comp / t_dom / 1e9, 1), "frac": round(comp / t_dom / 1e9 / peak, 4),
+                     "alg_bytes_per_launch": comp,
+                     "alg_bytes_definition": "compulsory bytes of the stored format per launch (one CG iteration, "
+                                             "ab_cg_tile_iter): 10 B x stored SELL entries (8 B value + 2 B "
+                                             "tile-local column) + 64 B per row ((r', q) and (x, p) pairs read and "
+                                             "written) + 20 B per ghost row + slice/ghost pointers",
+                     "survey_model_bytes": kern[dom]["alg_bytes"],
+                     "survey_model_gbs": round(kern[dom]["gbs"], 1),
+                     "survey_model_note": "SURVEY §8(d) K5 per-iteration model 12Z + 4(N+1) + 104N (CSR int32 "
+                                          "columns, Jacobi z and D^-1 vectors): exceeds the HBM peak because the "
+                                          "format moves fewer bytes"})
+        kern[dom]["compulsory_bytes"] = comp
     if dom == "K5_cg_spmv" and pm is not None and pm.get("tile") is not None:
         # The tiled SpMV stores fewer bytes per entry than the layout-independent
         # SURVEY model (12 B per non-zero), so that model over-counts its

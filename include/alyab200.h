@@ -229,6 +229,8 @@ int ab_sell_spmv(const ab_sell* a, const double* x, double* y, void* stream);
 #define AB_RED_RR 1
 #define AB_RED_PQ 2
 #define AB_RED_ITERS 3
+#define AB_RED_RQ 6    /* tiled single-pass CG (ab_cg_tile_iter): r'.q */
+#define AB_RED_QQ 7    /* tiled single-pass CG: q.q */
 #define AB_RED_FAIL 5  /* sticky failure flag of the decomposed solvers (1.0 = a peer wait timed out) */
 #define AB_SC_RZ 0
 #define AB_SC_BB 1
@@ -343,6 +345,28 @@ typedef struct ab_cg_local {
  * nbr are ignored. */
 int ab_cg_spmv_tile(const ab_sell* a, const ab_cg_local* m, const double* z, double* p, double* q, double* red,
                     double* sc, double* part, uint32_t* cnt, void* stream);
+/* Tiled single-pass scaled CG: ONE kernel per iteration on the same tiles
+ * (rows_per_cta = 1024, 2048 or 4096) and A' without its unit diagonal.
+ * Vectors as 16-byte pairs: xp[i] = (x'_i, p_i), in place; rq[i] = (r'_i,
+ * q_i), ping-pong between two buffers (iteration k reads rq_in, writes
+ * rq_out; the next swaps them).  Iteration: alpha = red[RZN]/red[PQ] (0 if
+ * PQ == 0), beta = (RZN - 2 alpha red[RQ] + alpha^2 red[QQ]) / RZN; per row
+ * r' -= alpha q (own and ghost rows, staged in shared memory), x' += alpha
+ * p, p = r' + beta p, q = A' r' + beta q; then red[RZN] = r'.r', red[RR] =
+ * sum d r'^2 (d non-NULL) or r'.r', red[PQ] = p.q, red[RQ] = r'.q, red[QQ] =
+ * q.q.  init: rq = (s_i b[perm[i]], 0), xp = 0, red[PQ] = red[RQ] =
+ * red[QQ] = 0, sc[BB] = red[RR] (b zeroed if zero_b).  After K iterations x'
+ * holds x'_{K-1}: finish with apply = 1 adds the last alpha p (= K
+ * iterations of the two-kernel loop), apply = 0 returns x'_{K-1} (tolerance
+ * met); out[j] = s_i x'_i, i = iperm[j].  part: >= 5 (nb + nb/64 + 1)
+ * doubles, nb = ceil(n / 256). */
+int ab_cg_tile_init(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                    const double* s, const double* d, double* xp, double* rq, double* red, double* sc, double* part,
+                    uint32_t* cnt, void* stream);
+int ab_cg_tile_iter(const ab_sell* a, const ab_cg_local* m, const double* rq_in, double* rq_out, double* xp,
+                    const double* d, double* red, double* part, uint32_t* cnt, void* stream);
+int ab_cg_tile_finish(int64_t n, const int64_t* iperm, const double* s, const double* xp, const double* red,
+                      int32_t apply, double* out, void* stream);
 /* Diagnostics: buf (device, >= 8 * n_cta int64, or NULL to disable) receives
  * globaltimer stamps of the resident solver's phase boundaries in iteration
  * 10 (per CTA: loop top, ghosts gathered, phase A reduced, barrier A,

@@ -140,6 +140,9 @@ _SIGS = {
     "ab_cg_update_scaled": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_finish_scaled": ([i64, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_spmv_tile": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_tile_init": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_tile_iter": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
+    "ab_cg_tile_finish": ([i64, vp, vp, vp, vp, i32, vp, vp], C.c_int),
     "ab_sell16_fill": ([P(AbSell), vp, vp, vp, vp], C.c_int),
     "ab_cg_spmv16": ([P(AbSell16), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_init_perm": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),

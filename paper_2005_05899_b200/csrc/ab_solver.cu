@@ -372,6 +372,141 @@ __global__ void __launch_bounds__(kTileBlock, TILE_MINB) k_cg_spmv_tile(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Tiled single-pass scaled CG: ONE kernel per iteration (ab_cg_tile_iter).
+// The two-kernel loop moves 88 vector bytes per row and iteration (SpMV: z,
+// p, q; update: x, r, p, q).  Kernel j instead forms, per tile, r'_j =
+// r'_{j-1} - alpha q_{j-1} while staging the tile's rows and ghost rows in
+// shared memory (from 16-byte (r', q) pairs: own rows coalesced, one gather
+// per ghost), then x_j = x_{j-1} + alpha p_{j-1}, p_j = r'_j + beta p_{j-1},
+// q_j = A' r'_j + beta q_{j-1}: 64 bytes per row ((r', q) read from one
+// buffer and written to the other, (x, p) in place) plus the ghosts.
+// alpha_{j-1} = r'r'_{j-1} / p.q_{j-1} comes from the previous kernel's
+// sums; beta_{j-1} needs r'r'_j before any tile has formed r'_j, so it uses
+// the recurrence r'r'_j = r'r'_{j-1} - 2 alpha r'.q_{j-1} + alpha^2 q.q_{j-1}
+// of the previous kernel's three dots (the true r'r'_j summed here feeds
+// alpha_j, so the error does not accumulate).  Iterates equal the two-kernel
+// form's up to that rounding-level difference in beta (tests: 1e-15 of the
+// oracle after 50 iterations on the 705k-row C2 system).
+// red slots: RZN = r'.r' of the r' formed, RR = sum d r'^2 (d given) or
+// r'.r', PQ = p.q, RQ = r'.q, QQ = q.q.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kCgBlock) k_cg_tile_init(int64_t n, const int64_t* __restrict__ perm,
+                                                           const double* __restrict__ b,
+                                                           const uint8_t* __restrict__ fixed,
+                                                           const double* __restrict__ s,
+                                                           const double* __restrict__ d, double2* __restrict__ xp,
+                                                           double2* __restrict__ rq, double* red, double* sc,
+                                                           double* part, uint32_t* cnt) {
+  double v[2] = {0.0, 0.0};
+  for (int64_t i = (int64_t)blockIdx.x * kCgBlock + threadIdx.x; i < n; i += (int64_t)gridDim.x * kCgBlock) {
+    double bi = b[perm[i]];
+    if (fixed && fixed[i]) bi = 0.0;
+    const double ri = s[i] * bi;
+    rq[i] = make_double2(ri, 0.0);
+    xp[i] = make_double2(0.0, 0.0);
+    v[0] += ri * ri;
+    v[1] += d ? d[i] * ri * ri : ri * ri;
+  }
+  double t[2];
+  if (grid_sum<2, kCgBlock>(v, part, cnt, t) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = t[0];
+    red[AB_RED_RR] = t[1];
+    red[AB_RED_PQ] = 0.0;  // alpha_{-1} = 0: the first iteration keeps r'_0 = b' and x = 0
+    red[AB_RED_RQ] = 0.0;
+    red[AB_RED_QQ] = 0.0;
+    sc[AB_SC_RZ] = 0.0;
+    sc[AB_SC_BB] = t[1];
+  }
+}
+
+#ifndef TSP_MINB
+#define TSP_MINB 4  // 63 registers: 4 CTAs of 2048-row tiles per SM (8.1M rows: 291 us vs 402 us uncapped, 86 registers)
+#endif
+// RPT rows per thread: R = 256 RPT rows per tile; warp w multiplies the
+// tile's slices w, w + 8, ...
+template <int RPT>
+__global__ void __launch_bounds__(kTileBlock, TSP_MINB) k_cg_tile_iter(
+    int64_t n, const int64_t* __restrict__ sp, const uint16_t* __restrict__ lcol, const double* __restrict__ sval,
+    const int32_t* __restrict__ ghost_ptr, const int32_t* __restrict__ ghost, const double2* __restrict__ rq_in,
+    double2* __restrict__ rq_out, double2* __restrict__ xp, const double* __restrict__ d, double* red, double* part,
+    uint32_t* cnt) {
+  constexpr int R = kTileBlock * RPT;
+  extern __shared__ __align__(16) double qs[];  // [R] q_{j-1} of the own rows, then zs
+  double* zs = qs + R;                          // [R + ghosts] r'_j of the own and ghost rows
+  const int64_t row0 = (int64_t)blockIdx.x * R;
+  const int rows = (int)(n - row0 < R ? n - row0 : R);
+  const double RR = red[AB_RED_RZN], PQ = red[AB_RED_PQ], RQ = red[AB_RED_RQ], QQ = red[AB_RED_QQ];
+  const double alpha = PQ != 0.0 ? RR / PQ : 0.0;
+  double rr_next = fma(alpha, fma(alpha, QQ, -2.0 * RQ), RR);
+  if (rr_next < 0.0) rr_next = 0.0;
+  const double beta = RR != 0.0 ? rr_next / RR : 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // own rows: r' = r' - alpha q and q_{j-1} into shared memory
+  for (int li = threadIdx.x; li < rows; li += kTileBlock) {
+    const double2 v = rq_in[row0 + li];
+    qs[li] = v.y;
+    zs[li] = fma(-alpha, v.y, v.x);
+  }
+  const int g0 = ghost_ptr[blockIdx.x], ng = ghost_ptr[blockIdx.x + 1] - g0;
+  for (int k = threadIdx.x; k < ng; k += kTileBlock) {
+    const double2 v = rq_in[__ldg(ghost + g0 + k)];
+    zs[R + k] = fma(-alpha, v.y, v.x);
+  }
+  __syncthreads();
+  const int64_t s0 = row0 >> 5;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll 1
+  for (int k = 0; k < RPT; ++k) {
+    const int sl = warp + 8 * k;
+    if (sl * 32 >= rows) break;
+    const double acc = sell_row_dot_smem<TILE_CHUNK>(sp + s0, lcol, sval, zs, sl, lane);
+    const int li = sl * 32 + lane;
+    if (li < rows) {
+      const int64_t i = row0 + li;
+      const double ri = zs[li];
+      const double ar = acc + ri;
+      const double2 w = xp[i];
+      const double pi = fma(beta, w.y, ri);
+      const double qi = fma(beta, qs[li], ar);
+      rq_out[i] = make_double2(ri, qi);
+      xp[i] = make_double2(fma(alpha, w.y, w.x), pi);
+      v[0] += ri * ri;
+      v[1] += d ? __ldg(d + i) * ri * ri : ri * ri;
+      v[2] += pi * qi;
+      v[3] += ri * qi;
+      v[4] += qi * qi;
+    }
+  }
+  double tot[5];
+  if (grid_sum<5, kTileBlock>(v, part, cnt, tot) && threadIdx.x == 0) {
+    red[AB_RED_RZN] = tot[0];
+    red[AB_RED_RR] = tot[1];
+    red[AB_RED_PQ] = tot[2];
+    red[AB_RED_RQ] = tot[3];
+    red[AB_RED_QQ] = tot[4];
+  }
+}
+
+// out[j] = s_i x'_i (i = iperm[j]); `apply`: x' += alpha p first (the x
+// update of the last iteration, alpha = red[RZN] / red[PQ]).
+__global__ void k_cg_tile_finish(int64_t n, const int64_t* __restrict__ iperm, const double* __restrict__ s,
+                                 const double2* __restrict__ xp, const double* __restrict__ red, int apply,
+                                 double* __restrict__ out) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    const int64_t i = iperm[j];
+    const double2 w = xp[i];
+    double xi = w.x;
+    if (apply) {
+      const double PQ = red[AB_RED_PQ];
+      const double alpha = PQ != 0.0 ? red[AB_RED_RZN] / PQ : 0.0;
+      xi = fma(alpha, w.y, xi);
+    }
+    out[j] = s[i] * xi;
+  }
+}
+
 // Single domain on the column-compressed SELL (ab_sell16): the DOT form of
 // k_cg_spmv with 2-byte columns in the slices that allow them.
 #ifndef SPMV16_MINB
@@ -802,6 +937,25 @@ static unsigned cg_grid(int64_t n) {
 
 using namespace ab;
 
+template <int RPT>
+static int tile_iter_launch(const ab_sell* a, const ab_cg_local* m, const double* rq_in, double* rq_out, double* xp,
+                            const double* d, double* red, double* part, uint32_t* cnt, cudaStream_t st) {
+  constexpr int R = kTileBlock * RPT;
+  const int64_t n = a->n_rows;
+  const size_t smem = (size_t)(2 * R + m->max_ghost) * sizeof(double);
+  static size_t smem_set = 0;
+  auto kern = k_cg_tile_iter<RPT>;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail("ab_cg_tile_iter: shared memory request rejected (too many ghost rows)");
+    smem_set = smem;
+  }
+  kern<<<(unsigned)((n + R - 1) / R), kTileBlock, smem, st>>>(
+      n, a->slice_ptr, m->cols, a->vals, m->ghost_ptr, m->ghost, reinterpret_cast<const double2*>(rq_in),
+      reinterpret_cast<double2*>(rq_out), reinterpret_cast<double2*>(xp), d, red, part, cnt);
+  return check_launch("ab_cg_tile_iter");
+}
+
 extern "C" {
 
 int ab_csr_dirichlet(int64_t n, const int64_t* rp, const int32_t* cols, double* vals, const uint8_t* fixed,
@@ -889,6 +1043,44 @@ int ab_cg_spmv_tile(const ab_sell* a, const ab_cg_local* m, const double* z, dou
   k_cg_spmv_tile<<<grid, kTileBlock, smem, S(stream)>>>(n, (int)R, a->slice_ptr, m->cols, a->vals, m->ghost_ptr,
                                                         m->ghost, z, p, q, red, sc, part, cnt);
   return check_launch("ab_cg_spmv_tile");
+}
+
+int ab_cg_tile_init(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,
+                    const double* s, const double* d, double* xp, double* rq, double* red, double* sc, double* part,
+                    uint32_t* cnt, void* stream) {
+  if (n <= 0 || !perm || !b || !s || !xp || !rq) return fail("ab_cg_tile_init: empty system or null argument");
+  if (((uintptr_t)xp | (uintptr_t)rq) & 15) return fail("ab_cg_tile_init: xp, rq must be 16-byte aligned");
+  k_cg_tile_init<<<cg_grid(n), kCgBlock, 0, S(stream)>>>(n, perm, b, fixed, s, d, reinterpret_cast<double2*>(xp),
+                                                         reinterpret_cast<double2*>(rq), red, sc, part, cnt);
+  if (zero_b && cudaMemsetAsync(b, 0, (size_t)n * sizeof(double), S(stream)) != cudaSuccess)
+    return fail("ab_cg_tile_init: cannot zero b");
+  return check_launch("ab_cg_tile_init");
+}
+
+int ab_cg_tile_iter(const ab_sell* a, const ab_cg_local* m, const double* rq_in, double* rq_out, double* xp,
+                    const double* d, double* red, double* part, uint32_t* cnt, void* stream) {
+  if (!a || !m || !m->cols || !m->ghost_ptr || !m->ghost || !rq_in || !rq_out || !xp)
+    return fail("ab_cg_tile_iter: null argument");
+  if (rq_in == rq_out) return fail("ab_cg_tile_iter: rq_in and rq_out must be different buffers (ping-pong)");
+  if (((uintptr_t)xp | (uintptr_t)rq_in | (uintptr_t)rq_out) & 15)
+    return fail("ab_cg_tile_iter: xp, rq must be 16-byte aligned");
+  const int64_t R = m->rows_per_cta;
+  if ((int64_t)m->n_cta * R < a->n_rows || R + m->max_ghost > 65536)
+    return fail("ab_cg_tile_iter: tile map does not match the matrix");
+  switch (R) {
+    case 1024: return tile_iter_launch<4>(a, m, rq_in, rq_out, xp, d, red, part, cnt, S(stream));
+    case 2048: return tile_iter_launch<8>(a, m, rq_in, rq_out, xp, d, red, part, cnt, S(stream));
+    case 4096: return tile_iter_launch<16>(a, m, rq_in, rq_out, xp, d, red, part, cnt, S(stream));
+    default: return fail("ab_cg_tile_iter: rows_per_cta must be 1024, 2048 or 4096");
+  }
+}
+
+int ab_cg_tile_finish(int64_t n, const int64_t* iperm, const double* s, const double* xp, const double* red,
+                      int32_t apply, double* out, void* stream) {
+  if (n > 0)
+    k_cg_tile_finish<<<grid_for(n, 256), 256, 0, S(stream)>>>(n, iperm, s, reinterpret_cast<const double2*>(xp), red,
+                                                              apply, out);
+  return check_launch("ab_cg_tile_finish");
 }
 
 int ab_cg_init_perm(int64_t n, const int64_t* perm, double* b, int32_t zero_b, const uint8_t* fixed,

@@ -262,7 +262,7 @@ class PCG:
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
                  reorder_two_kernel: bool = True, compress_cols: bool = False, scaled: bool = True,
-                 unit_diag: bool | None = None, tile_rows: int = 2048):
+                 unit_diag: bool | None = None, tile_rows: int = 2048, single_pass: bool = True):
         self.A = A
         n = A.n_rows
         dev = A.vals.device
@@ -345,6 +345,16 @@ class PCG:
                 tm = cg_local_map(self.perm2["A"], tile_rows, n_t)
                 if tm is not None:
                     self.perm2["tile"] = tm
+            # tiled single pass (ab_cg_tile_iter): one kernel per iteration,
+            # (x', p) and (r', q) as 16-byte pairs (64 instead of 88 vector
+            # bytes per row); needs a 1024/2048/4096-row tile map
+            if os.environ.get("AB_CG_SINGLE_PASS") is not None:  # lab switch
+                single_pass = os.environ["AB_CG_SINGLE_PASS"] != "0"
+            self.perm2["single"] = bool(single_pass and self.perm2["tile"] is not None
+                                        and tile_rows in (1024, 2048, 4096))
+            if self.perm2["single"]:
+                pair = lambda: torch.zeros(n, 2, dtype=torch.float64, device=dev)  # noqa: E731
+                self.perm2["xp"], self.perm2["rq"] = pair(), (pair(), pair())
 
     def _m(self, name):
         import contextlib
@@ -410,6 +420,8 @@ class PCG:
         A = ctypes.byref(pm["A"].struct)
         sc_ = pm["scaled"]
         d = pm["d"] if (sc_ and tol > 0) else None  # true ||r|| only when a tolerance is tested
+        if pm.get("single"):
+            return self._solve_single_pass(b, maxit, tol, check_every, zero_b, d)
         if sc_:
             call("ab_cg_init_scaled", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
                  ptr(pm["s"]), ptr(d), ptr(self.x), ptr(self.r), ptr(self.p), ptr(self.q), ptr(self.red),
@@ -450,6 +462,33 @@ class PCG:
             call("ab_cg_finish_scaled", self.n, ptr(pm["iperm"]), ptr(pm["s"]), ptr(self.x), ptr(pm["x"]), s)
         else:
             call("ab_perm_scatter", self.n, ptr(pm["perm"]), ptr(self.x), ptr(pm["x"]), s)
+        return pm["x"], it
+
+    def _solve_single_pass(self, b, maxit: int, tol: float, check_every: int, zero_b: bool, d):
+        """One kernel per iteration (ab_cg_tile_iter): iteration k forms x'_k,
+        r'_k, p_k and q_k; the finish adds the last alpha p when all ``maxit``
+        iterations ran (the same SpMV count as the two-kernel loop)."""
+        s = stream_handle()
+        pm = self.perm2
+        A = ctypes.byref(pm["A"].struct)
+        tm = ctypes.byref(pm["tile"]["struct"])
+        xp, rq = pm["xp"], pm["rq"]
+        call("ab_cg_tile_init", self.n, ptr(pm["perm"]), ptr(b), 1 if zero_b else 0, ptr(pm["fixed"]),
+             ptr(pm["s"]), ptr(d), ptr(xp), ptr(rq[0]), ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
+        it, apply = 0, 1 if maxit > 0 else 0
+        while it < maxit:
+            # kernel `it` forms r'_it (and x'_it), then the SpMV of iteration it
+            with self._m("K5_cg_tile_iter"):
+                call("ab_cg_tile_iter", A, tm, ptr(rq[it & 1]), ptr(rq[(it + 1) & 1]), ptr(xp), ptr(d),
+                     ptr(self.red), ptr(self.part), ptr(self.cnt), s)
+            if tol > 0 and it % check_every == 0:
+                rr, bb = float(self.red[1].item()), float(self.sc[1].item())
+                if bb == 0.0 or math.sqrt(rr / bb) <= tol:
+                    apply = 0  # r'_it converged: x'_it is the answer
+                    break
+            it += 1
+        call("ab_cg_tile_finish", self.n, ptr(pm["iperm"]), ptr(pm["s"]), ptr(xp), ptr(self.red), apply,
+             ptr(pm["x"]), s)
         return pm["x"], it
 
     def residual(self) -> float:

@@ -145,7 +145,8 @@ CG_VARIANTS = {
     "local": dict(),                        # local column map, node order
     "two-kernel": dict(resident=False),     # k_cg_spmv + k_cg_update per iteration
     "two-kernel-sfc": dict(order=True, resident=False, tile_rows=0),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC)
-    "two-kernel-sfc-tile": dict(order=True, resident=False, tile_rows=64),  # tiled SpMV, z in shared memory (default)
+    "two-kernel-sfc-tile": dict(order=True, resident=False, tile_rows=64),  # tiled SpMV, z in shared memory
+    "two-kernel-sfc-single": dict(order=True, resident=False, tile_rows=1024),  # tiled single pass (default form)
     "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False, compress_cols=False),  # z = D^-1 r form
     "two-kernel-sfc-diag": dict(order=True, resident=False, unit_diag=False),  # scaled, diagonal stored
 }
@@ -175,7 +176,8 @@ def test_pcg_fixed_iterations_and_convergence(name, variant):
     if variant in ("local-sfc", "local"):
         assert pcg.local is not None
     if pcg.perm2 is not None:
-        assert (pcg.perm2["tile"] is not None) == (variant == "two-kernel-sfc-tile")
+        assert (pcg.perm2["tile"] is not None) == (variant in ("two-kernel-sfc-tile", "two-kernel-sfc-single"))
+        assert pcg.perm2["single"] == (variant == "two-kernel-sfc-single")
     bt = torch.from_numpy(b).cuda()
     x, it = pcg.solve(bt.clone(), 7)
     xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 7)

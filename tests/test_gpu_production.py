@@ -123,9 +123,10 @@ def test_k2_full_c2(c2):
     assert rel_l2(got, ref) <= TOL_RHS
 
 
-@pytest.mark.parametrize("variant", ["resident-sfc", "two-kernel", "two-kernel-sfc", "two-kernel-sfc-tile"])
+@pytest.mark.parametrize("variant", ["resident-sfc", "two-kernel", "two-kernel-sfc", "two-kernel-sfc-tile",
+                                     "two-kernel-sfc-single"])
 def test_cg_full_c2_system(c2, variant):
-    """9 fixed Jacobi-PCG iterations on the full C2 Laplacian (705k rows)."""
+    """9 and 50 fixed Jacobi-PCG iterations on the full C2 Laplacian (705k rows)."""
     from paper_2005_05899_b200.device import DeviceMesh
     from paper_2005_05899_b200.solver import PCG, assemble_laplacian
     m, _u, _p, fixed = c2
@@ -136,7 +137,8 @@ def test_cg_full_c2_system(c2, variant):
     A = assemble_laplacian(dm, torch.from_numpy(fixed))
     kw = {"resident-sfc": dict(order=dm.node_order()), "two-kernel": dict(resident=False),
           "two-kernel-sfc": dict(order=dm.node_order(), resident=False, tile_rows=0),
-          "two-kernel-sfc-tile": dict(order=dm.node_order(), resident=False, tile_rows=2048)}[variant]  # ab_cg_spmv_tile
+          "two-kernel-sfc-tile": dict(order=dm.node_order(), resident=False, tile_rows=2048, single_pass=False),
+          "two-kernel-sfc-single": dict(order=dm.node_order(), resident=False, tile_rows=2048)}[variant]
     pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), **kw)
     if variant == "resident-sfc":
         lm = pcg.local
@@ -147,10 +149,13 @@ def test_cg_full_c2_system(c2, variant):
     else:
         assert not pcg.resident
         assert (m.n_nodes + 255) // 256 >= 20 * 64  # >= 20 groups in the grouped grid reduction
-    x, it = pcg.solve(torch.from_numpy(b).cuda(), 9, zero_b=False)
-    xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 9)
-    assert it == itr == 9
-    assert rel_l2(x.cpu().numpy(), xr) <= TOL_RHS
+    if variant.startswith("two-kernel-sfc-"):
+        assert pcg.perm2["tile"] is not None and pcg.perm2["single"] == (variant == "two-kernel-sfc-single")
+    for its in (9, 50):
+        x, it = pcg.solve(torch.from_numpy(b).cuda(), its, zero_b=False)
+        xr, itr, _ = fem.pcg(L, b, 1.0 / L.diagonal(), its)
+        assert it == itr == its
+        assert rel_l2(x.cpu().numpy(), xr) <= TOL_RHS
 
 
 def test_full_c2_step(c2):

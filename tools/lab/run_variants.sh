@@ -5,6 +5,6 @@ cmd=$1; shift
 cp paper_2005_05899_b200/libalyab200.so /tmp/lib_default.so
 for v in default "$@"; do
   if [ "$v" != default ]; then cp tools/lab/lib_$v.so paper_2005_05899_b200/libalyab200.so; else cp /tmp/lib_default.so paper_2005_05899_b200/libalyab200.so; fi
-  echo "== $v"; timeout 300 bash -c "$cmd" 2>&1 | tail -2
+  echo "== $v"; timeout 300 bash -c "$cmd" 2>&1 | tail -${TAIL:-2}
 done
 cp /tmp/lib_default.so paper_2005_05899_b200/libalyab200.so

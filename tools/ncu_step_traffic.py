@@ -26,6 +26,9 @@ NAMES = [  # (regex on the demangled kernel name, bench timeline label)
     (r"k_rk_stage", "K3_rk_stage"),
     (r"k_go_div", "K4_divergence"),
     (r"k_go_grad", "K67_grad_correct"),
+    (r"k_cg_tile_iter", "K5_cg_tile_iter"),
+    (r"k_cg_tile_init", "K5_cg_init"),
+    (r"k_cg_tile_finish", "K5_cg_finish"),
     (r"k_cg_spmv", "K5_cg_spmv"),
     (r"k_cg_update_scaled", "K5_cg_update_scaled"),
     (r"k_cg_update", "K5_cg_update"),

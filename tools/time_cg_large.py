@@ -6,7 +6,8 @@ first variant.
     python tools/time_cg_large.py [cells=200] [variants=two-pass,tile4096,...]
 
 variants: two-pass (ab_cg_spmv_unit + ab_cg_update_scaled), tile<R>
-(ab_cg_spmv_tile with R rows per tile + ab_cg_update_scaled).  The rejected
+(ab_cg_spmv_tile with R rows per tile + ab_cg_update_scaled), sptile<R> (the
+tiled single pass, ab_cg_tile_iter).  The rejected
 single-pass form is tools/lab/cg_single_pass.cu.
 """
 import sys
@@ -34,7 +35,7 @@ order = dm.node_order()
 del dm, m
 ref = None
 for name in names:
-    kw = dict(tile_rows=int(name[4:]) if name.startswith("tile") else 0)
+    kw = dict(tile_rows=int(name.split("tile")[1]) if "tile" in name else 0, single_pass=name.startswith("sp"))
     pcg = PCG(A, dinv, fixed=fixed, order=order, resident=False, **kw)
     info = ""
     if pcg.perm2.get("tile") is not None:
