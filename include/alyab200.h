@@ -596,6 +596,16 @@ typedef struct ab_ddcg2_rank {
   double* peer_recv[AB_PEER_MAX];     /* mapped */
   unsigned long long* peer_cnt[AB_PEER_MAX];  /* &peer.cnt_in[rank] (mapped) */
   double* peer_rec[AB_PEER_MAX];      /* &peer.rec[0] (mapped) */
+  /* optional tiled SpMV (tile_rows > 0; NULL/0: the plain SELL gather): the
+   * rows in tiles of tile_rows (1024, 2048 or 4096), per tile its ghost rows
+   * tghost[tghost_ptr[b] .. tghost_ptr[b+1]) and 16-bit tile-local columns
+   * tcols in the entry order of `cols` (ab_cg_spmv_tile's map); nsig and the
+   * peers' peer_nsig then count tiles: ceil(n_if / tile_rows) */
+  const uint16_t* tcols;
+  const int32_t* tghost_ptr;
+  const int32_t* tghost;
+  int32_t tile_rows;
+  int32_t tmax_ghost;
 } ab_ddcg2_rank;
 /* b (node order) -> r = b (fixed rows 0), z = D^-1 r, x = p = q = 0, and the
  * {r.z, r.r} record; b_zero (nullable) is zeroed.  tol is kept for the solve. */

@@ -78,7 +78,8 @@ class AbDdcg2Rank(C.Structure):
                                      "p", "q", "tif", "send_ptr", "send_peer", "send_off", "recv_ptr", "recv_rank",
                                      "recv_off", "recv", "cnt_in", "rec", "part", "cnt", "scal")]
                 + [("nsig", i32), ("scaled", i32), ("peer_rank", i32 * PEER_MAX), ("peer_nsig", i32 * PEER_MAX),
-                   ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX)])
+                   ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX),
+                   ("tcols", vp), ("tghost_ptr", vp), ("tghost", vp), ("tile_rows", i32), ("tmax_ghost", i32)])
 
 
 class AbMeshDesc(C.Structure):

@@ -15,7 +15,7 @@
 namespace ab {
 
 static_assert(sizeof(ab_peer_halo) == 272, "ab_peer_halo layout (mirrored by _lib.AbPeerHalo)");
-static_assert(sizeof(ab_ddcg2_rank) == 504, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
+static_assert(sizeof(ab_ddcg2_rank) == 536, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
 
 constexpr int kPeerBlock = 256;
 constexpr long long kPeerTimeoutNs = 10000000000ll;
@@ -269,10 +269,86 @@ __global__ void __launch_bounds__(kD2Block) k_d2_spmv(ab_ddcg2_rank d) {
       const double qi = fma(beta, d.q[i], az);
       d.p[i] = pi;
       d.q[i] = qi;
-      v[0] = d.own[i] * pi * qi;
+      v[0] = pi * qi;  // interior rows belong to this rank alone (own = 1)
     }
   }
   if ((int64_t)blockIdx.x * kD2Block < d.n_if) {  // a signalling block: its puts are complete
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < d.n_peers; ++q)
+        if (d.peer_nsig[q] > 0) red_rel_u64(d.peer_cnt[q], 1ull);
+    }
+  }
+  double tot[1];
+  if (grid_sum<1, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+    d.scal[AB_D2_PQI] = tot[0];
+    d.scal[AB_D2_BETA] = beta;
+    d.scal[AB_D2_RZ0 + (it & 1)] = rz_new;
+    d.scal[AB_D2_RR] = rr;
+    if (it == 0) d.scal[AB_D2_BB] = bb;
+  }
+}
+
+// Tiled form of k_d2_spmv (d.tile_rows > 0): CTA b owns rows [b R, (b+1) R),
+// stages z of its rows and ghost rows in shared memory and reads the slices
+// with 16-bit tile-local columns (ab_cg_spmv_tile's scheme); the tiles
+// holding interface rows come first and signal once their puts are done.
+__global__ void __launch_bounds__(kD2Block) k_d2_spmv_tile(ab_ddcg2_rank d) {
+  extern __shared__ __align__(16) double zs[];
+  __shared__ double sbuf[2 * 32];
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  const int it = (int)d.scal[AB_D2_IT];
+  double t2[2];
+  if (!d2_collect<2>(d, 1, d.scal[AB_D2_EPB], t2, sbuf, &sflag)) {
+    if (threadIdx.x == 0) { d.scal[AB_D2_FAIL] = 1.0; d.scal[AB_D2_DONE] = 1.0; }
+    return;
+  }
+  const double rz_new = t2[0], rr = t2[1];
+  const double bb = it == 0 ? rr : d.scal[AB_D2_BB];
+  const double tol = d.scal[AB_D2_TOL];
+  if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) {  // identical decision in every block and rank
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      d.scal[AB_D2_DONE] = 1.0;
+      d.scal[AB_D2_RR] = rr;
+      if (it == 0) d.scal[AB_D2_BB] = bb;
+    }
+    return;
+  }
+  const double rz_old = d.scal[AB_D2_RZ0 + ((it + 1) & 1)];
+  const double beta = it > 0 && rz_old != 0.0 ? rz_new / rz_old : 0.0;
+  const double* zv = d.scaled ? d.r : d.z;  // the scaled form gathers r' where Jacobi gathers z
+  const int R = d.tile_rows;
+  const int64_t row0 = (int64_t)blockIdx.x * R;
+  const int rows = (int)(d.n_rows - row0 < R ? d.n_rows - row0 : R);
+  for (int k = threadIdx.x; k < rows; k += kD2Block) zs[k] = __ldcg(zv + row0 + k);
+  const int g0 = d.tghost_ptr[blockIdx.x], ng = d.tghost_ptr[blockIdx.x + 1] - g0;
+  for (int k = threadIdx.x; k < ng; k += kD2Block) zs[R + k] = __ldcg(zv + __ldg(d.tghost + g0 + k));
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nsl = (rows + 31) >> 5;
+  double v[1] = {0.0};
+  for (int sl = warp; sl < nsl; sl += kD2Block / 32) {
+    const double az = sell_row_dot_smem<8>(d.slice_ptr + (row0 >> 5), d.tcols, d.vals, zs, sl, lane);
+    const int li = sl * 32 + lane;
+    if (li < rows) {
+      const int64_t i = row0 + li;
+      if (i < d.n_if) {
+        d.tif[i] = az;
+        for (int e = d.send_ptr[i]; e < d.send_ptr[i + 1]; ++e) d.peer_recv[d.send_peer[e]][d.send_off[e]] = az;
+      } else {
+        const double pi = fma(beta, d.p[i], zs[li]);
+        const double qi = fma(beta, d.q[i], az);
+        d.p[i] = pi;
+        d.q[i] = qi;
+        v[0] += pi * qi;  // interior rows belong to this rank alone (own = 1)
+      }
+    }
+  }
+  if (row0 < d.n_if) {  // a signalling tile: its puts are complete
     __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence_system();
@@ -360,21 +436,43 @@ __global__ void __launch_bounds__(kD2Block) k_d2_update(ab_ddcg2_rank d) {
   const double rz = d.scal[AB_D2_RZ0 + (it & 1)];
   const double alpha = t1[0] != 0.0 ? rz / t1[0] : 0.0;
   double v[2] = {0.0, 0.0};
-  const int64_t i = 2 * ((int64_t)blockIdx.x * kD2Block + threadIdx.x);
   const bool true_norm = d.scal[AB_D2_TOL] > 0.0;
-  for (int64_t k = i; k < i + 2 && k < d.n_rows; ++k) {
-    d.x[k] = fma(alpha, d.p[k], d.x[k]);
-    const double rk = fma(-alpha, d.q[k], d.r[k]);
-    d.r[k] = rk;
-    const double w = d.own[k];
-    if (d.scaled) {
-      v[0] += w * rk * rk;
-      v[1] += true_norm ? w * rk * rk / d.dinv[k] : w * rk * rk;
+  const int64_t n = d.n_rows;
+  // two rows per thread with 16-byte accesses, grid-stride (fewer blocks,
+  // so fewer record collections); interior rows have weight 1
+  for (int64_t k = (int64_t)blockIdx.x * kD2Block + threadIdx.x; 2 * k < n; k += (int64_t)gridDim.x * kD2Block) {
+    const int64_t i = 2 * k;
+    double rr2[2], w[2];
+    if (i + 1 < n) {
+      const double2 pv = *reinterpret_cast<const double2*>(d.p + i);
+      const double2 qv = *reinterpret_cast<const double2*>(d.q + i);
+      const double2 xv = *reinterpret_cast<const double2*>(d.x + i);
+      const double2 rv = *reinterpret_cast<const double2*>(d.r + i);
+      *reinterpret_cast<double2*>(d.x + i) = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+      rr2[0] = fma(-alpha, qv.x, rv.x);
+      rr2[1] = fma(-alpha, qv.y, rv.y);
+      *reinterpret_cast<double2*>(d.r + i) = make_double2(rr2[0], rr2[1]);
     } else {
-      const double zk = d.dinv[k] * rk;
-      d.z[k] = zk;
-      v[0] += w * rk * zk;
-      v[1] += w * rk * rk;
+      d.x[i] = fma(alpha, d.p[i], d.x[i]);
+      rr2[0] = fma(-alpha, d.q[i], d.r[i]);
+      d.r[i] = rr2[0];
+      rr2[1] = 0.0;
+    }
+    w[0] = i < d.n_if ? d.own[i] : 1.0;
+    w[1] = i + 1 < n ? (i + 1 < d.n_if ? d.own[i + 1] : 1.0) : 0.0;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (h == 1 && i + 1 >= n) break;
+      const double rk = rr2[h];
+      if (d.scaled) {
+        v[0] += w[h] * rk * rk;
+        v[1] += true_norm ? w[h] * rk * rk / d.dinv[i + h] : w[h] * rk * rk;
+      } else {
+        const double zk = d.dinv[i + h] * rk;
+        d.z[i + h] = zk;
+        v[0] += w[h] * rk * zk;
+        v[1] += w[h] * rk * rk;
+      }
     }
   }
   double tot[2];
@@ -448,6 +546,22 @@ int ab_ddcg2_init(const ab_ddcg2_rank* d, const double* b, double* b_zero, doubl
 
 int ab_ddcg2_spmv(const ab_ddcg2_rank* d, void* stream) {
   if (int rc = check_d2(d, "ab_ddcg2_spmv: incomplete descriptor")) return rc;
+  if (d->tile_rows > 0) {
+    const int64_t R = d->tile_rows;
+    if (R % 64 || !d->tcols || !d->tghost_ptr || !d->tghost || R + d->tmax_ghost > 65536)
+      return fail("ab_ddcg2_spmv: bad tile map (tile_rows % 64, tcols, tghost_ptr, tghost, R + max ghost <= 65536)");
+    if (d->nsig != (int32_t)((d->n_if + R - 1) / R)) return fail("ab_ddcg2_spmv: nsig must count tiles when tiled");
+    const size_t smem = (size_t)(R + d->tmax_ghost) * sizeof(double);
+    static size_t smem_set = 0;
+    if (smem > 48 * 1024 && smem > smem_set) {
+      if (cudaFuncSetAttribute(k_d2_spmv_tile, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+        return fail("ab_ddcg2_spmv: shared memory request rejected (tile too large)");
+      smem_set = smem;
+    }
+    const unsigned g = (unsigned)((d->n_rows + R - 1) / R);
+    k_d2_spmv_tile<<<g > 0 ? g : 1, kD2Block, smem, S(stream)>>>(*d);
+    return check_launch("ab_ddcg2_spmv");
+  }
   const unsigned g = grid_for(d->n_rows, kD2Block);
   k_d2_spmv<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d);
   return check_launch("ab_ddcg2_spmv");
@@ -464,7 +578,8 @@ int ab_ddcg2_iface(const ab_ddcg2_rank* d, void* stream) {
 
 int ab_ddcg2_update(const ab_ddcg2_rank* d, void* stream) {
   if (int rc = check_d2(d, "ab_ddcg2_update: incomplete descriptor")) return rc;
-  const unsigned g = grid_for((d->n_rows + 1) / 2, kD2Block);
+  unsigned g = grid_for((d->n_rows + 1) / 2, kD2Block);
+  if (g > 148u * 8u) g = 148u * 8u;  // grid-stride: 8 CTAs per SM
   k_d2_update<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d);
   return check_launch("ab_ddcg2_update");
 }

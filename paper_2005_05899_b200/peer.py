@@ -31,7 +31,7 @@ import numpy as np
 import torch
 
 from ._lib import PEER_MAX, AbDdcg2Rank, AbPeerHalo, call, lib, ptr, stream_handle
-from .solver import SellMatrix, permute_matrix
+from .solver import SellMatrix, cg_local_map, permute_matrix
 
 
 # ---------------------------------------------------------------------------
@@ -225,7 +225,7 @@ class DD2Rank:
 
     def __init__(self, rank: int, n_ranks: int, A: SellMatrix, dinv: torch.Tensor, own, shared: dict,
                  order: torch.Tensor, fixed: torch.Tensor | None = None, max_shared: int | None = None,
-                 scaled: bool = True):
+                 scaled: bool = True, tile_rows: int = 2048):
         dev = A.vals.device
         n = A.n_rows
         self.rank, self.n_ranks, self.n = rank, n_ranks, n
@@ -295,7 +295,16 @@ class DD2Rank:
         nb = (n + 255) // 256 + 1
         self.cnt = z((nb + 63) // 64 + 16, torch.int32)
         self.scal = z(16)
-        self.nsig = (self.n_if + 255) // 256
+        # tiled SpMV (k_d2_spmv_tile): z of a tile's rows and ghost rows in shared
+        # memory, 16-bit tile-local columns; signalling blocks are tiles then
+        self.tile = None
+        if tile_rows:
+            if tile_rows % 64:
+                raise ValueError("tile_rows must be a multiple of 64")
+            self.tile = cg_local_map(self.A, tile_rows, (n + tile_rows - 1) // tile_rows)
+        self.tile_rows = tile_rows if self.tile is not None else 0
+        blk = self.tile_rows or 256
+        self.nsig = (self.n_if + blk - 1) // blk
         self.x_node = z(n)
         self.peer = {}
         self._ipc = []
@@ -319,6 +328,9 @@ class DD2Rank:
             setattr(d, name, ptr(t))
         d.nsig = self.nsig
         d.scaled = 1 if self.scaled else 0
+        if self.tile is not None:
+            d.tcols, d.tghost_ptr, d.tghost = ptr(self.tile["cols"]), ptr(self.tile["ghost_ptr"]), ptr(self.tile["ghost"])
+            d.tile_rows, d.tmax_ghost = self.tile_rows, int(self.tile["max_ghost"])
         for k, q in enumerate(self.peers):
             d.peer_rank[k] = q
             d.peer_nsig[k] = int(peers[q]["nsig"]) if q in self.neighbors else 0
