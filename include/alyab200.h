@@ -560,7 +560,8 @@ int ab_peer_halo_grid(int32_t n_if);  /* the put kernel's CTA count for n_if int
 #define AB_D2_RR 11
 #define AB_D2_FAIL 12     /* sticky failure flag (1.0 = a peer wait timed out) */
 #define AB_D2_TOL 13
-#define AB_D2_NSCAL 16
+#define AB_D2_INT 16      /* single pass: this rank's interior dots of the current iteration, 16..20 */
+#define AB_D2_NSCAL 24
 typedef struct ab_ddcg2_rank {
   int64_t n_rows, n_if;
   int32_t rank, n_ranks;
@@ -606,6 +607,15 @@ typedef struct ab_ddcg2_rank {
   const int32_t* tghost;
   int32_t tile_rows;
   int32_t tmax_ghost;
+  /* single pass (single_pass != 0; scaled form and a tile map required):
+   * TWO launches per iteration, ab_ddcg2_tile_iter + ab_ddcg2_tile_iface,
+   * with x', p as 16-byte pairs xp[n][2] and r', q as pairs in the ping-pong
+   * buffers rq[0], rq[1] ([n][2] each; x, r, z, p, q unused).  init and
+   * finish follow the mode. */
+  double* xp;
+  double* rq[2];
+  int32_t single_pass;
+  int32_t pad_sp_;
 } ab_ddcg2_rank;
 /* b (node order) -> r = b (fixed rows 0), z = D^-1 r, x = p = q = 0, and the
  * {r.z, r.r} record; b_zero (nullable) is zeroed.  tol is kept for the solve. */
@@ -613,7 +623,19 @@ int ab_ddcg2_init(const ab_ddcg2_rank* d, const double* b, double* b_zero, doubl
 int ab_ddcg2_spmv(const ab_ddcg2_rank* d, void* stream);
 int ab_ddcg2_iface(const ab_ddcg2_rank* d, void* stream);
 int ab_ddcg2_update(const ab_ddcg2_rank* d, void* stream);
-/* x (row order) -> x_node[perm[i]] */
+/* Single-pass iteration (d->single_pass): tile_iter forms r' -= alpha q
+ * (own and ghost rows of each tile), x += alpha p, p = r' + beta p, q = A r'
+ * + beta q and the dots of the interior rows, and sends the interface rows'
+ * partial products; tile_iface waits for the neighbours' partials, forms the
+ * interface rows' q in global rank order, adds their ownership-weighted dots
+ * and publishes {r'.r', the ||r||^2 form, p.q, r'.q, q.q} to every rank
+ * (record sets alternate per iteration); beta from the three-dot recurrence
+ * of ab_cg_tile_iter.  The record array `rec` holds [2 sets][n_ranks][10]
+ * doubles in both modes. */
+int ab_ddcg2_tile_iter(const ab_ddcg2_rank* d, void* stream);
+int ab_ddcg2_tile_iface(const ab_ddcg2_rank* d, void* stream);
+/* x (row order) -> x_node[perm[i]] (single pass: x' + alpha p with alpha
+ * from the last published records unless the solve converged, scaled by s) */
 int ab_ddcg2_finish(const ab_ddcg2_rank* d, double* x_node, void* stream);
 /* doubles of `part` / uint32 of `cnt` the kernels need for n_rows */
 int64_t ab_ddcg2_part_size(int64_t n_rows);

@@ -79,7 +79,8 @@ class AbDdcg2Rank(C.Structure):
                                      "recv_off", "recv", "cnt_in", "rec", "part", "cnt", "scal")]
                 + [("nsig", i32), ("scaled", i32), ("peer_rank", i32 * PEER_MAX), ("peer_nsig", i32 * PEER_MAX),
                    ("peer_recv", vp * PEER_MAX), ("peer_cnt", vp * PEER_MAX), ("peer_rec", vp * PEER_MAX),
-                   ("tcols", vp), ("tghost_ptr", vp), ("tghost", vp), ("tile_rows", i32), ("tmax_ghost", i32)])
+                   ("tcols", vp), ("tghost_ptr", vp), ("tghost", vp), ("tile_rows", i32), ("tmax_ghost", i32),
+                   ("xp", vp), ("rq", vp * 2), ("single_pass", i32), ("pad_sp_", i32)])
 
 
 class AbMeshDesc(C.Structure):
@@ -110,6 +111,8 @@ _SIGS = {
     "ab_ddcg2_iface": ([P(AbDdcg2Rank), vp], C.c_int),
     "ab_ddcg2_update": ([P(AbDdcg2Rank), vp], C.c_int),
     "ab_ddcg2_finish": ([P(AbDdcg2Rank), vp, vp], C.c_int),
+    "ab_ddcg2_tile_iter": ([P(AbDdcg2Rank), vp], C.c_int),
+    "ab_ddcg2_tile_iface": ([P(AbDdcg2Rank), vp], C.c_int),
     "ab_ddcg2_part_size": ([i64], i64),
     "ab_version": ([], C.c_int),
     "ab_last_error": ([], C.c_char_p),

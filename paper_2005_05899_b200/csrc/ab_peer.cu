@@ -15,7 +15,7 @@
 namespace ab {
 
 static_assert(sizeof(ab_peer_halo) == 272, "ab_peer_halo layout (mirrored by _lib.AbPeerHalo)");
-static_assert(sizeof(ab_ddcg2_rank) == 536, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
+static_assert(sizeof(ab_ddcg2_rank) == 568, "ab_ddcg2_rank layout (mirrored by _lib.AbDdcg2Rank)");
 
 constexpr int kPeerBlock = 256;
 constexpr long long kPeerTimeoutNs = 10000000000ll;
@@ -133,17 +133,30 @@ __global__ void __launch_bounds__(kPeerBlock) k_halo_add(ab_peer_halo h, double*
 // ---------------------------------------------------------------------------
 constexpr int kD2Block = 256;
 constexpr int kD2IfGrid = 148;
+constexpr int kRecStride = 10;  // doubles per (set, rank) record: up to 5 {value, epoch} pairs
+
+// Grid-sum scratch: the row-parallel kernels (init, spmv, update, tile_iter:
+// <= 5 values over <= ceil(n/64) + 1 blocks, tiles of >= 64 rows) use the
+// front of `part` / `cnt`, the interface kernels the region behind it.
+__host__ __device__ inline int64_t d2_front_blocks(int64_t n) { return (n + 63) / 64 + 1; }
+__host__ __device__ inline int64_t d2_front_part(int64_t n) {
+  const int64_t nb = d2_front_blocks(n);
+  return 5 * (nb + (nb + kGroup - 1) / kGroup + 1) + 8;
+}
+__host__ __device__ inline int64_t d2_front_cnt(int64_t n) {
+  return 2 + (d2_front_blocks(n) + kGroup - 1) / kGroup;
+}
 
 // Record of `set` published by rank `src`: NV values into every rank's
 // record array (this rank's own included).
 template <int NV>
 __device__ __forceinline__ void d2_publish(const ab_ddcg2_rank& d, int set, const double (&v)[NV], double ep) {
   const int P = d.n_ranks;
-  double* dst0 = d.rec + ((size_t)set * P + d.rank) * 4;
+  double* dst0 = d.rec + ((size_t)set * P + d.rank) * kRecStride;
 #pragma unroll
   for (int k = 0; k < NV; ++k) st_rlx_f64(dst0 + 2 * k, v[k]);
   for (int q = 0; q < d.n_peers; ++q) {
-    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * 4;
+    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * kRecStride;
 #pragma unroll
     for (int k = 0; k < NV; ++k) st_rlx_f64(dst + 2 * k, v[k]);
   }
@@ -151,7 +164,7 @@ __device__ __forceinline__ void d2_publish(const ab_ddcg2_rank& d, int set, cons
 #pragma unroll
   for (int k = 0; k < NV; ++k) st_rel_f64(dst0 + 2 * k + 1, ep);
   for (int q = 0; q < d.n_peers; ++q) {
-    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * 4;
+    double* dst = d.peer_rec[q] + ((size_t)set * P + d.rank) * kRecStride;
 #pragma unroll
     for (int k = 0; k < NV; ++k) st_rel_f64(dst + 2 * k + 1, ep);
   }
@@ -164,7 +177,7 @@ __device__ __forceinline__ bool d2_collect(const ab_ddcg2_rank& d, int set, doub
                                            double* sbuf /* [NV * P] shared */, int* sflag) {
   const int P = d.n_ranks;
   if ((int)threadIdx.x < P) {
-    const double* rec = d.rec + ((size_t)set * P + threadIdx.x) * 4;
+    const double* rec = d.rec + ((size_t)set * P + threadIdx.x) * kRecStride;
     const long long t0 = peer_time();
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
@@ -403,9 +416,8 @@ __global__ void __launch_bounds__(kD2Block) k_d2_iface(ab_ddcg2_rank d) {
   }
   double tot[1];
   // (part/cnt behind the SpMV's: ab_ddcg2_part_size)
-  const int64_t nb_spmv = (d.n_rows + kD2Block - 1) / kD2Block;
-  double* part = d.part + 2 * (nb_spmv + (nb_spmv + kGroup - 1) / kGroup) + 8;
-  uint32_t* cnt = d.cnt + 2 + (nb_spmv + kGroup - 1) / kGroup;
+  double* part = d.part + d2_front_part(d.n_rows);
+  uint32_t* cnt = d.cnt + d2_front_cnt(d.n_rows);
   if (grid_sum<1, kD2Block>(v, part, cnt, tot) && threadIdx.x == 0) {
     d.scal[AB_D2_HEV] = hev + 1.0;
     if (failed) {
@@ -485,6 +497,234 @@ __global__ void __launch_bounds__(kD2Block) k_d2_update(ab_ddcg2_rank d) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Single-pass decomposed CG (d.single_pass, scaled form, tiled): TWO launches
+// per iteration instead of three.  k_d2_tile_iter forms r'_j = r'_{j-1} -
+// alpha q_{j-1} while staging the tile and its ghost rows (16-byte (r', q)
+// pairs, ping-pong), x_j, p_j for every row, q_j and the dots for the
+// interior rows, and the interface rows' partial products -> peers (their
+// q_{j-1} parked in the output pair); k_d2_tile_iface sums the interface
+// partials in rank order into q_j, adds the interface rows' weighted dots and
+// publishes {r'r', ||r||^2 form, p.q, r'.q, q.q} (record sets alternate
+// between iterations, so a set is rewritten only after every rank collected
+// it).  beta_{j-1} comes from the recurrence r'r'_j = r'r'_{j-1} - 2 alpha
+// r'.q_{j-1} + alpha^2 q.q_{j-1} (the single-domain ab_cg_tile_iter's
+// scheme); the finish adds the last alpha p unless the solve converged.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kD2Block) k_d2_init_sp(ab_ddcg2_rank d, const double* __restrict__ b, double tol) {
+  double v[2] = {0.0, 0.0};
+  double2* rq = reinterpret_cast<double2*>(d.rq[0]);
+  double2* xp = reinterpret_cast<double2*>(d.xp);
+  for (int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x; i < d.n_rows;
+       i += (int64_t)gridDim.x * kD2Block) {
+    double ri = b[d.perm[i]];
+    if (d.fixed && d.fixed[i]) ri = 0.0;
+    ri *= d.s[i];
+    const double w = i < d.n_if ? d.own[i] : 1.0;
+    v[0] += w * ri * ri;
+    v[1] += tol > 0.0 ? w * ri * ri / d.dinv[i] : w * ri * ri;
+    rq[i] = make_double2(ri, 0.0);
+    xp[i] = make_double2(0.0, 0.0);
+  }
+  double tot[2];
+  if (grid_sum<2, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+    const double ep = d.scal[AB_D2_EPOCH] + 1.0;
+    d.scal[AB_D2_EPOCH] = ep;
+    d.scal[AB_D2_EPB] = ep;
+    d.scal[AB_D2_IT] = 0.0;
+    d.scal[AB_D2_DONE] = 0.0;
+    d.scal[AB_D2_TOL] = tol;
+    const double rec[5] = {tot[0], tot[1], 0.0, 0.0, 0.0};  // alpha_{-1} = 0: the first iteration keeps x = 0
+    d2_publish<5>(d, 0, rec, ep);
+  }
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_tile_iter(ab_ddcg2_rank d) {
+  extern __shared__ __align__(16) double qs[];  // [R] q_{j-1} of the tile's rows, then zs
+  __shared__ double sbuf[5 * 32];
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  const int it = (int)d.scal[AB_D2_IT];
+  double t[5];
+  if (!d2_collect<5>(d, it & 1, d.scal[AB_D2_EPB], t, sbuf, &sflag)) {
+    if (threadIdx.x == 0) { d.scal[AB_D2_FAIL] = 1.0; d.scal[AB_D2_DONE] = 1.0; }
+    return;
+  }
+  const double RR = t[0], rr = t[1], PQ = t[2], RQ = t[3], QQ = t[4];
+  const double bb = it == 0 ? rr : d.scal[AB_D2_BB];
+  const double tol = d.scal[AB_D2_TOL];
+  if (tol > 0.0 && (bb == 0.0 || sqrt(rr / bb) <= tol)) {  // identical decision in every block and rank
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      d.scal[AB_D2_DONE] = 1.0;
+      d.scal[AB_D2_RR] = rr;
+      if (it == 0) d.scal[AB_D2_BB] = bb;
+    }
+    return;
+  }
+  const double alpha = PQ != 0.0 ? RR / PQ : 0.0;
+  double rr_next = fma(alpha, fma(alpha, QQ, -2.0 * RQ), RR);
+  if (rr_next < 0.0) rr_next = 0.0;
+  const double beta = RR != 0.0 ? rr_next / RR : 0.0;
+  const double2* rq_in = reinterpret_cast<const double2*>(d.rq[it & 1]);
+  double2* rq_out = reinterpret_cast<double2*>(d.rq[(it + 1) & 1]);
+  double2* xp = reinterpret_cast<double2*>(d.xp);
+  const int R = d.tile_rows;
+  double* zs = qs + R;
+  const bool true_norm = tol > 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  const int64_t n_tiles = (d.n_rows + R - 1) / R;
+  // persistent CTAs walk the tiles (the records are collected once per CTA)
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  const int64_t row0 = tile * R;
+  const int rows = (int)(d.n_rows - row0 < R ? d.n_rows - row0 : R);
+  __syncthreads();  // the previous tile's shared-memory reads are done
+  for (int li = threadIdx.x; li < rows; li += kD2Block) {
+    const double2 v = rq_in[row0 + li];
+    qs[li] = v.y;
+    zs[li] = fma(-alpha, v.y, v.x);
+  }
+  const int g0 = d.tghost_ptr[tile], ng = d.tghost_ptr[tile + 1] - g0;
+  for (int k = threadIdx.x; k < ng; k += kD2Block) {
+    const double2 gv = rq_in[__ldg(d.tghost + g0 + k)];
+    zs[R + k] = fma(-alpha, gv.y, gv.x);
+  }
+  __syncthreads();
+  const int nsl = (rows + 31) >> 5;
+  for (int sl = warp; sl < nsl; sl += kD2Block / 32) {
+    const double az = sell_row_dot_smem<8>(d.slice_ptr + (row0 >> 5), d.tcols, d.vals, zs, sl, lane);
+    const int li = sl * 32 + lane;
+    if (li < rows) {
+      const int64_t i = row0 + li;
+      const double ri = zs[li];
+      const double2 w = xp[i];
+      const double pi = fma(beta, w.y, ri);
+      xp[i] = make_double2(fma(alpha, w.y, w.x), pi);
+      if (i < d.n_if) {
+        d.tif[i] = az;
+        for (int e = d.send_ptr[i]; e < d.send_ptr[i + 1]; ++e) d.peer_recv[d.send_peer[e]][d.send_off[e]] = az;
+        rq_out[i] = make_double2(ri, qs[li]);  // q_{j-1} parked for k_d2_tile_iface
+      } else {
+        const double qi = fma(beta, qs[li], az);
+        rq_out[i] = make_double2(ri, qi);
+        v[0] += ri * ri;  // interior rows belong to this rank alone (own = 1)
+        v[1] += true_norm ? ri * ri / d.dinv[i] : ri * ri;
+        v[2] += pi * qi;
+        v[3] += ri * qi;
+        v[4] += qi * qi;
+      }
+    }
+  }
+  if (row0 < d.n_if) {  // a signalling tile: its puts are complete
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();
+      for (int q = 0; q < d.n_peers; ++q)
+        if (d.peer_nsig[q] > 0) red_rel_u64(d.peer_cnt[q], 1ull);
+    }
+  }
+  }
+  double tot[5];
+  if (grid_sum<5, kD2Block>(v, d.part, d.cnt, tot) && threadIdx.x == 0) {
+#pragma unroll
+    for (int k = 0; k < 5; ++k) d.scal[AB_D2_INT + k] = tot[k];
+    d.scal[AB_D2_BETA] = beta;
+    d.scal[AB_D2_RR] = rr;
+    if (it == 0) d.scal[AB_D2_BB] = bb;
+  }
+}
+
+__global__ void __launch_bounds__(kD2Block) k_d2_tile_iface(ab_ddcg2_rank d) {
+  __shared__ int sflag;
+  if (d.scal[AB_D2_DONE] != 0.0) return;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  const double hev = d.scal[AB_D2_HEV];
+  if ((int)threadIdx.x < d.n_peers && d.peer_nsig[threadIdx.x] > 0) {
+    const int q = d.peer_rank[threadIdx.x];
+    const unsigned long long want = (unsigned long long)(hev + 1.0) * (unsigned long long)d.peer_nsig[threadIdx.x];
+    const long long t0 = peer_time();
+    while (ld_acq_u64(d.cnt_in + q) < want) {
+      if (peer_time() - t0 > kPeerTimeoutNs) { sflag = 1; break; }
+    }
+  }
+  __syncthreads();
+  const bool failed = sflag != 0;
+  const double beta = d.scal[AB_D2_BETA];
+  const int it = (int)d.scal[AB_D2_IT];
+  double2* rq_out = reinterpret_cast<double2*>(d.rq[(it + 1) & 1]);
+  const double2* xp = reinterpret_cast<const double2*>(d.xp);
+  const bool true_norm = d.scal[AB_D2_TOL] > 0.0;
+  double v[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+  if (!failed) {
+    for (int64_t i = (int64_t)blockIdx.x * kD2Block + threadIdx.x; i < d.n_if; i += (int64_t)gridDim.x * kD2Block) {
+      const double own_t = d.tif[i];
+      double tsum = 0.0;
+      bool mine = false;
+      for (int e = d.recv_ptr[i]; e < d.recv_ptr[i + 1]; ++e) {
+        if (!mine && d.recv_rank[e] > d.rank) { tsum += own_t; mine = true; }
+        tsum += __ldcg(d.recv + d.recv_off[e]);
+      }
+      if (!mine) tsum += own_t;
+      const double2 rv = rq_out[i];
+      const double ri = rv.x;
+      const double qi = fma(beta, rv.y, tsum);
+      rq_out[i] = make_double2(ri, qi);
+      const double pi = xp[i].y;
+      const double w = d.own[i];
+      v[0] += w * ri * ri;
+      v[1] += true_norm ? w * ri * ri / d.dinv[i] : w * ri * ri;
+      v[2] += w * pi * qi;
+      v[3] += w * ri * qi;
+      v[4] += w * qi * qi;
+    }
+  }
+  double tot[5];
+  double* part = d.part + d2_front_part(d.n_rows);
+  uint32_t* cnt = d.cnt + d2_front_cnt(d.n_rows);
+  if (grid_sum<5, kD2Block>(v, part, cnt, tot) && threadIdx.x == 0) {
+    d.scal[AB_D2_HEV] = hev + 1.0;
+    if (failed) {
+      d.scal[AB_D2_FAIL] = 1.0;
+      d.scal[AB_D2_DONE] = 1.0;
+      return;
+    }
+    double rec[5];
+#pragma unroll
+    for (int k = 0; k < 5; ++k) rec[k] = d.scal[AB_D2_INT + k] + tot[k];
+    const double ep = d.scal[AB_D2_EPOCH] + 1.0;
+    d.scal[AB_D2_EPOCH] = ep;
+    d.scal[AB_D2_EPB] = ep;
+    d.scal[AB_D2_IT] = (double)(it + 1);
+    d2_publish<5>(d, (it + 1) & 1, rec, ep);
+  }
+}
+
+// x' + alpha_K p (the x update of the last iteration, alpha from the last
+// published record: every rank's totals, collected like the next iteration
+// would) unless the solve converged; out[perm[i]] = s_i x'_i.
+__global__ void __launch_bounds__(256) k_d2_finish_sp(ab_ddcg2_rank d, double* __restrict__ x_node) {
+  __shared__ double sbuf[5 * 32];
+  __shared__ int sflag;
+  if (threadIdx.x == 0) sflag = 0;
+  __syncthreads();
+  double alpha = 0.0;
+  if (d.scal[AB_D2_DONE] == 0.0 && d.scal[AB_D2_IT] > 0.0) {
+    double t[5];
+    if (d2_collect<5>(d, (int)d.scal[AB_D2_IT] & 1, d.scal[AB_D2_EPB], t, sbuf, &sflag))
+      alpha = t[2] != 0.0 ? t[0] / t[2] : 0.0;
+    else if (threadIdx.x == 0)
+      d.scal[AB_D2_FAIL] = 1.0;
+  }
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < d.n_rows) {
+    const double2 w = reinterpret_cast<const double2*>(d.xp)[i];
+    x_node[d.perm[i]] = d.s[i] * fma(alpha, w.y, w.x);
+  }
+}
+
 __global__ void k_d2_finish(ab_ddcg2_rank d, double* __restrict__ x_node) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < d.n_rows) x_node[d.perm[i]] = d.scaled ? d.s[i] * d.x[i] : d.x[i];
@@ -522,11 +762,8 @@ int ab_peer_halo_add(const ab_peer_halo* h, double* field, int32_t ncomp, int32_
 }
 
 int64_t ab_ddcg2_part_size(int64_t n_rows) {
-  const int64_t nb = (n_rows + kD2Block - 1) / kD2Block + 1;
-  const int64_t ng = (nb + kGroup - 1) / kGroup + 1;
-  // SpMV/update/init grid sums (<= 2 values over <= nb blocks) + the
-  // interface kernel's (1 value over kD2IfGrid blocks) behind them
-  return 2 * (nb + ng) + 8 + 2 * (kD2IfGrid + 4) + 8;
+  // front (row-parallel kernels) + the interface kernels' (5 values over <= kD2IfGrid blocks)
+  return d2_front_part(n_rows) + 5 * (kD2IfGrid + 4) + 8;
 }
 
 static int check_d2(const ab_ddcg2_rank* d, const char* what) {
@@ -535,9 +772,24 @@ static int check_d2(const ab_ddcg2_rank* d, const char* what) {
   return AB_OK;
 }
 
+static int check_sp(const ab_ddcg2_rank* d, const char* what) {
+  if (!d->scaled || d->tile_rows <= 0 || !d->xp || !d->rq[0] || !d->rq[1] || !d->s)
+    return fail(what);
+  if ((((uintptr_t)d->xp) | ((uintptr_t)d->rq[0]) | ((uintptr_t)d->rq[1])) & 15)
+    return fail("ddcg2 single pass: xp, rq must be 16-byte aligned");
+  return AB_OK;
+}
+
 int ab_ddcg2_init(const ab_ddcg2_rank* d, const double* b, double* b_zero, double tol, void* stream) {
   if (int rc = check_d2(d, "ab_ddcg2_init: incomplete descriptor")) return rc;
   const unsigned g = grid_for(d->n_rows, kD2Block);
+  if (d->single_pass) {
+    if (int rc = check_sp(d, "ab_ddcg2_init: single pass needs the scaled form, a tile map, xp and rq")) return rc;
+    k_d2_init_sp<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d, b, tol);
+    if (int rc = check_launch("ab_ddcg2_init")) return rc;
+    if (b_zero && d->n_rows > 0) k_d2_zero<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(d->n_rows, b_zero);
+    return check_launch("ab_ddcg2_init");
+  }
   k_d2_init<<<g > 0 ? g : 1, kD2Block, 0, S(stream)>>>(*d, b, b_zero, tol);
   if (int rc = check_launch("ab_ddcg2_init")) return rc;
   if (b_zero && d->n_rows > 0) k_d2_zero<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(d->n_rows, b_zero);
@@ -584,8 +836,51 @@ int ab_ddcg2_update(const ab_ddcg2_rank* d, void* stream) {
   return check_launch("ab_ddcg2_update");
 }
 
+int ab_ddcg2_tile_iter(const ab_ddcg2_rank* d, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_tile_iter: incomplete descriptor")) return rc;
+  if (int rc = check_sp(d, "ab_ddcg2_tile_iter: needs single_pass, the scaled form, a tile map, xp and rq")) return rc;
+  if (!d->single_pass) return fail("ab_ddcg2_tile_iter: descriptor not in single-pass mode");
+  const int64_t R = d->tile_rows;
+  if (R % 64 || !d->tcols || !d->tghost_ptr || !d->tghost || R + d->tmax_ghost > 65536)
+    return fail("ab_ddcg2_tile_iter: bad tile map");
+  if (d->nsig != (int32_t)((d->n_if + R - 1) / R)) return fail("ab_ddcg2_tile_iter: nsig must count tiles");
+  const size_t smem = (size_t)(2 * R + d->tmax_ghost) * sizeof(double);
+  static size_t smem_set = 0;
+  if (smem > 48 * 1024 && smem > smem_set) {
+    if (cudaFuncSetAttribute(k_d2_tile_iter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return fail("ab_ddcg2_tile_iter: shared memory request rejected (tile too large)");
+    smem_set = smem;
+  }
+  static int per_sm = 0;
+  if (!per_sm) {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_d2_tile_iter, kD2Block, smem);
+    if (per_sm < 1) per_sm = 1;
+  }
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int64_t g = (d->n_rows + R - 1) / R;
+  if (g > (int64_t)sms * per_sm) g = (int64_t)sms * per_sm;
+  k_d2_tile_iter<<<(unsigned)(g > 0 ? g : 1), kD2Block, smem, S(stream)>>>(*d);
+  return check_launch("ab_ddcg2_tile_iter");
+}
+
+int ab_ddcg2_tile_iface(const ab_ddcg2_rank* d, void* stream) {
+  if (int rc = check_d2(d, "ab_ddcg2_tile_iface: incomplete descriptor")) return rc;
+  if (!d->single_pass) return fail("ab_ddcg2_tile_iface: descriptor not in single-pass mode");
+  int g = (int)((d->n_if + kD2Block - 1) / kD2Block);
+  if (g < 1) g = 1;
+  if (g > kD2IfGrid) g = kD2IfGrid;
+  k_d2_tile_iface<<<g, kD2Block, 0, S(stream)>>>(*d);
+  return check_launch("ab_ddcg2_tile_iface");
+}
+
 int ab_ddcg2_finish(const ab_ddcg2_rank* d, double* x_node, void* stream) {
   if (int rc = check_d2(d, "ab_ddcg2_finish: incomplete descriptor")) return rc;
+  if (d->single_pass) {
+    if (d->n_rows > 0) k_d2_finish_sp<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(*d, x_node);
+    return check_launch("ab_ddcg2_finish");
+  }
   if (d->n_rows > 0) k_d2_finish<<<grid_for(d->n_rows, 256), 256, 0, S(stream)>>>(*d, x_node);
   return check_launch("ab_ddcg2_finish");
 }

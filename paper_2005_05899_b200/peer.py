@@ -225,7 +225,7 @@ class DD2Rank:
 
     def __init__(self, rank: int, n_ranks: int, A: SellMatrix, dinv: torch.Tensor, own, shared: dict,
                  order: torch.Tensor, fixed: torch.Tensor | None = None, max_shared: int | None = None,
-                 scaled: bool = True, tile_rows: int = 2048):
+                 scaled: bool = True, tile_rows: int = 2048, single_pass: bool = True):
         dev = A.vals.device
         n = A.n_rows
         self.rank, self.n_ranks, self.n = rank, n_ranks, n
@@ -290,11 +290,11 @@ class DD2Rank:
         self.tif = z(self.n_if)
         self.recv = z(n_ranks * self.M)
         self.cnt_in = z(n_ranks, torch.int64)
-        self.rec = torch.full((2 * n_ranks * 4,), -1.0, dtype=torch.float64, device=dev)
+        self.rec = torch.full((2 * n_ranks * 10,), -1.0, dtype=torch.float64, device=dev)
         self.part = z(int(lib().ab_ddcg2_part_size(n)))
-        nb = (n + 255) // 256 + 1
+        nb = (n + 63) // 64 + 1  # grid-sum counters: blocks of >= 64 rows (ab_ddcg2 kernels), then the interface kernels'
         self.cnt = z((nb + 63) // 64 + 16, torch.int32)
-        self.scal = z(16)
+        self.scal = z(24)
         # tiled SpMV (k_d2_spmv_tile): z of a tile's rows and ghost rows in shared
         # memory, 16-bit tile-local columns; signalling blocks are tiles then
         self.tile = None
@@ -305,6 +305,12 @@ class DD2Rank:
         self.tile_rows = tile_rows if self.tile is not None else 0
         blk = self.tile_rows or 256
         self.nsig = (self.n_if + blk - 1) // blk
+        # single pass (ab_ddcg2_tile_iter + ab_ddcg2_tile_iface: two launches per
+        # iteration, (x', p) and (r', q) as 16-byte pairs): scaled form on tiles
+        self.single_pass = bool(single_pass and self.scaled and self.tile is not None)
+        if self.single_pass:
+            pair = lambda: torch.zeros(max(1, n), 2, dtype=torch.float64, device=dev)  # noqa: E731
+            self.xp, self.rq = pair(), (pair(), pair())
         self.x_node = z(n)
         self.peer = {}
         self._ipc = []
@@ -331,6 +337,8 @@ class DD2Rank:
         if self.tile is not None:
             d.tcols, d.tghost_ptr, d.tghost = ptr(self.tile["cols"]), ptr(self.tile["ghost_ptr"]), ptr(self.tile["ghost"])
             d.tile_rows, d.tmax_ghost = self.tile_rows, int(self.tile["max_ghost"])
+        if self.single_pass:
+            d.xp, d.rq[0], d.rq[1], d.single_pass = ptr(self.xp), ptr(self.rq[0]), ptr(self.rq[1]), 1
         for k, q in enumerate(self.peers):
             d.peer_rank[k] = q
             d.peer_nsig[k] = int(peers[q]["nsig"]) if q in self.neighbors else 0
@@ -390,7 +398,9 @@ class DD2Solver:
             if tol > 0 and it % self.check_every == 0 and it > 0:
                 if float(self.ranks[0].scal[1].item()) != 0.0:
                     break
-            for fn in ("ab_ddcg2_spmv", "ab_ddcg2_iface", "ab_ddcg2_update"):
+            fns = (("ab_ddcg2_tile_iter", "ab_ddcg2_tile_iface") if self.ranks[0].single_pass
+                   else ("ab_ddcg2_spmv", "ab_ddcg2_iface", "ab_ddcg2_update"))
+            for fn in fns:
                 for r in self.ranks:
                     call(fn, C.byref(r.struct), s)
         for r in self.ranks:

@@ -62,7 +62,7 @@ def test_peer_halo_sum_rank_ordered(P):
     assert all(not h.failed() for h in halos)
 
 
-def _dd2_setup(P, spec=SPEC, scaled=True, tile_rows=2048):
+def _dd2_setup(P, spec=SPEC, scaled=True, tile_rows=2048, single_pass=True):
     from paper_2005_05899_b200.device import DeviceMesh
     from paper_2005_05899_b200.peer import DD2Rank, virtual_dd2
     from paper_2005_05899_b200.solver import assemble_laplacian
@@ -80,21 +80,24 @@ def _dd2_setup(P, spec=SPEC, scaled=True, tile_rows=2048):
         A = assemble_laplacian(dm, fl)
         dinv = torch.from_numpy(1.0 / dglob[plan.l2g]).cuda()
         ranks.append(DD2Rank(r, P, A, dinv, plan.own, plan.shared, dm.node_order(), fixed=fl, max_shared=ms,
-                             scaled=scaled, tile_rows=tile_rows))
+                             scaled=scaled, tile_rows=tile_rows, single_pass=single_pass))
     virtual_dd2(ranks)
     return L, fixed, locs, ranks
 
 
-@pytest.mark.parametrize("P,scaled,tile", [(2, True, 2048), (3, True, 2048), (4, True, 2048), (3, False, 2048),
-                                           (3, True, 64), (2, True, 0)])
-def test_dd2_cg_matches_single_domain(P, scaled, tile):
+@pytest.mark.parametrize("P,scaled,tile,single", [(2, True, 2048, True), (3, True, 2048, True), (4, True, 2048, True),
+                                                  (3, True, 64, True), (3, True, 2048, False), (3, True, 64, False),
+                                                  (3, False, 2048, False), (2, True, 0, False)])
+def test_dd2_cg_matches_single_domain(P, scaled, tile, single):
     """scaled: CG on D^-1/2 A D^-1/2 (default); False: the Jacobi z-form.
     tile: rows per tile of the tiled SpMV (64: several tiles, interface rows
-    spanning more than one; 0: the plain SELL gather)."""
+    spanning more than one; 0: the plain SELL gather).  single: the
+    two-launch single pass (default) or the three-launch form."""
     from paper_2005_05899_b200.peer import DD2Solver
-    L, fixed, locs, ranks = _dd2_setup(P, scaled=scaled, tile_rows=tile)
+    L, fixed, locs, ranks = _dd2_setup(P, scaled=scaled, tile_rows=tile, single_pass=single)
     assert all(r.n_if > 0 for r in ranks)
     assert all((r.tile is not None) == (tile > 0) for r in ranks)
+    assert all(r.single_pass == single for r in ranks)
     if tile == 64:
         assert all(r.nsig >= 2 and r.n > 2 * 64 for r in ranks)
     b = np.random.default_rng(11).standard_normal(L.shape[0])

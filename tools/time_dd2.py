@@ -58,7 +58,7 @@ if "--oracle" in sys.argv:  # the CPU oracle's iterate (slow): which of the GPU 
 parts, _, _ = sfc_partition(m, P, level=8)
 subs = [decompose(m, parts, P, r) for r in range(P)]
 ms = max([len(v) for _, pl in subs for v in pl.shared.values()] + [0])
-for tile in (0, 2048):
+for tile, single in ((0, False), (2048, False), (2048, True), (64, True)):
     ranks = []
     for r, (sub, plan) in enumerate(subs):
         sdm = DeviceMesh(sub)
@@ -66,7 +66,7 @@ for tile in (0, 2048):
         Ar = assemble_laplacian(sdm, fl)
         dinv = 1.0 / dglob[torch.from_numpy(plan.l2g).cuda()]
         ranks.append(DD2Rank(r, P, Ar, dinv, plan.own, plan.shared, sdm.node_order(), fixed=fl, max_shared=ms,
-                             tile_rows=tile))
+                             tile_rows=tile, single_pass=single))
     virtual_dd2(ranks)
     bs = [torch.from_numpy(b[plan.l2g]).cuda() for _, plan in subs]
     solver = DD2Solver(ranks)
@@ -74,7 +74,7 @@ for tile in (0, 2048):
     xs, _ = solver.solve(bs, its, zero_b=False)
     err = max(np.linalg.norm(x.cpu().numpy() - ref[pl.l2g]) / np.linalg.norm(ref[pl.l2g])
               for x, (_, pl) in zip(xs, subs))
-    print(f"P={P} virtual ranks, tile_rows={tile}: {t:.2f} us/iteration (interface rows "
+    print(f"P={P} virtual ranks, tile_rows={tile}, single_pass={single}: {t:.2f} us/iteration (interface rows "
           f"{[r.n_if for r in ranks]}), max rel diff vs single domain {err:.1e}", flush=True)
     del ranks, solver
     torch.cuda.empty_cache()
