@@ -188,7 +188,11 @@ def test_ordered_wall_traction_reproducible():
 
 def test_colour_wall_model_steps_repeat_bitwise():
     """Mixed tet/prism/pyramid/hex mesh with the wall model: colour scatter +
-    ordered K8 -> the full step is bitwise repeatable and matches the oracle."""
+    ordered K8 -> the full step is bitwise repeatable and matches the oracle.
+    The pressure solves run 150 fixed iterations (converged on this
+    1600-node system): with 40 the unconverged iterate amplifies the
+    rounding of the (atomically assembled) Laplacian and gradient operator to
+    ~1e-8 between solver instances, which is noise, not a scatter property."""
     from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
     m = meshgen.c3_mesh(0.06)
     bc, wall = meshgen.wall_model_bcs(m)
@@ -202,8 +206,8 @@ def test_colour_wall_model_steps_repeat_bitwise():
         fs.set_state(u, p)
         for _ in range(2):
             if rep == 0:
-                st = ora.step(st, 2e-3, cg_iters=40)
-            fs.step(2e-3, cg_iters=40, graph=True)
+                st = ora.step(st, 2e-3, cg_iters=150)
+            fs.step(2e-3, cg_iters=150, graph=True)
         torch.cuda.synchronize()
         runs.append((fs.u.cpu().numpy().copy(), fs.p.cpu().numpy().copy()))
     assert rel_l2(runs[0][0], st["u"]) <= TOL_STATE
