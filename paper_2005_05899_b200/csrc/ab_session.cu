@@ -11,9 +11,10 @@
 //
 // Setup choices that only change rounding (the bank-aware tet node order and
 // the bank-spread reference order of device.py) are not applied here; the
-// pressure solve is the two-kernel Jacobi-PCG on P L P^T in the Hilbert order
+// pressure solve is the tiled single-pass CG on D^-1/2 P L P^T D^-1/2 in the Hilbert order (two-kernel Jacobi-PCG on P L P^T if a tile map does not fit 16 bits)
 // of the nodes (the path of every system too large for the on-chip solver).
 #include <thrust/binary_search.h>
+#include <thrust/copy.h>
 #include <thrust/device_ptr.h>
 #include <thrust/execution_policy.h>
 #include <thrust/iterator/counting_iterator.h>
@@ -175,6 +176,81 @@ __global__ void k_slice_width(int64_t n, const int64_t* __restrict__ rp, int64_t
   for (int64_t i = 32 * s; i < 32 * s + 32 && i < n; ++i) w = max(w, rp[i + 1] - rp[i]);
   w32[s] = 32 * w;
 }
+// Unit-diagonal scaled system for the tiled single-pass CG: per-row count of
+// the off-diagonal entries, then their compaction (same order).
+__global__ void k_count_offdiag(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                                int64_t* __restrict__ cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t c = 0;
+  for (int64_t k = rp[i]; k < rp[i + 1]; ++k) c += cols[k] != i;
+  cnt[i] = c;
+}
+__global__ void k_compact_offdiag(int64_t n, const int64_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                                  const double* __restrict__ v, const int64_t* __restrict__ rp2,
+                                  int32_t* __restrict__ cols2, double* __restrict__ v2) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int64_t o = rp2[i];
+  for (int64_t k = rp[i]; k < rp[i + 1]; ++k)
+    if (cols[k] != i) {
+      cols2[o] = cols[k];
+      v2[o++] = v[k];
+    }
+}
+__global__ void k_sqrt(int64_t n, const double* __restrict__ a, double* __restrict__ b) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) b[i] = sqrt(a[i]);
+}
+// Tile map of a SELL-32 matrix (solver.cg_local_map): row i's entries; an own-
+// tile column gets its local index, a remote one a key tile * n + col.
+__global__ void k_tile_keys(int64_t n, int64_t R, const int64_t* __restrict__ sp, const int32_t* __restrict__ scol,
+                            uint16_t* __restrict__ lcol, int64_t* __restrict__ key) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = i >> 5, t = i / R, r0 = t * R;
+  const int64_t b = sp[s] + (i & 31), w = (sp[s + 1] - sp[s]) >> 5;
+  for (int64_t j = 0; j < w; ++j) {
+    const int64_t e = b + 32 * j;
+    const int64_t c = scol[e];
+    if (c >= r0 && c < r0 + R) {
+      lcol[e] = (uint16_t)(c - r0);
+      key[e] = -1;
+    } else {
+      key[e] = t * n + c;
+    }
+  }
+}
+__global__ void k_tile_ghost_cols(int64_t n, int64_t R, const int64_t* __restrict__ sp, const int64_t* __restrict__ key,
+                                  const int64_t* __restrict__ gkeys, int64_t ng, const int32_t* __restrict__ gptr,
+                                  uint16_t* __restrict__ lcol) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int64_t s = i >> 5, t = i / R;
+  const int64_t b = sp[s] + (i & 31), w = (sp[s + 1] - sp[s]) >> 5;
+  for (int64_t j = 0; j < w; ++j) {
+    const int64_t e = b + 32 * j;
+    const int64_t k = key[e];
+    if (k < 0) continue;
+    int64_t lo = 0, hi = ng;  // first gkey >= k (present)
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (gkeys[mid] < k) lo = mid + 1; else hi = mid;
+    }
+    lcol[e] = (uint16_t)(R + (lo - gptr[t]));
+  }
+}
+__global__ void k_ghost_split(int64_t ng, int64_t n, const int64_t* __restrict__ gkeys, int32_t* __restrict__ ghost,
+                              int64_t* __restrict__ gtile) {
+  const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= ng) return;
+  ghost[g] = (int32_t)(gkeys[g] % n);
+  gtile[g] = gkeys[g] / n;
+}
+struct IsRemote {
+  __host__ __device__ bool operator()(int64_t k) const { return k >= 0; }
+};
+
 __global__ void k_set_diag_fixed(int64_t n, const uint8_t* __restrict__ fixed, double* __restrict__ d) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n && fixed[i]) d[i] = 1.0;
@@ -235,6 +311,13 @@ struct ab_ctx {
   double* dinv_p = nullptr;
   uint8_t* fixed_p = nullptr;
   double *x = nullptr, *r = nullptr, *z = nullptr, *p = nullptr, *q = nullptr, *xn = nullptr;
+  // tiled single-pass CG (ab_cg_tile_*): A' = S P L P^T S without its unit
+  // diagonal, 2048-row tile map, (x', p) and (r', q) pairs
+  bool tiled = false;
+  ab_sell Lu{};
+  ab_cg_local tmap{};
+  int64_t* iperm = nullptr;
+  double *s_p = nullptr, *xp = nullptr, *rq[2] = {nullptr, nullptr};
   double *red = nullptr, *sc = nullptr, *part = nullptr;
   uint32_t* cnt = nullptr;
   // state
@@ -330,6 +413,76 @@ int to_sell(ab_ctx* c, int64_t n, const int64_t* rp, const int32_t* cols, const 
   *sval_out = sval;
   if (stored) *stored = total;
   return AB_OK;
+}
+
+// Tiled single-pass CG setup (solver.PCG's default large-system form):
+// A' = S P L P^T S (S = D^-1/2) without its unit diagonal, its 2048-row tile
+// map (16-bit tile-local columns, per-tile ghost rows) and the pair vectors.
+// Leaves c->tiled false (the plain two-kernel form runs) when a tile's rows
+// and ghosts exceed 16 bits.
+constexpr int64_t kTileRows = 2048;
+int build_tiled_cg(ab_ctx* c, int64_t n, const int64_t* rp, const int32_t* cols, const double* v, int64_t* iperm) {
+  int64_t* cnt = c->alloc<int64_t>(n + 1);
+  if (!cnt) return fail("ab_mesh_upload: device memory exhausted");
+  k_count_offdiag<<<g256(n), 256, 0, c->st>>>(n, rp, cols, cnt + 1);
+  thrust::inclusive_scan(thrust::cuda::par.on(c->st), cnt + 1, cnt + 1 + n, cnt + 1);  // cnt[0] = 0 (alloc zeroes)
+  int64_t m = 0;
+  cudaMemcpyAsync(&m, cnt + n, 8, cudaMemcpyDeviceToHost, c->st);
+  cudaStreamSynchronize(c->st);
+  int32_t* cols2 = c->alloc<int32_t>(m);
+  double* v2 = c->alloc<double>(m);
+  if (!cols2 || !v2) return fail("ab_mesh_upload: device memory exhausted");
+  k_compact_offdiag<<<g256(n), 256, 0, c->st>>>(n, rp, cols, v, cnt, cols2, v2);
+  int64_t* sp = nullptr;
+  int32_t* scol = nullptr;
+  double* sv = nullptr;
+  int64_t stored = 0;
+  AB_TRY(to_sell(c, n, cnt, cols2, v2, &sp, &scol, &sv, nullptr, &stored));
+  AB_ALLOC(c->s_p, double, n);
+  k_sqrt<<<g256(n), 256, 0, c->st>>>(n, c->dinv_p, c->s_p);
+  c->Lu = ab_sell{n, (n + 31) / 32, 0, sp, scol, sv};
+  AB_TRY(ab_sell_symscale(&c->Lu, c->s_p, c->st));
+  // tile map
+  const int64_t R = kTileRows, n_t = (n + R - 1) / R;
+  uint16_t* lcol = c->alloc<uint16_t>(stored);
+  int64_t* key = c->alloc<int64_t>(stored);
+  if (!lcol || !key) return fail("ab_mesh_upload: device memory exhausted");
+  k_tile_keys<<<g256(n), 256, 0, c->st>>>(n, R, sp, scol, lcol, key);
+  int64_t* gk = c->alloc<int64_t>(stored);
+  if (!gk) return fail("ab_mesh_upload: device memory exhausted");
+  int64_t* gend = thrust::copy_if(thrust::cuda::par.on(c->st), key, key + stored, gk, IsRemote{});
+  int64_t ng = gend - gk;
+  thrust::sort(thrust::cuda::par.on(c->st), gk, gk + ng);
+  ng = thrust::unique(thrust::cuda::par.on(c->st), gk, gk + ng) - gk;
+  int32_t* ghost = c->alloc<int32_t>(ng > 0 ? ng : 1);
+  int64_t* gtile = c->alloc<int64_t>(ng > 0 ? ng : 1);
+  int64_t* gptr64 = c->alloc<int64_t>(n_t + 1);
+  int32_t* gptr = c->alloc<int32_t>(n_t + 1);
+  if (!ghost || !gtile || !gptr64 || !gptr) return fail("ab_mesh_upload: device memory exhausted");
+  if (ng > 0) k_ghost_split<<<g256(ng), 256, 0, c->st>>>(ng, n, gk, ghost, gtile);
+  thrust::lower_bound(thrust::cuda::par.on(c->st), gtile, gtile + ng, thrust::counting_iterator<int64_t>(0),
+                      thrust::counting_iterator<int64_t>(n_t + 1), gptr64);
+  thrust::copy(thrust::cuda::par.on(c->st), gptr64, gptr64 + n_t + 1, gptr);
+  std::vector<int64_t> hp(n_t + 1);
+  cudaMemcpyAsync(hp.data(), gptr64, 8 * (n_t + 1), cudaMemcpyDeviceToHost, c->st);
+  cudaStreamSynchronize(c->st);
+  int64_t max_ghost = 0;
+  for (int64_t t = 0; t < n_t; ++t) max_ghost = hp[t + 1] - hp[t] > max_ghost ? hp[t + 1] - hp[t] : max_ghost;
+  if (R + max_ghost > 65536) return check_launch("ab_mesh_upload");  // stays on the plain two-kernel form
+  k_tile_ghost_cols<<<g256(n), 256, 0, c->st>>>(n, R, sp, key, gk, ng, gptr, lcol);
+  c->tmap = ab_cg_local{};
+  c->tmap.rows_per_cta = R;
+  c->tmap.n_cta = (int32_t)n_t;
+  c->tmap.max_ghost = (int32_t)max_ghost;
+  c->tmap.cols = lcol;
+  c->tmap.ghost_ptr = gptr;
+  c->tmap.ghost = ghost;
+  AB_ALLOC(c->xp, double, 2 * n);
+  AB_ALLOC(c->rq[0], double, 2 * n);
+  AB_ALLOC(c->rq[1], double, 2 * n);
+  c->iperm = iperm;
+  c->tiled = true;
+  return check_launch("ab_mesh_upload");
 }
 
 int build_windows(ab_ctx* c, int k, int64_t ne, int nn) {
@@ -587,6 +740,7 @@ int ab_mesh_upload(ab_ctx* c, const ab_mesh_desc* d) {
     k_gather_u8<<<g256(n), 256, 0, c->st>>>(n, fixed, c->perm, c->fixed_p);
     if (any_fixed) k_set_diag_fixed<<<g256(n), 256, 0, c->st>>>(n, c->fixed_p, diag);
     AB_TRY(ab_reciprocal(n, diag, c->dinv_p, c->st));
+    AB_TRY(build_tiled_cg(c, n, rp2, cols2, v2, iperm));
   }
   // CG workspace (two-kernel form: grouped grid reductions)
   const int64_t nb = (n + 255) / 256 + 1;
@@ -599,7 +753,7 @@ int ab_mesh_upload(ab_ctx* c, const ab_mesh_desc* d) {
   AB_ALLOC(c->xn, double, n);
   AB_ALLOC(c->red, double, 8);
   AB_ALLOC(c->sc, double, 8);
-  AB_ALLOC(c->part, double, 2 * (nb + ng) + 8);
+  AB_ALLOC(c->part, double, 5 * (nb + ng) + 8);
   AB_ALLOC(c->cnt, uint32_t, ng + 2);
   // state
   AB_ALLOC(c->U0, double, 4 * n);
@@ -705,14 +859,24 @@ int ab_step(ab_ctx* c, double dt, int32_t cg_iters, void* stream) {
     AB_TRY(apply_bc(c, c->U, s));
   }
   AB_TRY(ab_gradop_div(&c->B3, c->U, -c->phys.rho / dt, c->Bv, s));  // K4: b = -(rho/dt) D u_3
-  // K5: Jacobi-PCG on P L P^T (b gathered in, x scattered out)
-  AB_TRY(ab_cg_init_perm(n, c->perm, c->Bv, 1, c->fixed_p, c->dinv_p, c->x, c->r, c->z, c->p, c->q, c->red, c->sc,
-                         c->part, c->cnt, s));
-  for (int it = 0; it < cg_iters; ++it) {
-    AB_TRY(ab_cg_spmv(&c->Lp, c->z, c->p, c->q, nullptr, 1, nullptr, c->red, c->sc, c->part, c->cnt, s));
-    AB_TRY(ab_cg_update(n, c->p, c->q, c->dinv_p, c->x, c->r, c->z, nullptr, c->red, c->sc, c->part, c->cnt, s));
+  if (c->tiled) {
+    // K5: tiled single-pass CG on S P L P^T S (= Jacobi-PCG), one kernel per iteration
+    AB_TRY(ab_cg_tile_init(n, c->perm, c->Bv, 1, c->fixed_p, c->s_p, nullptr, c->xp, c->rq[0], c->red, c->sc,
+                           c->part, c->cnt, s));
+    for (int it = 0; it < cg_iters; ++it)
+      AB_TRY(ab_cg_tile_iter(&c->Lu, &c->tmap, c->rq[it & 1], c->rq[(it + 1) & 1], c->xp, nullptr, c->red, c->part,
+                             c->cnt, s));
+    AB_TRY(ab_cg_tile_finish(n, c->iperm, c->s_p, c->xp, c->red, cg_iters > 0 ? 1 : 0, c->xn, s));
+  } else {
+    // K5: Jacobi-PCG on P L P^T (b gathered in, x scattered out)
+    AB_TRY(ab_cg_init_perm(n, c->perm, c->Bv, 1, c->fixed_p, c->dinv_p, c->x, c->r, c->z, c->p, c->q, c->red, c->sc,
+                           c->part, c->cnt, s));
+    for (int it = 0; it < cg_iters; ++it) {
+      AB_TRY(ab_cg_spmv(&c->Lp, c->z, c->p, c->q, nullptr, 1, nullptr, c->red, c->sc, c->part, c->cnt, s));
+      AB_TRY(ab_cg_update(n, c->p, c->q, c->dinv_p, c->x, c->r, c->z, nullptr, c->red, c->sc, c->part, c->cnt, s));
+    }
+    AB_TRY(ab_perm_scatter(n, c->perm, c->x, c->xn, s));
   }
-  AB_TRY(ab_perm_scatter(n, c->perm, c->x, c->xn, s));
   // K6 + K7: u = u_3 - dt/rho M^-1 B dp; p += dp; Gp += B dp
   AB_TRY(ab_gradop_correct(&c->B3, c->xn, k, c->U, c->U0, c->minv, c->P, c->GP, s));
   AB_TRY(apply_bc(c, c->U0, s));
