@@ -251,7 +251,7 @@ int ab_perm_scatter(int64_t n, const int64_t* perm, const double* in, double* ou
  * D^-1/2 r playing z's role, so per iteration neither z nor D^-1 moves (16
  * bytes per row less).  ab_sell_symscale: vals *= s_row s_col (s = d^-1/2,
  * row order, on a copy the caller owns); init: r'_i = s_i b[perm[i]];
- * the SpMV is ab_cg_spmv / ab_cg_spmv16 with z := r'; update: x' += alpha p,
+ * the SpMV is ab_cg_spmv with z := r'; update: x' += alpha p,
  * r' -= alpha q, red[RZN] = r'.r', red[RR] = sum d r'^2 (d non-NULL, when a
  * tolerance is tested) or r'.r'; finish: out[j] = s_i x'_i, i = iperm[j]
  * (the inverse permutation: coalesced writes). */
@@ -270,28 +270,6 @@ int ab_cg_finish_scaled(int64_t n, const int64_t* iperm, const double* s, const 
                         void* stream);
 int ab_cg_spmv(const ab_sell* a, const double* z, double* p, double* q, double* t, int32_t with_dot,
                const double* own, double* red, double* sc, double* part, uint32_t* cnt, void* stream);
-/* Column-compressed SELL-32 for the single-domain two-kernel CG: the same
- * slices, values and entry order as an ab_sell; slice s keeps its columns
- * as uint16 offsets from cbase[s] when they span < 65536 rows (int32 and
- * cbase[s] = -1 otherwise), at byte offset cptr[s] of `cols` (16-byte
- * aligned).  In the Hilbert row order most slices qualify, which cuts the
- * column stream - a third of the matrix bytes - nearly in half.
- * ab_sell16_plan: cbase and per-slice byte counts from an ab_sell; the
- * caller scans the counts into cptr; ab_sell16_fill writes the columns.
- * ab_cg_spmv16 = ab_cg_spmv(with_dot = 1, own = NULL), bitwise the same. */
-typedef struct ab_sell16 {
-  int64_t n_rows;
-  int64_t n_slices;
-  const int64_t* slice_ptr;
-  const int64_t* cptr;
-  const int32_t* cbase;
-  const unsigned char* cols;
-  const double* vals;
-} ab_sell16;
-int ab_sell16_plan(const ab_sell* a, int32_t* cbase, int64_t* bytes, void* stream);
-int ab_sell16_fill(const ab_sell* a, const int32_t* cbase, const int64_t* cptr, unsigned char* cols, void* stream);
-int ab_cg_spmv16(const ab_sell16* a, const double* z, double* p, double* q, double* red, double* sc, double* part,
-                 uint32_t* cnt, void* stream);
 int ab_cg_dot(int64_t n, const double* z, const double* t, double* p, double* q, const double* own, double* red,
               double* sc, double* part, uint32_t* cnt, void* stream);
 int ab_cg_update(int64_t n, const double* p, const double* q, const double* dinv, double* x, double* r, double* z,

@@ -38,11 +38,6 @@ class AbSell(C.Structure):
                 ("vals", vp)]
 
 
-class AbSell16(C.Structure):
-    _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cptr", vp), ("cbase", vp), ("cols", vp),
-                ("vals", vp)]
-
-
 class AbSell3(C.Structure):
     _fields_ = [("n_rows", i64), ("n_slices", i64), ("slice_ptr", vp), ("cols", vp), ("vx", vp), ("vy", vp),
                 ("vz", vp)]
@@ -137,7 +132,6 @@ _SIGS = {
     "ab_sell_spmv": ([P(AbSell), vp, vp, vp], C.c_int),
     "ab_cg_init": ([i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_set_bb": ([vp, vp, vp], C.c_int),
-    "ab_sell16_plan": ([P(AbSell), vp, vp, vp], C.c_int),
     "ab_sell_symscale": ([P(AbSell), vp, vp], C.c_int),
     "ab_cg_spmv_unit": ([P(AbSell), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_init_scaled": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
@@ -147,8 +141,6 @@ _SIGS = {
     "ab_cg_tile_init": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_tile_iter": ([P(AbSell), P(AbCgLocal), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_tile_finish": ([i64, vp, vp, vp, vp, i32, vp, vp], C.c_int),
-    "ab_sell16_fill": ([P(AbSell), vp, vp, vp, vp], C.c_int),
-    "ab_cg_spmv16": ([P(AbSell16), vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_cg_init_perm": ([i64, vp, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp], C.c_int),
     "ab_perm_scatter": ([i64, vp, vp, vp, vp], C.c_int),
     "ab_cg_spmv": ([P(AbSell), vp, vp, vp, vp, i32, vp, vp, vp, vp, vp, vp], C.c_int),

@@ -95,53 +95,6 @@ __device__ __forceinline__ double sell_row_dot(const int64_t* __restrict__ sp, c
   return acc;
 }
 
-// The same row product on the column-compressed SELL (ab_sell16): slice s
-// stores its columns as 16-bit offsets from cbase[s] when they span < 64k
-// rows, else as int32 (cbase[s] = -1); the branch is uniform per warp (one
-// slice = one warp) and the FMA order is sell_row_dot's, so the result is
-// bitwise the same.
-#ifndef SPMV16_CHUNK
-#define SPMV16_CHUNK 16
-#endif
-template <bool NEAR>
-__device__ __forceinline__ double sell16_row_body(const unsigned char* __restrict__ cb, int64_t cofs, int cbase,
-                                                  const double* __restrict__ sval, int64_t base, int lane, int width,
-                                                  const double* zv) {
-  constexpr int CH = SPMV16_CHUNK;
-  double acc = 0.0;
-  for (int j0 = 0; j0 < width; j0 += CH) {
-    int c[CH];
-    double a[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) {
-      const bool ok = j0 + u < width;
-      const int64_t k = (int64_t)(j0 + u) * 32 + lane;
-      if constexpr (NEAR)
-        c[u] = ok ? cbase + (int)__ldcs(reinterpret_cast<const uint16_t*>(cb + cofs) + k) : 0;
-      else
-        c[u] = ok ? __ldcs(reinterpret_cast<const int32_t*>(cb + cofs) + k) : 0;
-      a[u] = ok ? __ldcs(sval + base + (int64_t)(j0 + u) * 32) : 0.0;
-    }
-    double g[CH];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) g[u] = zv[c[u]];
-#pragma unroll
-    for (int u = 0; u < CH; ++u) acc = fma(a[u], g[u], acc);
-  }
-  return acc;
-}
-
-__device__ __forceinline__ double sell16_row_dot(const int64_t* __restrict__ sp, const int64_t* __restrict__ cptr,
-                                                 const int32_t* __restrict__ cbase, const unsigned char* __restrict__ cb,
-                                                 const double* __restrict__ sval, const double* zv, int64_t i) {
-  const int64_t s = i >> 5;
-  const int lane = (int)(i & 31);
-  const int64_t base = sp[s] + lane;
-  const int width = (int)((sp[s + 1] - sp[s]) >> 5);
-  const int b = cbase[s];
-  if (b >= 0) return sell16_row_body<true>(cb, cptr[s], b, sval, base, lane, width, zv);
-  return sell16_row_body<false>(cb, cptr[s], 0, sval, base, lane, width, zv);
-}
 
 // Replicated per-CTA partials (resident solvers): the NV values of CTA b are
 // written to kRep copies of a [NV][nbp] table (nbp = nb rounded up to 4),

@@ -22,7 +22,7 @@ from dataclasses import dataclass
 
 import torch
 
-from ._lib import AbCgLocal, AbSell, AbSell3, AbSell16, call, lib, ptr, stream_handle
+from ._lib import AbCgLocal, AbSell, AbSell3, call, lib, ptr, stream_handle
 from .device import DeviceMesh
 
 
@@ -175,27 +175,6 @@ def cg_local_map(A: SellMatrix, rows_per_cta: int, n_cta: int):
                 nbr_ptr=nbr_ptr)
 
 
-def compress_columns(A: SellMatrix) -> dict:
-    """Column-compressed copy of A's SELL-32 columns (ab_sell16: 16-bit
-    offsets from a per-slice base where the slice's columns span < 64k rows,
-    int32 elsewhere); values and slice pointers are shared with A."""
-    s = stream_handle()
-    dev = A.vals.device
-    ns = A.slice_ptr.numel() - 1
-    cbase = torch.empty(max(1, ns), dtype=torch.int32, device=dev)
-    nbytes = torch.zeros(max(1, ns), dtype=torch.int64, device=dev)
-    call("ab_sell16_plan", ctypes.byref(A.struct), ptr(cbase), ptr(nbytes), s)
-    cptr = torch.zeros(ns + 1, dtype=torch.int64, device=dev)
-    cptr[1:] = torch.cumsum(nbytes[:ns], 0)
-    total = int(cptr[-1].item())
-    cols = torch.zeros(total + 64, dtype=torch.uint8, device=dev)
-    call("ab_sell16_fill", ctypes.byref(A.struct), ptr(cbase), ptr(cptr), ptr(cols), s)
-    struct = AbSell16(n_rows=A.n_rows, n_slices=ns, slice_ptr=ptr(A.slice_ptr), cptr=ptr(cptr), cbase=ptr(cbase),
-                      cols=ptr(cols), vals=ptr(A.vals))
-    near = float((cbase[:ns] >= 0).float().mean().item()) if ns else 1.0
-    return dict(cptr=cptr, cbase=cbase, cols=cols, struct=struct, near_fraction=near, col_bytes=total)
-
-
 def assemble_laplacian(mesh, fixed: torch.Tensor | None = None) -> SellMatrix:
     """Assemble L (SPD after Dirichlet rows/cols of ``fixed`` -> identity)."""
     dm = mesh if isinstance(mesh, DeviceMesh) else DeviceMesh(mesh)
@@ -261,7 +240,7 @@ class PCG:
     def __init__(self, A: SellMatrix, dinv: torch.Tensor, fixed: torch.Tensor | None = None,
                  own: torch.Tensor | None = None, halo=None, resident: bool = True,
                  order: torch.Tensor | None = None, prefetch_depth: int = 1, force_mode: int = 0,
-                 reorder_two_kernel: bool = True, compress_cols: bool = False, scaled: bool = True,
+                 reorder_two_kernel: bool = True, scaled: bool = True,
                  unit_diag: bool | None = None, tile_rows: int = 2048, single_pass: bool = True):
         self.A = A
         n = A.n_rows
@@ -318,7 +297,7 @@ class PCG:
         if not self.resident and halo is None and order is not None and reorder_two_kernel:
             pl = order.to(device=dev, dtype=torch.int64).contiguous()
             # scaled form: every diagonal entry of D^-1/2 A D^-1/2 is 1, so it is not stored
-            unit = bool(scaled and not compress_cols) if unit_diag is None else bool(unit_diag and scaled)
+            unit = bool(scaled) if unit_diag is None else bool(unit_diag and scaled)
             self.perm2 = dict(A=permute_matrix(A, pl, drop_diag=unit), perm=pl,
                               dinv=dinv[pl].contiguous(),
                               fixed=self.fixed[pl].contiguous() if self.fixed is not None else None,
@@ -330,9 +309,6 @@ class PCG:
                 self.perm2["iperm"][pl] = torch.arange(n, device=dev)
                 self.perm2["d"] = (1.0 / self.perm2["dinv"]).contiguous()
                 call("ab_sell_symscale", ctypes.byref(self.perm2["A"].struct), ptr(self.perm2["s"]), stream_handle())
-            # optional 16-bit columns in the slices whose columns span < 64k
-            # rows: 7% fewer matrix bytes, but measured slower
-            self.perm2["A16"] = compress_columns(self.perm2["A"]) if compress_cols else None
             # tiled SpMV (ab_cg_spmv_tile): z of a tile's rows and ghost rows in
             # shared memory, 16-bit tile-local columns
             if os.environ.get("AB_CG_TILE") is not None:  # lab switch
@@ -444,9 +420,6 @@ class PCG:
                 elif pm["unit"]:
                     call("ab_cg_spmv_unit", A, ptr(zvec), ptr(self.p), ptr(self.q), ptr(self.red), ptr(self.sc),
                          ptr(self.part), ptr(self.cnt), s)
-                elif pm["A16"] is not None:
-                    call("ab_cg_spmv16", ctypes.byref(pm["A16"]["struct"]), ptr(zvec), ptr(self.p), ptr(self.q),
-                         ptr(self.red), ptr(self.sc), ptr(self.part), ptr(self.cnt), s)
                 else:
                     call("ab_cg_spmv", A, ptr(zvec), ptr(self.p), ptr(self.q), None, 1, None, ptr(self.red),
                          ptr(self.sc), ptr(self.part), ptr(self.cnt), s)

@@ -147,7 +147,7 @@ CG_VARIANTS = {
     "two-kernel-sfc": dict(order=True, resident=False, tile_rows=0),  # two kernels on D^-1/2 P A P^T D^-1/2 (SFC)
     "two-kernel-sfc-tile": dict(order=True, resident=False, tile_rows=64),  # tiled SpMV, z in shared memory
     "two-kernel-sfc-single": dict(order=True, resident=False, tile_rows=1024),  # tiled single pass (default form)
-    "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False, compress_cols=False),  # z = D^-1 r form
+    "two-kernel-sfc-jacobi": dict(order=True, resident=False, scaled=False),  # z = D^-1 r form
     "two-kernel-sfc-diag": dict(order=True, resident=False, unit_diag=False),  # scaled, diagonal stored
 }
 

@@ -242,26 +242,3 @@ def test_chunked_setup_paths_equal_unchunked():
         assert torch.equal(ca, cb)
 
 
-def test_column_compressed_spmv_is_bitwise_equal(c2):
-    """The two-kernel CG on the column-compressed SELL (ab_cg_spmv16: 16-bit
-    column offsets in the slices spanning < 64k rows) gives bit-identical
-    iterates to the int32-column SELL on the full C2 system."""
-    from paper_2005_05899_b200.device import DeviceMesh
-    from paper_2005_05899_b200.solver import PCG, assemble_laplacian
-    m, _u, _p, fixed = c2
-    b = np.random.default_rng(9).standard_normal(m.n_nodes)
-    b[fixed] = 0.0
-    dm = DeviceMesh(m)
-    A = assemble_laplacian(dm, torch.from_numpy(fixed))
-    xs = []
-    for comp in (True, False):
-        pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), order=dm.node_order(), resident=False,
-                  compress_cols=comp, unit_diag=False)  # (the option is off by default: measured slower)
-        assert (pcg.perm2["A16"] is not None) == comp
-        x, _ = pcg.solve(torch.from_numpy(b).cuda(), 12, zero_b=False)
-        xs.append(x.clone())
-        if comp:
-            info = pcg.perm2["A16"]
-            assert info["near_fraction"] > 0.5
-            assert info["col_bytes"] < 4 * pcg.perm2["A"].nnz_stored * 0.8
-    assert torch.equal(xs[0], xs[1])

@@ -3,6 +3,9 @@ int32 vs 16-bit columns, Jacobi z-form vs the symmetrically scaled form.
 Graph-replayed 50-iteration solves, L2 flushed before each, device time.
 
     python tools/lab/time_spmv16.py [scale] [variant,variant,...]
+
+The 16-bit variants need the column-compressed SELL of tools/lab/cg_sell16.cu
+built back into the library (it left the product in round 2).
 """
 import sys
 from pathlib import Path
