@@ -250,7 +250,11 @@ class FlowSolver:
                     solver.timeline.append((name, self_inner.a, b))
         return _M()
 
-    def _step_body(self, dt: float, cg_iters: int, cg_tol: float):
+    def _step_body(self, dt: float, cg_iters: int, cg_tol: float, before_k3=None, after_cg=None):
+        """One fractional step on the current stream.  Hooks (end-to-end
+        overlap, step_host): ``before_k3()`` runs after the first stage's
+        right-hand side (K2, K8) and before its K3 (the first use of G p^n);
+        ``after_cg(x)`` runs after the pressure solve, before K6 + K7."""
         s = stream_handle()
         dm = self.dm
         rho = self.params.rho
@@ -265,6 +269,8 @@ class FlowSolver:
             if self.halo is not None:
                 with self._mark("X_halo_sum"):
                     self.halo.sum_(self.R, 3, 4)
+            if st == 0 and before_k3 is not None:
+                before_k3()
             with self._mark("K3_rk_stage"):
                 call("ab_rk_stage", self.n, RK3_A[st], RK3_B[st], k, ptr(self.U0), ptr(uin), ptr(self.R),
                      ptr(self.GP), ptr(self.minv), ptr(self.U), s)
@@ -284,6 +290,8 @@ class FlowSolver:
         else:
             x, it = self.pcg.solve(self.B, cg_iters, tol=cg_tol)
         self.last_cg_iters = it
+        if after_cg is not None:
+            after_cg(x)
         if self.Bop is not None and self.halo is None:
             # K6 + K7 fused: u = u_3 - dt/rho M^-1 B dp; p += dp; Gp += B dp
             with self._mark("K67_grad_correct"):
@@ -301,14 +309,23 @@ class FlowSolver:
         self._bc(self.U0)
 
     def step_host(self, u_host: torch.Tensor, p_host: torch.Tensor, dt: float, cg_iters: int = 50,
-                  graph: bool = True):
+                  graph: bool = True, overlap: bool = True):
         """End-to-end call with HOST buffers (pinned for async copies): upload
-        (u, p), advance one step, download (u, p) in place.  p goes first and
-        G p^n is assembled on a side stream while u is still uploading.
-        Returns after the download has completed (u_host, p_host are valid)."""
+        (u, p), advance one step, download (u, p) in place.  Returns after the
+        downloads have completed (u_host, p_host are valid).
+
+        Single domain (``overlap``): u goes up first and the step starts as
+        soon as it is there; p's upload and G p^n run on a side stream under
+        the first momentum assembly, and p^{n+1} = p^n + dp is formed and
+        downloaded on the side stream while K6 + K7 run (the step is then
+        launched eagerly: the hooks sit inside it).  Otherwise: p first, G p^n
+        on a side stream while u uploads, then the (graph) step."""
         main = torch.cuda.current_stream()
         if self._side is None:
             self._side = torch.cuda.Stream()
+        if overlap and self.halo is None:
+            self._step_host_overlap(u_host, p_host, dt, cg_iters, main)
+            return
         self.P.copy_(p_host, non_blocking=True)
         self._side.wait_stream(main)
         with torch.cuda.stream(self._side):
@@ -322,6 +339,40 @@ class FlowSolver:
         u_host.copy_(self.U0[:, :3], non_blocking=True)
         p_host.copy_(self.P, non_blocking=True)
         # the host buffers are read by the caller on return
+        main.synchronize()
+        self.check_health()
+
+    def _step_host_overlap(self, u_host, p_host, dt, cg_iters, main):
+        side = self._side
+        self.U0[:, :3].copy_(u_host, non_blocking=True)  # the first kernel's input: up first
+        side.wait_stream(main)  # (previous step's work on the device buffers is ordered before)
+        ev_gp = torch.cuda.Event()
+        with torch.cuda.stream(side):
+            self.P.copy_(p_host, non_blocking=True)
+            self.GP.zero_()
+            self._grad(self.P, self.GP)
+            ev_gp.record(side)
+        if getattr(self, "_P_next", None) is None or self._P_next.shape != self.P.shape:
+            self._P_next = torch.empty_like(self.P)
+
+        def before_k3():
+            main.wait_event(ev_gp)
+
+        def after_cg(x):
+            ev_x = torch.cuda.Event()
+            ev_x.record(main)
+            ev_read = torch.cuda.Event()
+            with torch.cuda.stream(side):
+                side.wait_event(ev_x)
+                torch.add(self.P, x, out=self._P_next)  # = K7's p + dp, bitwise
+                ev_read.record(side)
+                p_host.copy_(self._P_next, non_blocking=True)
+            main.wait_event(ev_read)  # K6 + K7 update P in place after the side stream read it
+
+        self._step_body(dt, cg_iters, 0.0, before_k3=before_k3, after_cg=after_cg)
+        self.last_cg_iters = cg_iters
+        u_host.copy_(self.U0[:, :3], non_blocking=True)
+        main.wait_stream(side)
         main.synchronize()
         self.check_health()
 

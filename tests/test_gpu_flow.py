@@ -302,12 +302,13 @@ def test_halo_pack_unpack_kernels():
     assert np.allclose(ft.cpu().numpy(), want, rtol=0, atol=1e-15)
 
 
-@pytest.mark.parametrize("graph", [False, True])
-def test_step_host_matches_oracle(graph):
-    """The end-to-end entry point (pinned host u, p in; step; host u, p out;
-    G p^n assembled on a side stream while u uploads) against the oracle over
-    3 steps, with the host state perturbed between steps so the uploaded p
-    differs from the device's."""
+@pytest.mark.parametrize("graph,overlap", [(False, False), (True, False), (False, True)])
+def test_step_host_matches_oracle(graph, overlap):
+    """The end-to-end entry point (pinned host u, p in; step; host u, p out)
+    against the oracle over 3 steps, with the host state perturbed between
+    steps so the uploaded p differs from the device's.  overlap: p's upload +
+    G p^n under the first momentum assembly and p^{n+1}'s download under
+    K6 + K7 (side stream); otherwise G p^n while u uploads, then the step."""
     from paper_2005_05899_b200.timestep import FlowParams, FlowSolver
     m = meshgen.box_tets(7, 6, 5, jitter=0.2, seed=5)
     u, p = _field(m, seed=4)
@@ -321,7 +322,7 @@ def test_step_host_matches_oracle(graph):
     for k in range(3):
         st = ora.init_state(u_h.numpy().copy(), p_h.numpy().copy())
         st = ora.step(st, 1e-3, cg_iters=30)
-        fs.step_host(u_h, p_h, 1e-3, cg_iters=30, graph=graph)
+        fs.step_host(u_h, p_h, 1e-3, cg_iters=30, graph=graph, overlap=overlap)
         torch.cuda.synchronize()
         assert rel_l2(u_h.numpy(), st["u"]) <= TOL_STATE, k
         assert rel_l2(p_h.numpy(), st["p"]) <= TOL_STATE, k
