@@ -67,7 +67,7 @@ def test_empty_mesh_packs():
 
 
 @pytest.mark.parametrize("cells", [(1, 1, 1), (3, 2, 5), (2, 7, 3)])
-@pytest.mark.parametrize("variant", ["local", "local-node-order", "two-kernel"])
+@pytest.mark.parametrize("variant", ["local", "local-node-order", "two-kernel", "tiled-single", "tiled-64"])
 def test_ragged_small_systems(cells, variant):
     """Row counts below 148 CTAs / not a multiple of the slice height."""
     from paper_2005_05899_b200.device import DeviceMesh
@@ -84,14 +84,22 @@ def test_ragged_small_systems(cells, variant):
     b[fixed] = 0.0
     dm = DeviceMesh(m)
     A = assemble_laplacian(dm, torch.from_numpy(fixed))
-    kw = {"local": dict(order=dm.node_order()), "local-node-order": dict(), "two-kernel": dict(resident=False)}
+    kw = {"local": dict(order=dm.node_order()), "local-node-order": dict(), "two-kernel": dict(resident=False),
+          # tiled single pass (one 2048-row tile, partial slices) / tiled SpMV with 64-row tiles
+          "tiled-single": dict(order=dm.node_order(), resident=False),
+          "tiled-64": dict(order=dm.node_order(), resident=False, tile_rows=64)}
     pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), **kw[variant])
+    if variant.startswith("tiled"):
+        assert pcg.perm2["tile"] is not None and pcg.perm2["single"] == (variant == "tiled-single")
     x, it = pcg.solve(torch.from_numpy(b).cuda(), 5, zero_b=False)
     xr, _, _ = fem.pcg(L, b, 1.0 / L.diagonal(), 5)
     assert rel_l2(x.cpu().numpy(), xr) <= 1e-10
+    # no iterations: x = 0
+    x0, it0 = pcg.solve(torch.from_numpy(b).cuda(), 0, zero_b=False)
+    assert it0 == 0 and float(x0.abs().max()) == 0.0
 
 
-@pytest.mark.parametrize("variant", ["local", "two-kernel"])
+@pytest.mark.parametrize("variant", ["local", "two-kernel", "tiled-single"])
 def test_zero_rhs_converges_immediately(variant):
     from paper_2005_05899_b200.device import DeviceMesh
     from paper_2005_05899_b200.solver import PCG, assemble_laplacian
@@ -99,7 +107,8 @@ def test_zero_rhs_converges_immediately(variant):
     fixed = meshgen.boundary_nodes(m)
     dm = DeviceMesh(m)
     A = assemble_laplacian(dm, torch.from_numpy(fixed))
-    kw = dict(order=dm.node_order()) if variant == "local" else dict(resident=False)
+    kw = {"local": dict(order=dm.node_order()), "two-kernel": dict(resident=False),
+          "tiled-single": dict(order=dm.node_order(), resident=False)}[variant]
     pcg = PCG(A, 1.0 / A.diag, fixed=torch.from_numpy(fixed), **kw)
     x, it = pcg.solve(torch.zeros(m.n_nodes, dtype=torch.float64, device="cuda"), 100, tol=1e-10)
     assert it == 0 and float(x.abs().max()) == 0.0
