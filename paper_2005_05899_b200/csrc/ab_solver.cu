@@ -1,10 +1,14 @@
 // Pressure-Poisson Jacobi-PCG on a
 // sliced-ELL (SELL-32) matrix: one thread per row, slice = warp, column
 // index and value arrays lane-innermost so every warp load is one 128/256 B
-// transaction.  Per iteration two fused kernels:
-//   spmv:   p_new = z + beta p_old (evaluated at gather time), q = A p_new,
-//           p.q partial sums;
-//   update: x += alpha p, r -= alpha q, z = D^-1 r, r.z and r.r partials.
+// transaction.  Forms:
+//   resident: the whole solve in one cooperative kernel (k_cg_resident_local,
+//     systems that fit on chip);
+//   tiled single pass (default for larger systems): one kernel per iteration
+//     on 2048-row tiles staged in shared memory (k_cg_tile_iter);
+//   two kernels per iteration (options and the decomposed NCCL path):
+//     spmv:   p_new = z + beta p_old, q = A p_new, p.q partial sums;
+//     update: x += alpha p, r -= alpha q, z = D^-1 r, r.z and r.r partials.
 // Scalars (alpha, beta) are formed on the device from the reduction slots,
 // so the loop never synchronises with the host.
 #include "ab_cg_common.cuh"

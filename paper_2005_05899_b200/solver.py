@@ -6,10 +6,13 @@ The Laplacian L_ab = sum_e int grad N_a . grad N_b is assembled once
 (Algorithm 1 line 1): the CSR pattern comes from a GPU sort of
 the element (row, col) pairs, values from ``ab_laplacian_csr``, Dirichlet rows
 and columns become identity (``ab_csr_dirichlet``), and the matrix is stored
-as SELL-32 for the solver (``ab_csr_to_sell``).  The CG loop (PAPER.md:219,
-:329-330) is two fused kernels per iteration with all scalars on the device
-(``ab_cg_spmv`` + ``ab_cg_update``); in a decomposed domain the SpMV result
-is interface-summed and the dots all-reduced between them (DESIGN.md §4.3/§5).
+as SELL-32 for the solver (``ab_csr_to_sell``).  The CG (PAPER.md:219,
+:329-330) keeps all scalars on the device: one cooperative kernel per solve
+when the system fits on chip (``ab_cg_resident_local``), else the tiled
+single pass on the symmetrically scaled, SFC-ordered system (one
+``ab_cg_tile_iter`` per iteration), with the two-kernel forms as options; in
+a decomposed domain driven over NCCL the SpMV result is interface-summed and
+the dots all-reduced between the kernels (DESIGN.md §4/§5).
 """
 
 from __future__ import annotations
