@@ -339,6 +339,18 @@ struct ab_ctx {
     mem.push_back(q);
     return reinterpret_cast<T*>(q);
   }
+  // release a setup temporary early (stream-ordered: after the work queued so far)
+  void release(void* q) {
+    if (!q) return;
+    for (size_t i = 0; i < mem.size(); ++i)
+      if (mem[i] == q) {
+        cudaStreamSynchronize(st);
+        cudaFree(q);
+        mem[i] = mem.back();
+        mem.pop_back();
+        return;
+      }
+  }
   ~ab_ctx() {
     for (int k = 0; k < 5; ++k)
       if (conn[k]) {
@@ -468,8 +480,14 @@ int build_tiled_cg(ab_ctx* c, int64_t n, const int64_t* rp, const int32_t* cols,
   cudaStreamSynchronize(c->st);
   int64_t max_ghost = 0;
   for (int64_t t = 0; t < n_t; ++t) max_ghost = hp[t + 1] - hp[t] > max_ghost ? hp[t + 1] - hp[t] : max_ghost;
-  if (R + max_ghost > 65536) return check_launch("ab_mesh_upload");  // stays on the plain two-kernel form
+  if (R + max_ghost > 65536) {  // stays on the plain two-kernel form
+    for (void* q : {(void*)cnt, (void*)cols2, (void*)v2, (void*)key, (void*)gk, (void*)gtile, (void*)gptr64})
+      c->release(q);
+    return check_launch("ab_mesh_upload");
+  }
   k_tile_ghost_cols<<<g256(n), 256, 0, c->st>>>(n, R, sp, key, gk, ng, gptr, lcol);
+  // setup temporaries (the CSR copy went into the SELL; keys and ghost tiles are consumed)
+  for (void* q : {(void*)cnt, (void*)cols2, (void*)v2, (void*)key, (void*)gk, (void*)gtile, (void*)gptr64}) c->release(q);
   c->tmap = ab_cg_local{};
   c->tmap.rows_per_cta = R;
   c->tmap.n_cta = (int32_t)n_t;
